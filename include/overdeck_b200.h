@@ -1,0 +1,252 @@
+/*
+ * overdeck_b200.h -- C ABI of the B200-native BRAMS-like column-update path
+ * with Charm++/AMPI-style over-decomposition and dynamic load balancing.
+ *
+ * Every entry point here replaces one symbol of the reference simulator
+ * `overdeck` (headers under /root/reference/proj/include/overdeck/).  The reference is
+ * a header-only C++20 library whose API is free functions and value types;
+ * the cited file:line is the symbol a binding for this path would call.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; the caller owns every buffer.
+ *  - Return code: OD_OK (0), OD_EVALIDATION (2) for the reference's
+ *    ValidationError, OD_ERUNTIME (3) for RuntimeFault and any CUDA/NCCL
+ *    failure.  These are the CLI exit codes of tools/main.cpp:17-19.
+ *    Nothing throws across this boundary; od_last_error() returns the
+ *    message of the last failing call on the calling thread.
+ *  - Enumerations keep the reference's declaration order:
+ *      LaunchMode  Sync=0 Async=1            (gpu_cost.hpp:15)
+ *      Strategy    Greedy=0 RefineSwap=1     (cluster.hpp:69)
+ *      VpClass     Heavy=0 Light=1           (cluster.hpp:47)
+ *      LoadPattern Uniform=0 StaticNode0=1 UpperHalfHeavy=2 (workload.hpp:141)
+ *      DecompositionKind OneD=0 TwoD=1       (engine.hpp:18)
+ *  - The pure functions (workload, cluster, measurement, balancer) are
+ *    reentrant.  An od_runtime handle is driven by one host thread.
+ */
+#ifndef OVERDECK_B200_H
+#define OVERDECK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { OD_OK = 0, OD_EVALIDATION = 2, OD_ERUNTIME = 3 };
+enum { OD_SYNC = 0, OD_ASYNC = 1 };
+enum { OD_GREEDY = 0, OD_REFINE_SWAP = 1 };
+enum { OD_HEAVY = 0, OD_LIGHT = 1 };
+enum { OD_UNIFORM = 0, OD_STATIC_NODE0 = 1, OD_UPPER_HALF_HEAVY = 2 };
+enum { OD_ONE_D = 0, OD_TWO_D = 1 };
+/* per-chunk load measurement in Sync steps */
+enum {
+  OD_MEASURE_EVENTS = 0, /* paper protocol: one launch per chunk, cudaEvent pair */
+  OD_MEASURE_TIMER = 1   /* batched launch, in-kernel per-chunk SM-time accumulation */
+};
+
+/* Move{vp, from, to}                                   cluster.hpp:62-67 */
+typedef struct od_move {
+  int32_t vp, from, to;
+} od_move;
+
+/* SubDomain: half-open column ranges, shared-face count workload.hpp:29-38 */
+typedef struct od_subdomain {
+  int32_t owner_vp, x_begin, x_end, y_begin, y_end;
+  int64_t boundary_cells;
+} od_subdomain;
+
+/* StepSample{vp, step (0-based in epoch), mode, seconds} measurement.hpp:14-19 */
+typedef struct od_sample {
+  int32_t vp, step, mode, pad_;
+  double value;
+} od_sample;
+
+/* KernelWork{work_items, serial_depth}                   workload.hpp:75-80 */
+typedef struct od_kernel_work {
+  double work_items, serial_depth;
+} od_kernel_work;
+
+const char* od_last_error(void);
+int32_t od_abi_version(void);
+
+/* ---------------------------------------------------------------- workload */
+/* decompose_1d                                        workload.hpp:100-114 */
+int od_decompose_1d(int32_t nx, int32_t ny, int32_t k, od_subdomain* out /* k */);
+/* decompose_2d                                        workload.hpp:117-139 */
+int od_decompose_2d(int32_t nx, int32_t ny, int32_t kx, int32_t ky,
+                    od_subdomain* out /* kx*ky */);
+/* init_load_field; out is y-major c[y*nx+x]           workload.hpp:160-181 */
+int od_init_load_field(int32_t nx, int32_t ny, int32_t pattern, double heavy_value,
+                       double light_value, const od_subdomain* node0_subs,
+                       int32_t n_node0, double* out /* nx*ny */);
+/* advect_load_field                                   workload.hpp:185-195 */
+int od_advect_load_field(const double* c, int32_t nx, int32_t ny, int32_t shift_rows,
+                         double* out /* nx*ny */);
+/* LoadField::mean_over                                  workload.hpp:58-64 */
+int od_mean_over(const double* c, int32_t nx, int32_t ny, const od_subdomain* sub,
+                 double* out);
+/* physics_work                                        workload.hpp:199-204 */
+int od_physics_work(const od_subdomain* sub, const double* c, int32_t nx, int32_t ny,
+                    int32_t mzp, od_kernel_work* out);
+/* jacobi_work                                         workload.hpp:207-210 */
+int od_jacobi_work(const od_subdomain* sub, int32_t nz, int32_t fields,
+                   od_kernel_work* out);
+/* halo_bytes / subdomain_bytes (8-byte values)        workload.hpp:213-220 */
+int od_halo_bytes(const od_subdomain* sub, int32_t nz, int32_t fields, int64_t* out);
+int od_subdomain_bytes(const od_subdomain* sub, int32_t nz, int32_t fields, int64_t* out);
+
+/* ----------------------------------------------------------------- cluster */
+/* initial_block_mapping                               cluster.hpp:115-127 */
+int od_initial_block_mapping(int32_t vp_count, int32_t proc_count, int32_t* map /* K */);
+/* apply_plan: all-or-nothing; map_out untouched on error cluster.hpp:130-139 */
+int od_apply_plan(const int32_t* map_in, int32_t vp_count, int32_t proc_count,
+                  const od_move* moves, int32_t n_moves, int32_t* map_out /* K */);
+/* proc_loads                                          cluster.hpp:142-148 */
+int od_proc_loads(const double* loads, int32_t n_loads, const int32_t* map,
+                  int32_t vp_count, int32_t proc_count, double* totals /* P */);
+/* imbalance_ratio                                     cluster.hpp:151-157 */
+int od_imbalance_ratio(const double* totals, int32_t n, double* out);
+
+/* ---------------------------------------------------------------- balancer */
+/* should_balance                                       balancer.hpp:29-32 */
+int od_should_balance(const double* totals, int32_t n, double trigger_threshold,
+                      int32_t* out);
+/* greedy_lb; moves in ascending vp order; cap >= K     balancer.hpp:36-63 */
+int od_greedy_lb(const double* loads, int32_t n_loads, const int32_t* map,
+                 int32_t vp_count, int32_t proc_count, od_move* out, int32_t cap,
+                 int32_t* n_out);
+/* refine_swap_lb; a swap is two moves; cap >= 2*K*P   balancer.hpp:68-152 */
+int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
+                      int32_t vp_count, int32_t proc_count, double tolerance,
+                      od_move* out, int32_t cap, int32_t* n_out);
+
+/* ------------------------------------------------------------- measurement */
+/* LoadDB                                             measurement.hpp:40-70 */
+typedef struct od_loaddb od_loaddb;
+int od_loaddb_create(int32_t vp_count, int32_t async_steps, int32_t sync_steps,
+                     od_loaddb** out);
+int od_loaddb_record(od_loaddb* db, const od_sample* sample);
+int od_loaddb_clear(od_loaddb* db);
+int od_loaddb_size(const od_loaddb* db, int32_t* n);
+/* epoch_loads: mean of Sync samples only             measurement.hpp:75-91 */
+int od_loaddb_epoch_loads(const od_loaddb* db, double* out /* K */);
+void od_loaddb_destroy(od_loaddb* db);
+
+/* ----------------------------------------------------------------- runtime */
+/*
+ * ExperimentConfig (engine.hpp:43-83) restricted to what the B200 path uses.
+ * Cluster mapping: one node per GPU (one rank per GPU, world == nodes);
+ * procs_per_node processors share a node's GPU exactly as the reference's
+ * ClusterSpec (cluster.hpp:18-32).  GpuModel/CpuModel are not present: the
+ * B200 path measures instead of modelling.
+ */
+typedef struct od_config {
+  int32_t nodes, procs_per_node;
+  int32_t nx, ny, nz, fields;
+  int32_t decomposition_kind, kx, ky;
+  int32_t async_steps, sync_steps;
+  int32_t epochs;
+  int32_t pattern;
+  double heavy_value, light_value;
+  int32_t adv_total_shift_rows, adv_epoch, adv_duration_steps;
+  int32_t first_call_strategy, later_call_strategy;
+  double trigger_threshold, refine_tolerance;
+  uint64_t seed;
+  /* B200 path parameters (no reference counterpart) */
+  int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
+  int32_t measure;      /* OD_MEASURE_EVENTS | OD_MEASURE_TIMER */
+  int32_t overlap;      /* 1: physics and Jacobi run concurrently in async steps */
+  int32_t reserved_[5];
+} od_config;
+
+/* EpochRecord (engine.hpp:85-97); arrays are caller-allocated */
+typedef struct od_epoch_record {
+  int32_t epoch;
+  int32_t n_steps;           /* out */
+  double* step_times;        /* in: cap >= epoch_steps; seconds, max over ranks */
+  double compute_total;      /* out: sum of step_times */
+  int32_t strategy;          /* out: OD_GREEDY / OD_REFINE_SWAP, -1 = no call */
+  int32_t n_moves;           /* out */
+  od_move* moves;            /* in: cap moves_cap */
+  int32_t moves_cap;
+  double migration_seconds;  /* out: measured device time of the chunk moves */
+  double imbalance_before, imbalance_after;
+  double* proc_loads;        /* in: P */
+  double* vp_loads;          /* in: K */
+  int32_t* mapping;          /* in: K, mapping active during the epoch */
+  int32_t* classes;          /* in: K */
+} od_epoch_record;
+
+typedef struct od_runtime od_runtime;
+
+/* NCCL unique id for multi-rank runtimes (rank 0 creates, caller broadcasts) */
+int od_nccl_unique_id(uint8_t* out /* 128 bytes */);
+/*
+ * Engine ctor (engine.hpp:135-157) on the local GPU `device`: decomposition,
+ * block mapping, load field, chunk allocation and seeded initial fields.
+ * world > 1 needs the NCCL id from od_nccl_unique_id on every rank.
+ */
+int od_rt_create(const od_config* cfg, int32_t rank, int32_t world, int32_t device,
+                 const uint8_t* nccl_id, od_runtime** out);
+void od_rt_destroy(od_runtime* rt);
+int od_rt_vp_count(const od_runtime* rt, int32_t* k);
+int od_rt_proc_count(const od_runtime* rt, int32_t* p);
+/* Engine::mapping                                        engine.hpp:163 */
+int od_rt_mapping(const od_runtime* rt, int32_t* map /* K */);
+/* Engine::subdomains                                     engine.hpp:161 */
+int od_rt_subdomains(const od_runtime* rt, od_subdomain* out /* K */);
+/* Engine::classify_vps                                 engine.hpp:281-287 */
+int od_rt_classify(const od_runtime* rt, int32_t* classes /* K */);
+/* Engine::load_field (current shifted field)            engine.hpp:165 */
+int od_rt_load_field(const od_runtime* rt, double* c /* nx*ny */);
+/*
+ * Engine::step_time (engine.hpp:183-233), executed for real: one timestep of
+ * halo exchange + Jacobi + physics over every resident chunk.  *wall is the
+ * step's device time (max over ranks); samples[v] for every VP (gathered).
+ */
+int od_rt_step(od_runtime* rt, int32_t mode, int32_t epoch_step, int32_t global_step,
+               double* wall, od_sample* samples /* K */);
+/* Engine::run_epoch (engine.hpp:235-272) with real chunk migration */
+int od_rt_run_epoch(od_runtime* rt, int32_t epoch_index, od_epoch_record* rec);
+/*
+ * Advance the epoch schedule by n timesteps (epoch boundaries perform
+ * measurement, balancing and migration).  Records of completed epochs are not
+ * returned; *epochs_done counts them.  Used by the benchmark.
+ */
+int od_rt_advance(od_runtime* rt, int32_t n_steps, int32_t* epochs_done);
+/*
+ * End-to-end variant of od_rt_advance for the host-facing path: every step
+ * copies the step's load multiplier field (nx*ny doubles, pinned host memory)
+ * H2D and the step's per-chunk device times (K doubles) D2H.
+ */
+int od_rt_advance_host(od_runtime* rt, int32_t n_steps, const double* host_c_fields,
+                       int32_t n_fields, double* host_step_loads /* n_steps*K */);
+/* apply_plan plus the data movement of every moved chunk  cluster.hpp:130 */
+int od_rt_migrate(od_runtime* rt, const od_move* moves, int32_t n_moves);
+/*
+ * Chunk state of VP vp if resident on this rank: u (fields*nz*h*w, layout
+ * [f][k][y][x]) and a (nz*h*w, [k][y][x]).  *resident = 0 when not local.
+ */
+int od_rt_read_chunk(od_runtime* rt, int32_t vp, double* u, double* a,
+                     int32_t* resident);
+/* Diagnostics for the benchmark / roofline. */
+typedef struct od_rt_stats {
+  int64_t kernel_launches;     /* kernels of this library launched so far */
+  int64_t steps;
+  double jacobi_ms, physics_ms, pack_ms, exchange_ms; /* cumulative event time */
+  int64_t jacobi_launches, physics_launches;
+  int64_t halo_bytes_sent;     /* cumulative cross-rank halo bytes */
+  int64_t migrated_bytes;      /* cumulative chunk bytes moved across ranks */
+  int64_t physics_trips;       /* sum of trips of resident columns, last step */
+  int32_t resident_chunks;
+  int32_t pad_;
+} od_rt_stats;
+int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
+/* enable per-kernel event timing (adds events around each batched kernel) */
+int od_rt_set_profiling(od_runtime* rt, int32_t on);
+int od_rt_synchronize(od_runtime* rt);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OVERDECK_B200_H */

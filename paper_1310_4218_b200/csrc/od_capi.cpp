@@ -1,0 +1,296 @@
+// extern "C" surface of include/overdeck_b200.h for the pure host model.
+// Exceptions never cross the boundary: ValidationError -> 2, RuntimeFault and
+// any other failure -> 3, message kept per thread for od_last_error().
+#include <cstring>
+#include <exception>
+#include <new>
+#include <string>
+
+#include "../../include/overdeck_b200.h"
+#include "od_capi_util.hpp"
+#include "od_model.hpp"
+
+namespace odb {
+thread_local std::string g_last_error;
+
+int fail_with(const std::exception& e, int code) {
+  g_last_error = e.what();
+  return code;
+}
+}  // namespace odb
+
+using namespace odb;
+
+namespace {
+
+Sub to_sub(const od_subdomain& s) {
+  Sub r;
+  r.vp = s.owner_vp;
+  r.x0 = s.x_begin;
+  r.x1 = s.x_end;
+  r.y0 = s.y_begin;
+  r.y1 = s.y_end;
+  r.boundary = s.boundary_cells;
+  return r;
+}
+
+void put_subs(const std::vector<Sub>& v, od_subdomain* out) {
+  for (size_t i = 0; i < v.size(); ++i)
+    out[i] = od_subdomain{v[i].vp, v[i].x0, v[i].x1, v[i].y0, v[i].y1, v[i].boundary};
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw ValidationError(std::string("null pointer: ") + what);
+}
+
+Field2D field_view(const double* c, int32_t nx, int32_t ny) {
+  check_domain(nx, ny, 1, 0);
+  need(c, "load field");
+  Field2D f;
+  f.nx = nx;
+  f.ny = ny;
+  f.c.assign(c, c + size_t(nx) * ny);
+  return f;
+}
+
+void check_sub_in(const od_subdomain* s, int32_t nx, int32_t ny) {
+  need(s, "subdomain");
+  if (s->x_begin < 0 || s->x_end > nx || s->x_begin > s->x_end || s->y_begin < 0 ||
+      s->y_end > ny || s->y_begin > s->y_end)
+    throw ValidationError("subdomain outside the load field");
+}
+
+std::vector<int32_t> map_view(const int32_t* map, int32_t K, int32_t P) {
+  if (K < 0) throw ValidationError("vp count must be >= 0");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  if (K > 0) need(map, "mapping");
+  std::vector<int32_t> m(map, map + K);
+  for (int32_t p : m)
+    if (p < 0 || p >= P) throw ValidationError("processor id out of range");
+  return m;
+}
+
+std::vector<double> vec_view(const double* a, int32_t n, const char* what) {
+  if (n < 0) throw ValidationError(std::string("negative length: ") + what);
+  if (n > 0) need(a, what);
+  return std::vector<double>(a, a + n);
+}
+
+int emit_moves(const std::vector<MoveRec>& plan, od_move* out, int32_t cap, int32_t* n_out) {
+  need(n_out, "n_out");
+  *n_out = int32_t(plan.size());
+  if (int32_t(plan.size()) > cap) throw ValidationError("move buffer too small");
+  if (!plan.empty()) need(out, "out");
+  for (size_t i = 0; i < plan.size(); ++i) out[i] = od_move{plan[i].vp, plan[i].from, plan[i].to};
+  return OD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* od_last_error(void) { return g_last_error.c_str(); }
+int32_t od_abi_version(void) { return 1; }
+
+int od_decompose_1d(int32_t nx, int32_t ny, int32_t k, od_subdomain* out) {
+  return guarded([&] {
+    auto s = strips_1d(nx, ny, k);
+    need(out, "out");
+    put_subs(s, out);
+  });
+}
+
+int od_decompose_2d(int32_t nx, int32_t ny, int32_t kx, int32_t ky, od_subdomain* out) {
+  return guarded([&] {
+    auto s = tiles_2d(nx, ny, kx, ky);
+    need(out, "out");
+    put_subs(s, out);
+  });
+}
+
+int od_init_load_field(int32_t nx, int32_t ny, int32_t pattern, double heavy_value,
+                       double light_value, const od_subdomain* node0_subs, int32_t n_node0,
+                       double* out) {
+  return guarded([&] {
+    if (pattern < OD_UNIFORM || pattern > OD_UPPER_HALF_HEAVY)
+      throw ValidationError("unknown load pattern");
+    std::vector<Sub> subs;
+    if (n_node0 > 0) need(node0_subs, "node0_subs");
+    for (int32_t i = 0; i < n_node0; ++i) {
+      check_sub_in(&node0_subs[i], nx, ny);
+      subs.push_back(to_sub(node0_subs[i]));
+    }
+    Field2D f = make_load_field(nx, ny, Pattern(pattern), heavy_value, light_value, subs);
+    need(out, "out");
+    std::memcpy(out, f.c.data(), f.c.size() * sizeof(double));
+  });
+}
+
+int od_advect_load_field(const double* c, int32_t nx, int32_t ny, int32_t shift_rows,
+                         double* out) {
+  return guarded([&] {
+    Field2D f = shift_rows_down(field_view(c, nx, ny), shift_rows);
+    need(out, "out");
+    std::memcpy(out, f.c.data(), f.c.size() * sizeof(double));
+  });
+}
+
+int od_mean_over(const double* c, int32_t nx, int32_t ny, const od_subdomain* sub,
+                 double* out) {
+  return guarded([&] {
+    check_sub_in(sub, nx, ny);
+    need(out, "out");
+    *out = field_view(c, nx, ny).mean_over(to_sub(*sub));
+  });
+}
+
+int od_physics_work(const od_subdomain* sub, const double* c, int32_t nx, int32_t ny,
+                    int32_t mzp, od_kernel_work* out) {
+  return guarded([&] {
+    check_sub_in(sub, nx, ny);
+    need(out, "out");
+    Work w = physics_trips(to_sub(*sub), field_view(c, nx, ny), mzp);
+    *out = od_kernel_work{w.items, w.depth};
+  });
+}
+
+int od_jacobi_work(const od_subdomain* sub, int32_t nz, int32_t fields, od_kernel_work* out) {
+  return guarded([&] {
+    need(sub, "subdomain");
+    need(out, "out");
+    Work w = jacobi_items(to_sub(*sub), nz, fields);
+    *out = od_kernel_work{w.items, w.depth};
+  });
+}
+
+int od_halo_bytes(const od_subdomain* sub, int32_t nz, int32_t fields, int64_t* out) {
+  return guarded([&] {
+    need(sub, "subdomain");
+    need(out, "out");
+    *out = halo_footprint(to_sub(*sub), nz, fields);
+  });
+}
+
+int od_subdomain_bytes(const od_subdomain* sub, int32_t nz, int32_t fields, int64_t* out) {
+  return guarded([&] {
+    need(sub, "subdomain");
+    need(out, "out");
+    *out = chunk_footprint(to_sub(*sub), nz, fields);
+  });
+}
+
+int od_initial_block_mapping(int32_t vp_count, int32_t proc_count, int32_t* map) {
+  return guarded([&] {
+    auto m = block_mapping(vp_count, proc_count);
+    if (vp_count > 0) need(map, "map");
+    std::memcpy(map, m.data(), m.size() * sizeof(int32_t));
+  });
+}
+
+int od_apply_plan(const int32_t* map_in, int32_t vp_count, int32_t proc_count,
+                  const od_move* moves, int32_t n_moves, int32_t* map_out) {
+  return guarded([&] {
+    auto m = map_view(map_in, vp_count, proc_count);
+    if (n_moves < 0) throw ValidationError("negative move count");
+    if (n_moves > 0) need(moves, "moves");
+    std::vector<MoveRec> mv(n_moves);
+    for (int32_t i = 0; i < n_moves; ++i) mv[i] = {moves[i].vp, moves[i].from, moves[i].to};
+    auto r = apply_moves(m, proc_count, mv);
+    if (vp_count > 0) need(map_out, "map_out");
+    std::memcpy(map_out, r.data(), r.size() * sizeof(int32_t));
+  });
+}
+
+int od_proc_loads(const double* loads, int32_t n_loads, const int32_t* map, int32_t vp_count,
+                  int32_t proc_count, double* totals) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    auto t = totals_per_proc(l, m, proc_count);
+    need(totals, "totals");
+    std::memcpy(totals, t.data(), t.size() * sizeof(double));
+  });
+}
+
+int od_imbalance_ratio(const double* totals, int32_t n, double* out) {
+  return guarded([&] {
+    auto t = vec_view(totals, n, "totals");
+    need(out, "out");
+    *out = max_over_mean(t);
+  });
+}
+
+int od_should_balance(const double* totals, int32_t n, double trigger_threshold, int32_t* out) {
+  return guarded([&] {
+    auto t = vec_view(totals, n, "totals");
+    need(out, "out");
+    *out = balance_needed(t, trigger_threshold) ? 1 : 0;
+  });
+}
+
+int od_greedy_lb(const double* loads, int32_t n_loads, const int32_t* map, int32_t vp_count,
+                 int32_t proc_count, od_move* out, int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    return emit_moves(plan_greedy(l, m, proc_count), out, cap, n_out);
+  });
+}
+
+int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
+                      int32_t vp_count, int32_t proc_count, double tolerance, od_move* out,
+                      int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    return emit_moves(plan_refine_swap(l, m, proc_count, tolerance), out, cap, n_out);
+  });
+}
+
+struct od_loaddb {
+  SampleStore store;
+};
+
+int od_loaddb_create(int32_t vp_count, int32_t async_steps, int32_t sync_steps,
+                     od_loaddb** out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = new od_loaddb{SampleStore(vp_count, async_steps, sync_steps)};
+  });
+}
+
+int od_loaddb_record(od_loaddb* db, const od_sample* s) {
+  return guarded([&] {
+    need(db, "db");
+    need(s, "sample");
+    db->store.add(s->vp, s->step, s->mode, s->value);
+  });
+}
+
+int od_loaddb_clear(od_loaddb* db) {
+  return guarded([&] {
+    need(db, "db");
+    db->store.reset();
+  });
+}
+
+int od_loaddb_size(const od_loaddb* db, int32_t* n) {
+  return guarded([&] {
+    need(db, "db");
+    need(n, "n");
+    *n = int32_t(db->store.size());
+  });
+}
+
+int od_loaddb_epoch_loads(const od_loaddb* db, double* out) {
+  return guarded([&] {
+    need(db, "db");
+    auto m = db->store.sync_means();
+    if (!m.empty()) need(out, "out");
+    std::memcpy(out, m.data(), m.size() * sizeof(double));
+  });
+}
+
+void od_loaddb_destroy(od_loaddb* db) { delete db; }
+
+}  // extern "C"

@@ -1,0 +1,306 @@
+// sm_100a kernels of the column-update path.
+//
+//  jacobi_step   3D 7-point Jacobi ("laminar diffusion") over all
+//                fields of all resident chunks in one launch (chunk-index
+//                table), k-marching with a cp.async plane ring.  HBM-bound.
+//  physics_step  the Fig. 4 column recurrence, one thread
+//                per column, trip count floor(nz*C)-1 from the (shifted) load
+//                multiplier field.  FP64-pipe-bound.
+//  pack_faces    boundary strips of chunks that border another rank into a
+//                contiguous per-peer send buffer (Fig. 2 "compute boundaries").
+//  init_chunk    seeded initial state, keyed by global coordinates.
+//
+// All arithmetic on field values uses explicit IEEE round-to-nearest
+// intrinsics so the results are bitwise equal to oracle/field_oracle.c.
+#pragma once
+
+#include <cstdint>
+
+namespace odb {
+
+// Jacobi weights: u' = W1*((xm+xp)+(ym+yp)+(zm+zp)) + W0*u, W0 + 6*W1 = 1.
+constexpr double kW0 = 0.25;
+constexpr double kW1 = 0.125;
+// physics map: y <- R*(y - y^2) + (b+1)/512 ; R = 4 - 1/64
+constexpr double kR = 3.984375;
+constexpr double kEps = 0.001953125;  // 2^-9
+
+enum Face : int32_t { kLeft = 0, kRight = 1, kTop = 2, kBottom = 3 };
+
+struct FaceDev {
+  const double* p;     // element (f=0, k=0, e=0) of the strip
+  int64_t fs, ks, es;  // strides (elements) for field, level, position along the face
+};
+
+struct ChunkDev {
+  const double* in;  // U^t, [F][nz][h][pitch]
+  double* out;       // U^{t+1}
+  double* a;         // physics state A, [nz][h][pitch]
+  int64_t fstride;   // nz * kstride
+  int64_t kstride;   // h * pitch
+  int32_t w, h, pitch, x0, y0, vp, pad0, pad1;
+  FaceDev face[4];
+};
+
+struct TileDev {
+  int32_t slot, tx0, ty0, pad;
+};
+
+struct PackJob {
+  int32_t slot, side, len, pad;  // side: which edge of the source chunk
+  int64_t dst;                   // element offset into the send buffer
+};
+
+__device__ __forceinline__ uint64_t dmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ double unit_hash(uint64_t seed, uint64_t idx) {
+  return double(dmix64(seed ^ dmix64(idx)) >> 11) * 0x1.0p-53;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// f(b, a) of Fig. 1 / Fig. 4: mix a and b, then n micro-steps of the
+// perturbed logistic map.  Every operation is a correctly rounded add/mul/fma.
+__device__ __forceinline__ double column_f(double b, double a, int n) {
+  const double hb = __dmul_rn(0.5, b);
+  const double eb = __fma_rn(b, kEps, kEps);
+  double y = __fma_rn(0.5, a, hb);
+#pragma unroll 8
+  for (int i = 0; i < n; ++i) {
+    const double u = __fma_rn(-y, y, y);
+    y = __fma_rn(kR, u, eb);
+  }
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi.  Grid (tiles, F); block (TX, TY).  A CTA marches its TX x TY column
+// tile through the nz levels of one field.  Plane k (tile + 1-cell halo) is
+// staged in smem slot k % R by cp.async, S planes ahead of the compute.
+// ---------------------------------------------------------------------------
+template <int TX, int TY, int S, bool TIMED>
+__global__ void __launch_bounds__(TX* TY)
+    jacobi_step(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                int32_t nz, unsigned long long* __restrict__ chunk_ns) {
+  constexpr int R = S + 2;
+  __shared__ __align__(16) double ring[R][TY + 2][TX + 2];
+
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const TileDev tile = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[tile.slot];
+  const int f = blockIdx.y;
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride;
+  const int wv = min(TX, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
+  const bool act = lx < wv && ly < hv;
+  const double* src = c.in + f * c.fstride;
+  double* dst = c.out + f * c.fstride;
+
+  // center element of this thread
+  const double* pc = src + int64_t(y) * pitch + x;
+  // x-halo duty (left by lane 0, right by lane TX-1) for rows inside the tile
+  const double* phx = nullptr;
+  int64_t hxk = 0;
+  int hx_col = 0;
+  if (ly < hv && (lx == 0 || lx == TX - 1)) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    hx_col = left ? 0 : wv + 1;
+    if (xs >= 0 && xs < w) {
+      phx = src + int64_t(y) * pitch + xs;
+      hxk = ks;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      phx = fd.p + f * fd.fs + int64_t(y) * fd.es;
+      hxk = fd.ks;
+    }
+  }
+  // y-halo duty (top by row 0, bottom by row TY-1) for columns inside the tile
+  const double* phy = nullptr;
+  int64_t hyk = 0;
+  int hy_row = 0;
+  if (lx < wv && (ly == 0 || ly == TY - 1)) {
+    const bool top = ly == 0;
+    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
+    hy_row = top ? 0 : hv + 1;
+    if (ys >= 0 && ys < h) {
+      phy = src + int64_t(ys) * pitch + x;
+      hyk = ks;
+    } else {
+      const FaceDev& fd = c.face[top ? kTop : kBottom];
+      phy = fd.p + f * fd.fs + int64_t(x) * fd.es;
+      hyk = fd.ks;
+    }
+  }
+
+  auto issue = [&](int k) {
+    if (k < nz) {
+      const int s = k % R;
+      if (act) cp_async8(&ring[s][ly + 1][lx + 1], pc + k * ks);
+      if (phx) cp_async8(&ring[s][ly + 1][hx_col], phx + k * hxk);
+      if (phy) cp_async8(&ring[s][hy_row][lx + 1], phy + k * hyk);
+    }
+    cp_async_commit();
+  };
+
+#pragma unroll
+  for (int k = 0; k < S; ++k) issue(k);
+
+  for (int k = 0; k < nz; ++k) {
+    cp_async_wait<S - 2>();  // planes <= k+1 have landed for this thread
+    __syncthreads();         // ... and for every thread; slot of plane k-2 is free
+    issue(k + S);
+    if (act) {
+      const int s0 = k % R;
+      const double uc = ring[s0][ly + 1][lx + 1];
+      const double xm = ring[s0][ly + 1][lx];
+      const double xp = ring[s0][ly + 1][lx + 2];
+      const double ym = ring[s0][ly][lx + 1];
+      const double yp = ring[s0][ly + 2][lx + 1];
+      const double zm = k > 0 ? ring[(k + R - 1) % R][ly + 1][lx + 1] : uc;
+      const double zp = k + 1 < nz ? ring[(k + 1) % R][ly + 1][lx + 1] : uc;
+      const double s =
+          __dadd_rn(__dadd_rn(__dadd_rn(xm, xp), __dadd_rn(ym, yp)), __dadd_rn(zm, zp));
+      const double v = __fma_rn(kW1, s, __dmul_rn(kW0, uc));
+      __stcs(dst + int64_t(y) * pitch + x + k * ks, v);
+    }
+  }
+  cp_async_wait<0>();
+
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Physics.  Grid (tiles); block (TX, TY); one thread per column.  B is field 0
+// of U^t (read-only this step, so the kernel is independent of jacobi_step).
+// ---------------------------------------------------------------------------
+template <int TX, int TY, bool TIMED, bool COUNT>
+__global__ void __launch_bounds__(TX* TY)
+    physics_step(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                 const double* __restrict__ cfield, int32_t nx, int32_t ny, int32_t shift,
+                 int32_t nz, int32_t n_inner, unsigned long long* __restrict__ chunk_ns,
+                 unsigned long long* __restrict__ trips) {
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const TileDev tile = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[tile.slot];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
+  int T = 0;
+  if (x < c.w && y < c.h) {
+    int row = c.y0 + y - shift;
+    if (row < 0) row += ny;
+    const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + x);
+    T = int(floor(__dmul_rn(double(nz), cm))) - 1;
+    if (T < 0) T = 0;
+    const int64_t ks = c.kstride;
+    const double* B = c.in + int64_t(y) * c.pitch + x;  // field 0
+    double* A = c.a + int64_t(y) * c.pitch + x;
+    double a = A[0];
+    int l = 0;
+    int ln = nz > 1 ? 1 : 0;
+    double bn = T >= 1 ? B[ln * ks] : 0.0;
+    for (int t = 1; t <= T; ++t) {
+      l = ln;
+      const double b = bn;
+      ln = l + 1 == nz ? 0 : l + 1;
+      if (t < T) bn = B[ln * ks];  // prefetch the next level
+      a = column_f(b, a, n_inner);
+      A[l * ks] = a;
+    }
+  }
+  if (COUNT) {
+    unsigned long long v = (unsigned long long)T;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&trips[tile.slot], v);
+  }
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Face packing: grid (jobs, F); the strip of one field, all levels.
+// Send layout per face: [f][k][e].
+// ---------------------------------------------------------------------------
+__global__ void pack_faces(const ChunkDev* __restrict__ chunks, const PackJob* __restrict__ jobs,
+                           double* __restrict__ sendbuf, int32_t nz) {
+  const PackJob j = jobs[blockIdx.x];
+  const ChunkDev& c = chunks[j.slot];
+  const int f = blockIdx.y;
+  const double* base = c.in + f * c.fstride;
+  int64_t off = 0, es = 1;
+  switch (j.side) {
+    case kLeft: off = 0; es = c.pitch; break;
+    case kRight: off = c.w - 1; es = c.pitch; break;
+    case kTop: off = 0; es = 1; break;
+    default: off = int64_t(c.h - 1) * c.pitch; es = 1; break;
+  }
+  double* out = sendbuf + j.dst + int64_t(f) * nz * j.len;
+  const int64_t n = int64_t(nz) * j.len;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t k = i / j.len, e = i - k * j.len;
+    out[i] = base[off + k * c.kstride + e * es];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Initial state: U[f][k][y][x] = H(seed, ((f*nz+k)*ny+gy)*nx+gx), A uses f = F.
+// Padding columns are zeroed.
+// ---------------------------------------------------------------------------
+__global__ void init_chunk(double* __restrict__ u, double* __restrict__ a, int32_t w, int32_t h,
+                           int32_t pitch, int32_t x0, int32_t y0, int32_t nx, int32_t ny,
+                           int32_t nz, int32_t F, uint64_t seed) {
+  const int64_t plane = int64_t(h) * pitch;
+  const int64_t total = plane * nz * (F + 1);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t fk = i / plane;
+    const int64_t r = i - fk * plane;
+    const int yy = int(r / pitch), xx = int(r - int64_t(yy) * pitch);
+    double v = 0.0;
+    if (xx < w) {
+      const uint64_t idx =
+          ((uint64_t(fk) * uint64_t(ny) + uint64_t(y0 + yy)) * uint64_t(nx)) + uint64_t(x0 + xx);
+      v = unit_hash(seed, idx);
+    }
+    if (fk < int64_t(F) * nz)
+      u[i] = v;
+    else
+      a[i - int64_t(F) * nz * plane] = v;
+  }
+}
+
+}  // namespace odb

@@ -1,0 +1,350 @@
+// Host model: see od_model.hpp.  Compiled with -ffp-contract=off so that no
+// multiply-add is fused differently from the reference build.
+#include "od_model.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace odb {
+
+// ---------------------------------------------------------------- workload --
+
+void check_domain(int32_t nx, int32_t ny, int32_t nz, int32_t fields) {
+  if (nx < 1 || ny < 1 || nz < 1 || fields < 0)
+    throw ValidationError("domain dimensions must be >= 1 (fields >= 0)");
+}
+
+std::vector<std::pair<int32_t, int32_t>> split_extent(int32_t extent, int32_t pieces) {
+  std::vector<std::pair<int32_t, int32_t>> r(pieces);
+  const int32_t q = extent / pieces, extra = extent % pieces;
+  int32_t lo = 0;
+  for (int32_t i = 0; i < pieces; ++i) {
+    const int32_t hi = lo + q + (i < extra);
+    r[i] = {lo, hi};
+    lo = hi;
+  }
+  return r;
+}
+
+std::vector<Sub> strips_1d(int32_t nx, int32_t ny, int32_t k) {
+  check_domain(nx, ny, 1, 0);
+  if (k < 1 || k > ny) throw ValidationError("1d decomposition: k must be in [1, ny]");
+  const auto rows = split_extent(ny, k);
+  std::vector<Sub> out(k);
+  for (int32_t i = 0; i < k; ++i) {
+    Sub& s = out[i];
+    s.vp = i;
+    s.x0 = 0;
+    s.x1 = nx;
+    s.y0 = rows[i].first;
+    s.y1 = rows[i].second;
+    s.boundary = int64_t((i > 0) + (i + 1 < k)) * nx;
+  }
+  return out;
+}
+
+std::vector<Sub> tiles_2d(int32_t nx, int32_t ny, int32_t kx, int32_t ky) {
+  check_domain(nx, ny, 1, 0);
+  if (kx < 1 || kx > nx || ky < 1 || ky > ny)
+    throw ValidationError("2d decomposition: tile counts exceed domain");
+  const auto cols = split_extent(nx, kx), rows = split_extent(ny, ky);
+  std::vector<Sub> out;
+  out.reserve(size_t(kx) * ky);
+  for (int32_t j = 0; j < ky; ++j)
+    for (int32_t i = 0; i < kx; ++i) {
+      Sub s;
+      s.vp = j * kx + i;
+      s.x0 = cols[i].first;
+      s.x1 = cols[i].second;
+      s.y0 = rows[j].first;
+      s.y1 = rows[j].second;
+      const int64_t w = s.x1 - s.x0, h = s.y1 - s.y0;
+      s.boundary = h * ((i > 0) + (i + 1 < kx)) + w * ((j > 0) + (j + 1 < ky));
+      out.push_back(s);
+    }
+  return out;
+}
+
+double Field2D::mean_over(const Sub& s) const {
+  double acc = 0;
+  for (int32_t y = s.y0; y < s.y1; ++y) {
+    const double* row = c.data() + size_t(y) * nx;
+    for (int32_t x = s.x0; x < s.x1; ++x) acc += row[x];
+  }
+  const int64_t n = s.cells();
+  return n > 0 ? acc / double(n) : 0.0;
+}
+
+Field2D make_load_field(int32_t nx, int32_t ny, Pattern p, double heavy, double light,
+                        const std::vector<Sub>& node0_subs) {
+  check_domain(nx, ny, 1, 0);
+  if (!(light >= 1.0) || !(heavy >= light))
+    throw ValidationError("load field requires heavy_value >= light_value >= 1");
+  Field2D f;
+  f.nx = nx;
+  f.ny = ny;
+  f.c.assign(size_t(nx) * ny, light);
+  if (p == kUpperHalfHeavy) {
+    std::fill(f.c.begin(), f.c.begin() + size_t(ny / 2) * nx, heavy);
+  } else if (p == kStaticNode0) {
+    for (const Sub& s : node0_subs)
+      for (int32_t y = s.y0; y < s.y1; ++y)
+        std::fill(f.c.begin() + size_t(y) * nx + s.x0, f.c.begin() + size_t(y) * nx + s.x1,
+                  heavy);
+  } else if (p != kUniform) {
+    throw ValidationError("unknown load pattern");
+  }
+  return f;
+}
+
+Field2D shift_rows_down(const Field2D& c, int32_t shift) {
+  if (shift < 0 || shift > c.ny) throw ValidationError("advection shift must be in [0, ny]");
+  if (shift == 0 || shift == c.ny) return c;
+  Field2D o;
+  o.nx = c.nx;
+  o.ny = c.ny;
+  o.c.resize(c.c.size());
+  // row y of the output is row (y - shift) mod ny of the input
+  const size_t row_bytes = size_t(c.nx);
+  for (int32_t y = 0; y < c.ny; ++y) {
+    const int32_t src = (y + c.ny - shift) % c.ny;
+    std::copy_n(c.c.begin() + size_t(src) * row_bytes, row_bytes,
+                o.c.begin() + size_t(y) * row_bytes);
+  }
+  return o;
+}
+
+Work physics_trips(const Sub& s, const Field2D& c, int32_t mzp) {
+  const int64_t n = s.cells();
+  if (n == 0) return {0, 0};
+  const double mc = c.mean_over(s);
+  return {double(n), mzp * mc - 1.0};
+}
+
+Work jacobi_items(const Sub& s, int32_t nz, int32_t fields) {
+  const double items = double(s.cells()) * nz * fields;
+  return {items, items > 0 ? 1.0 : 0.0};
+}
+
+int64_t halo_footprint(const Sub& s, int32_t nz, int32_t fields) {
+  return s.boundary * nz * fields * int64_t(8);
+}
+
+int64_t chunk_footprint(const Sub& s, int32_t nz, int32_t fields) {
+  return s.cells() * nz * fields * int64_t(8);
+}
+
+// ----------------------------------------------------------------- cluster --
+
+std::vector<int32_t> block_mapping(int32_t K, int32_t P) {
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  if (K < P) throw ValidationError("vp count must be >= proc count");
+  std::vector<int32_t> m(K);
+  const int32_t q = K / P, extra = K % P;
+  int32_t v = 0;
+  for (int32_t p = 0; p < P; ++p)
+    for (int32_t n = q + (p < extra); n > 0; --n) m[v++] = p;
+  return m;
+}
+
+std::vector<int32_t> apply_moves(const std::vector<int32_t>& map, int32_t P,
+                                 const std::vector<MoveRec>& moves) {
+  std::vector<int32_t> out = map;
+  const int32_t K = int32_t(map.size());
+  for (const MoveRec& m : moves) {
+    if (m.vp < 0 || m.vp >= K) throw ValidationError("move names an unknown vp");
+    if (out[m.vp] != m.from)
+      throw RuntimeFault("stale move: vp " + std::to_string(m.vp) + " is not on processor " +
+                         std::to_string(m.from));
+    if (m.to < 0 || m.to >= P) throw ValidationError("processor id out of range");
+    out[m.vp] = m.to;
+  }
+  return out;
+}
+
+std::vector<double> totals_per_proc(const std::vector<double>& loads,
+                                    const std::vector<int32_t>& map, int32_t P) {
+  if (loads.size() != map.size())
+    throw ValidationError("load vector length does not match vp count");
+  std::vector<double> t(P, 0.0);
+  for (size_t v = 0; v < map.size(); ++v) {
+    if (map[v] < 0 || map[v] >= P) throw ValidationError("processor id out of range");
+    t[map[v]] += loads[v];
+  }
+  return t;
+}
+
+double max_over_mean(const std::vector<double>& totals) {
+  if (totals.empty()) throw ValidationError("no processor totals");
+  double sum = 0.0, hi = totals[0];
+  for (double t : totals) sum += t;
+  if (sum <= 0.0) return 1.0;
+  for (double t : totals) hi = hi < t ? t : hi;
+  return hi / (sum / double(totals.size()));
+}
+
+// ---------------------------------------------------------------- balancer --
+
+bool balance_needed(const std::vector<double>& totals, double threshold) {
+  return max_over_mean(totals) > threshold;
+}
+
+std::vector<MoveRec> plan_greedy(const std::vector<double>& loads,
+                                 const std::vector<int32_t>& map, int32_t P) {
+  const int32_t K = int32_t(map.size());
+  if (int32_t(loads.size()) != K) throw ValidationError("greedy_lb: load vector length mismatch");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  // heaviest first; equal loads keep ascending vp order
+  std::vector<int32_t> order(K);
+  for (int32_t v = 0; v < K; ++v) order[v] = v;
+  std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return loads[a] > loads[b] || (!(loads[b] > loads[a]) && !(loads[a] > loads[b]) && a < b);
+  });
+  std::vector<double> bin(P, 0.0);
+  std::vector<int32_t> dest(K, 0);
+  for (int32_t v : order) {
+    // least-loaded processor, lowest id on ties
+    const int32_t p = int32_t(std::min_element(bin.begin(), bin.end()) - bin.begin());
+    dest[v] = p;
+    bin[p] += loads[v];
+  }
+  std::vector<MoveRec> plan;
+  for (int32_t v = 0; v < K; ++v)
+    if (dest[v] != map[v]) plan.push_back({v, map[v], dest[v]});
+  return plan;
+}
+
+namespace {
+inline double larger(double a, double b) { return a < b ? b : a; }
+}  // namespace
+
+std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
+                                      const std::vector<int32_t>& map, int32_t P,
+                                      double tol) {
+  const int32_t K = int32_t(map.size());
+  if (int32_t(loads.size()) != K)
+    throw ValidationError("refine_swap_lb: load vector length mismatch");
+  if (tol < 0) throw ValidationError("refine_swap_lb: tolerance must be >= 0");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+
+  std::vector<int32_t> where = map;
+  std::vector<double> acc = totals_per_proc(loads, where, P);
+  double sum = 0.0;
+  for (double a : acc) sum += a;
+  const double avg = sum / P;
+  const double ceil_load = avg * (1.0 + tol);
+
+  std::vector<MoveRec> plan;
+  std::vector<int32_t> donors, takers;
+  auto members = [&](int32_t p, std::vector<int32_t>& out) {
+    out.clear();
+    for (int32_t v = 0; v < K; ++v)
+      if (where[v] == p) out.push_back(v);
+  };
+
+  const int32_t max_rounds = K * P;
+  for (int32_t round = 0; round < max_rounds; ++round) {
+    int32_t hot = -1;
+    for (int32_t p = 0; p < P; ++p)
+      if (acc[p] > ceil_load && (hot < 0 || acc[p] > acc[hot])) hot = p;
+    if (hot < 0) break;
+    const double excess = acc[hot] - avg;
+    members(hot, donors);
+
+    // 1) single object from the hottest processor to an under-average one
+    int32_t mv = -1, mq = -1;
+    double mscore = 0;
+    for (int32_t v : donors)
+      for (int32_t q = 0; q < P; ++q) {
+        if (q == hot || acc[q] >= avg) continue;
+        const double after_src = acc[hot] - loads[v];
+        const double after_dst = acc[q] + loads[v];
+        const double ds = std::fabs(after_src - avg);
+        if (ds >= excess || after_dst > ceil_load) continue;
+        const double score = larger(ds, std::fabs(after_dst - avg));
+        if (mv < 0 || score < mscore) { mv = v; mq = q; mscore = score; }
+      }
+    if (mv >= 0) {
+      plan.push_back({mv, hot, mq});
+      acc[hot] -= loads[mv];
+      acc[mq] += loads[mv];
+      where[mv] = mq;
+      continue;
+    }
+
+    // 2) otherwise exchange one object each way with an under-average processor
+    int32_t sa = -1, sb = -1, sq = -1;
+    double sscore = 0;
+    for (int32_t q = 0; q < P; ++q) {
+      if (q == hot || acc[q] >= avg) continue;
+      members(q, takers);
+      for (int32_t a : donors)
+        for (int32_t b : takers) {
+          const double d = loads[a] - loads[b];
+          if (d <= 0) continue;
+          const double after_src = acc[hot] - d;
+          const double after_dst = acc[q] + d;
+          const double ds = std::fabs(after_src - avg);
+          if (ds >= excess || after_dst > ceil_load) continue;
+          const double score = larger(ds, std::fabs(after_dst - avg));
+          if (sa < 0 || score < sscore) { sa = a; sb = b; sq = q; sscore = score; }
+        }
+    }
+    if (sa < 0) break;
+    plan.push_back({sa, hot, sq});
+    plan.push_back({sb, sq, hot});
+    const double d = loads[sa] - loads[sb];
+    acc[hot] -= d;
+    acc[sq] += d;
+    where[sa] = sq;
+    where[sb] = hot;
+  }
+  return plan;
+}
+
+// ------------------------------------------------------------- measurement --
+
+SampleStore::SampleStore(int32_t K, int32_t async_steps, int32_t sync_steps)
+    : K_(K), async_(async_steps), sync_(sync_steps) {
+  if (K < 0) throw ValidationError("vp count must be >= 0");
+  if (async_steps < 0) throw ValidationError("window.async_steps must be >= 0");
+  if (sync_steps < 1) throw ValidationError("window.sync_steps must be >= 1");
+  seen_.assign(size_t(K) * (async_ + sync_), 0);
+}
+
+void SampleStore::add(int32_t vp, int32_t step, int32_t mode, double value) {
+  if (vp < 0 || vp >= K_) throw ValidationError("sample vp out of range");
+  if (step < 0 || step >= async_ + sync_)
+    throw RuntimeFault("sample step outside the current epoch");
+  if (value < 0) throw ValidationError("sample value must be >= 0");
+  uint8_t& slot = seen_[size_t(vp) * (async_ + sync_) + step];
+  if (slot)
+    throw RuntimeFault("duplicate sample for vp " + std::to_string(vp) + " step " +
+                       std::to_string(step));
+  slot = 1;
+  rec_.push_back({vp, step, mode, value});
+}
+
+void SampleStore::reset() {
+  rec_.clear();
+  std::fill(seen_.begin(), seen_.end(), 0);
+}
+
+std::vector<double> SampleStore::sync_means() const {
+  std::vector<double> s(K_, 0.0);
+  std::vector<int32_t> n(K_, 0);
+  for (const Rec& r : rec_)
+    if (r.mode == kSync) {
+      s[r.vp] += r.v;
+      ++n[r.vp];
+    }
+  for (int32_t v = 0; v < K_; ++v) {
+    if (n[v] == 0)
+      throw RuntimeFault("incomplete measurement: vp " + std::to_string(v) +
+                         " has no synchronous sample in this epoch");
+    s[v] = s[v] / n[v];
+  }
+  return s;
+}
+
+}  // namespace odb

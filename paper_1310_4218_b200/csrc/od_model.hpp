@@ -1,0 +1,118 @@
+// Host-side model of the over-decomposed BRAMS-like workload: decomposition,
+// load field, chunk->processor mapping, measurement store and the two load
+// balancers.  Pure functions on plain vectors, callable from the C ABI
+// (od_capi.cpp) and from the device runtime (od_runtime.cu).
+//
+// Arithmetic that feeds a balancing decision follows the reference's
+// operation order exactly so plans are bit-identical for the same loads
+// (/root/reference/proj/include/overdeck/{workload,cluster,measurement,
+// balancer}.hpp; the file:line of each counterpart is cited per function).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace odb {
+
+// Input-contract violation -> OD_EVALIDATION (errors.hpp:9-12).
+struct ValidationError : std::runtime_error {
+  explicit ValidationError(const std::string& m) : std::runtime_error(m) {}
+};
+// Mid-run failure (stale plan, incomplete measurement, device error)
+// -> OD_ERUNTIME (errors.hpp:15-18).
+struct RuntimeFault : std::runtime_error {
+  explicit RuntimeFault(const std::string& m) : std::runtime_error(m) {}
+};
+
+enum Mode : int32_t { kSync = 0, kAsync = 1 };
+enum Strategy : int32_t { kGreedy = 0, kRefineSwap = 1 };
+enum VpClass : int32_t { kHeavy = 0, kLight = 1 };
+enum Pattern : int32_t { kUniform = 0, kStaticNode0 = 1, kUpperHalfHeavy = 2 };
+
+struct Sub {  // one chunk of columns, half-open ranges
+  int32_t vp = 0, x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+  int64_t boundary = 0;  // cells on faces shared with another chunk
+  int64_t cells() const { return int64_t(x1 - x0) * (y1 - y0); }
+  int32_t w() const { return x1 - x0; }
+  int32_t h() const { return y1 - y0; }
+};
+
+struct MoveRec {
+  int32_t vp, from, to;
+  bool operator==(const MoveRec& o) const { return vp == o.vp && from == o.from && to == o.to; }
+};
+
+struct Work {
+  double items = 0, depth = 0;
+  double total() const { return items * depth; }
+};
+
+// ---- workload ---------------------------------------------------------------
+// contiguous pieces, the first extent%k pieces one longer (workload.hpp:85-95)
+std::vector<std::pair<int32_t, int32_t>> split_extent(int32_t extent, int32_t pieces);
+std::vector<Sub> strips_1d(int32_t nx, int32_t ny, int32_t k);                 // :100-114
+std::vector<Sub> tiles_2d(int32_t nx, int32_t ny, int32_t kx, int32_t ky);     // :117-139
+void check_domain(int32_t nx, int32_t ny, int32_t nz, int32_t fields);         // :20-23
+
+// Column multiplier C, y-major c[y*nx+x] (workload.hpp:41-71).
+struct Field2D {
+  int32_t nx = 0, ny = 0;
+  std::vector<double> c;
+  double at(int32_t x, int32_t y) const { return c[size_t(y) * nx + x]; }
+  double mean_over(const Sub& s) const;  // :58-64
+};
+Field2D make_load_field(int32_t nx, int32_t ny, Pattern p, double heavy, double light,
+                        const std::vector<Sub>& node0_subs);          // :160-181
+Field2D shift_rows_down(const Field2D& c, int32_t shift);              // :185-195
+Work physics_trips(const Sub& s, const Field2D& c, int32_t mzp);       // :199-204
+Work jacobi_items(const Sub& s, int32_t nz, int32_t fields);           // :207-210
+int64_t halo_footprint(const Sub& s, int32_t nz, int32_t fields);      // :213-215
+int64_t chunk_footprint(const Sub& s, int32_t nz, int32_t fields);     // :218-220
+
+// ---- cluster ----------------------------------------------------------------
+std::vector<int32_t> block_mapping(int32_t K, int32_t P);              // cluster.hpp:115-127
+// all-or-nothing; throws RuntimeFault on the first stale move (:130-139)
+std::vector<int32_t> apply_moves(const std::vector<int32_t>& map, int32_t P,
+                                 const std::vector<MoveRec>& moves);
+std::vector<double> totals_per_proc(const std::vector<double>& loads,
+                                    const std::vector<int32_t>& map, int32_t P);  // :142-148
+double max_over_mean(const std::vector<double>& totals);              // :151-157
+
+// ---- balancer ---------------------------------------------------------------
+bool balance_needed(const std::vector<double>& totals, double threshold);  // balancer.hpp:29-32
+std::vector<MoveRec> plan_greedy(const std::vector<double>& loads,
+                                 const std::vector<int32_t>& map, int32_t P);  // :36-63
+std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
+                                      const std::vector<int32_t>& map, int32_t P,
+                                      double tol);                            // :68-152
+
+// ---- measurement --------------------------------------------------------------
+// Per-epoch sample store (measurement.hpp:40-70) + epoch_loads (:75-91).
+class SampleStore {
+ public:
+  SampleStore(int32_t K, int32_t async_steps, int32_t sync_steps);
+  void add(int32_t vp, int32_t step, int32_t mode, double value);
+  void reset();
+  std::vector<double> sync_means() const;
+  int32_t vp_count() const { return K_; }
+  size_t size() const { return rec_.size(); }
+
+ private:
+  struct Rec { int32_t vp, step, mode; double v; };
+  int32_t K_, async_, sync_;
+  std::vector<Rec> rec_;
+  std::vector<uint8_t> seen_;  // K x epoch_steps occupancy
+};
+
+// splitmix64 finaliser (public-domain mixer; engine.hpp:112-118 uses it too)
+inline uint64_t mix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+}  // namespace odb

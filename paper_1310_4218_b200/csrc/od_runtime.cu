@@ -1,0 +1,1058 @@
+// B200 runtime of the over-decomposed column-update path: one instance per
+// rank (= per GPU).  Replaces the modelled execution of the reference's
+// Engine (engine.hpp:135-272) with real device work:
+//
+//   Engine::Engine      -> decomposition, block mapping, load field, chunk
+//                          allocation, seeded initial state on the device
+//   Engine::step_time   -> pack + NCCL halo exchange (cross-rank faces only),
+//                          one batched Jacobi and one batched physics launch
+//                          over the chunk table (Async), or per-chunk launches
+//                          bracketed by cudaEvents / in-kernel per-chunk timers
+//                          (Sync)
+//   Engine::run_epoch   -> the same epoch policy on measured loads, then the
+//                          migrate call moves chunk buffers between GPUs
+//
+// Neighbouring chunks on the same GPU read each other's boundary cells
+// directly through per-face descriptors, so there is no halo copy at all
+// inside a GPU; only faces that border another rank are packed and exchanged.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/overdeck_b200.h"
+#include "od_capi_util.hpp"
+#include "od_kernels.cuh"
+#include "od_model.hpp"
+#include "od_nccl.hpp"
+
+namespace odb {
+
+#define OD_CU(expr)                                                                      \
+  do {                                                                                   \
+    cudaError_t e__ = (expr);                                                            \
+    if (e__ != cudaSuccess)                                                              \
+      throw RuntimeFault(std::string("CUDA error ") + cudaGetErrorString(e__) + " in " + \
+                         #expr);                                                         \
+  } while (0)
+
+#define OD_NC(expr)                                                                      \
+  do {                                                                                   \
+    ncclResult_t r__ = (expr);                                                           \
+    if (r__ != ncclSuccess)                                                              \
+      throw RuntimeFault(std::string("NCCL error ") + odb::nccl().GetErrorString(r__) + " in " + \
+                         #expr);                                                         \
+  } while (0)
+
+constexpr int kTX = 32, kTY = 8, kPrefetch = 4;
+
+static int opposite(int d) { return d ^ 1; }
+
+struct ChunkMem {
+  int32_t vp = -1;
+  Sub sub;
+  int32_t pitch = 0;
+  size_t bytes = 0;
+  double* base = nullptr;
+  double* u[2] = {nullptr, nullptr};
+  double* a = nullptr;
+  int64_t kstride() const { return int64_t(sub.h()) * pitch; }
+};
+
+struct StepRec {
+  int32_t mode = kAsync;
+  int32_t epoch_step = 0;
+  int ev_begin = -1, ev_end = -1;
+  double host_launch_s = 0;
+  int ns_row = -1;                  // TIMER: row of the per-chunk ns counters
+  int chunk_ev0 = -1;               // EVENTS: first event of the per-chunk pairs
+  std::vector<int32_t> slot_vps;    // resident vps at launch time (slot order)
+};
+
+class Runtime {
+ public:
+  Runtime(const od_config& cfg, int rank, int world, int device, const uint8_t* nccl_id);
+  ~Runtime();
+
+  int32_t K() const { return int32_t(subs_.size()); }
+  int32_t P() const { return cfg_.nodes * cfg_.procs_per_node; }
+  const std::vector<int32_t>& mapping() const { return map_; }
+  const std::vector<Sub>& subs() const { return subs_; }
+  const Field2D& field() const { return field_; }
+  std::vector<int32_t> classify() const;
+
+  void step_api(int32_t mode, int32_t epoch_step, double* wall, od_sample* samples);
+  void run_epoch(int32_t e, od_epoch_record* rec);
+  void advance(int32_t n, int32_t* epochs_done);
+  void advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads);
+  void migrate(const std::vector<MoveRec>& plan);
+  bool read_chunk(int32_t vp, double* u, double* a);
+  void stats(od_rt_stats* s);
+  void set_profiling(bool on) { profiling_ = on; }
+  void sync() { OD_CU(cudaStreamSynchronize(s0_)); }
+
+ private:
+  int rank_of_proc(int32_t p) const { return p / cfg_.procs_per_node; }
+  int rank_of_vp(int32_t v) const { return rank_of_proc(map_[v]); }
+  int32_t nbr(int32_t v, int d) const;
+  void set_shift(int32_t rows);
+  void advance_advection(int32_t epoch, int32_t step);
+  ChunkMem alloc_chunk(int32_t vp);
+  void release_chunk(ChunkMem& m);
+  void rebuild_tables();
+  FaceDev edge_of(const ChunkMem& s, int side, int par) const;
+  int new_event();
+  void begin_window();
+  void launch_step(int32_t mode, int32_t epoch_step, bool host_io);
+  // waits for the window, gathers per-step walls and the K x S sample matrix
+  void collect(std::vector<double>& walls, std::vector<double>& samples);
+  struct EpochOut {
+    std::vector<double> walls, loads, totals;
+    std::vector<int32_t> map_before, classes;
+    std::vector<MoveRec> plan;
+    int32_t strategy = -1;
+    double mig_s = 0, imb_before = 1, imb_after = 1;
+  };
+  void finish_epoch(int32_t e, int32_t steps, EpochOut& out);
+
+  od_config cfg_;
+  int rank_, world_, device_;
+  std::vector<Sub> subs_;
+  std::vector<int32_t> map_;
+  Field2D base_, field_;
+  int32_t shift_ = 0;
+  int32_t global_step_ = 0, balance_calls_ = 0;
+  int32_t parity_ = 0;
+  // advance() state
+  int32_t cur_epoch_ = 1, cur_step_ = 0;
+
+  cudaStream_t s0_ = nullptr;
+  ncclComm_t comm_ = nullptr;
+  double* d_cbase_ = nullptr;   // base load field (device copy)
+  double* d_cstage_ = nullptr;  // host-staged shifted field (host_io path)
+  double* h_cstage_ = nullptr;  // pinned
+  double* h_loads_ = nullptr;   // pinned, per-step chunk times (host_io path)
+  std::vector<ChunkMem> chunks_;  // indexed by vp; base == nullptr if not local
+  std::multimap<size_t, double*> pool_;
+  std::vector<int32_t> resident_;  // slot -> vp
+  std::vector<int32_t> tile_begin_, tile_count_;
+  int32_t ntiles_ = 0;
+  ChunkDev* d_chunks_[2] = {nullptr, nullptr};
+  size_t d_chunks_cap_[2] = {0, 0};
+  TileDev* d_tiles_ = nullptr;
+  size_t d_tiles_cap_ = 0;
+  // exchange
+  std::vector<PackJob> jobs_;
+  PackJob* d_jobs_ = nullptr;
+  size_t d_jobs_cap_ = 0;
+  std::vector<int64_t> send_off_, send_cnt_, recv_off_, recv_cnt_;  // per peer, elements
+  double* d_send_ = nullptr;
+  double* d_recv_ = nullptr;
+  size_t send_cap_ = 0, recv_cap_ = 0;
+  std::vector<std::array<int64_t, 4>> recv_face_off_;  // per slot
+  // measurement
+  std::vector<cudaEvent_t> events_;
+  int ev_used_ = 0;
+  std::vector<StepRec> window_;
+  unsigned long long* d_ns_ = nullptr;  // [rows][cap_slots]
+  int ns_rows_ = 0, ns_cols_ = 0, ns_used_ = 0;
+  unsigned long long* d_trips_ = nullptr;
+  double* d_gather_ = nullptr;
+  size_t gather_cap_ = 0;
+  // stats
+  bool profiling_ = false;
+  std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_;
+  od_rt_stats st_{};
+};
+
+// --------------------------------------------------------------- lifecycle --
+
+Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const uint8_t* nccl_id)
+    : cfg_(cfg), rank_(rank), world_(world), device_(device) {
+  // ExperimentConfig::validate (engine.hpp:62-83) + B200 constraints
+  if (cfg.nodes < 1) throw ValidationError("cluster.nodes must be >= 1");
+  if (cfg.procs_per_node < 1) throw ValidationError("cluster.procs_per_node must be >= 1");
+  check_domain(cfg.nx, cfg.ny, cfg.nz, cfg.fields);
+  if (cfg.fields < 1) throw ValidationError("the B200 path needs fields >= 1 (physics reads field 0)");
+  if (cfg.async_steps < 0) throw ValidationError("window.async_steps must be >= 0");
+  if (cfg.sync_steps < 1) throw ValidationError("window.sync_steps must be >= 1");
+  if (cfg.adv_total_shift_rows < 0) throw ValidationError("advection.total_shift_rows must be >= 0");
+  if (cfg.adv_epoch < 0) throw ValidationError("advection.epoch must be >= 0");
+  if (cfg.adv_duration_steps < 1) throw ValidationError("advection.duration_steps must be >= 1");
+  if (cfg.trigger_threshold < 1.0) throw ValidationError("policy.trigger_threshold must be >= 1");
+  if (cfg.refine_tolerance < 0.0) throw ValidationError("policy.refine_tolerance must be >= 0");
+  if (cfg.epochs < 1) throw ValidationError("epochs must be >= 1");
+  if (cfg.kx < 1 || cfg.ky < 1) throw ValidationError("decomposition counts must be >= 1");
+  if (cfg.decomposition_kind == OD_ONE_D && cfg.kx != 1)
+    throw ValidationError("1d decomposition requires kx = 1");
+  if (cfg.decomposition_kind != OD_ONE_D && cfg.decomposition_kind != OD_TWO_D)
+    throw ValidationError("unknown decomposition kind");
+  if (cfg.kx * cfg.ky < cfg.nodes * cfg.procs_per_node)
+    throw ValidationError("vp count must be >= processor count");
+  if (cfg.heavy_value < cfg.light_value || cfg.light_value < 1)
+    throw ValidationError("load values require heavy >= light >= 1");
+  if (cfg.first_call_strategy < 0 || cfg.first_call_strategy > 1 ||
+      cfg.later_call_strategy < 0 || cfg.later_call_strategy > 1)
+    throw ValidationError("unknown strategy");
+  if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
+  if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER)
+    throw ValidationError("unknown measurement mode");
+  if (world != cfg.nodes)
+    throw ValidationError("one rank per node GPU: world size must equal cluster.nodes");
+  if (rank < 0 || rank >= world) throw ValidationError("rank out of range");
+  if (world > 1 && !nccl_id) throw ValidationError("multi-rank runtime needs an NCCL id");
+
+  subs_ = cfg.decomposition_kind == OD_ONE_D ? strips_1d(cfg.nx, cfg.ny, cfg.ky)
+                                             : tiles_2d(cfg.nx, cfg.ny, cfg.kx, cfg.ky);
+  map_ = block_mapping(K(), P());
+  std::vector<Sub> node0;
+  for (int32_t v = 0; v < K(); ++v)
+    if (rank_of_vp(v) == 0) node0.push_back(subs_[v]);
+  base_ = make_load_field(cfg.nx, cfg.ny, Pattern(cfg.pattern), cfg.heavy_value,
+                          cfg.light_value, node0);
+
+  OD_CU(cudaSetDevice(device_));
+  OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
+  if (world_ > 1) {
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    OD_NC(odb::nccl().CommInitRank(&comm_, world_, id, rank_));
+  }
+  const size_t cbytes = base_.c.size() * sizeof(double);
+  OD_CU(cudaMalloc(&d_cbase_, cbytes));
+  OD_CU(cudaMemcpy(d_cbase_, base_.c.data(), cbytes, cudaMemcpyHostToDevice));
+  set_shift(0);
+
+  chunks_.resize(K());
+  for (int32_t v = 0; v < K(); ++v) {
+    if (rank_of_vp(v) != rank_) continue;
+    chunks_[v] = alloc_chunk(v);
+    const ChunkMem& m = chunks_[v];
+    init_chunk<<<296, 256, 0, s0_>>>(m.u[0], m.a, m.sub.w(), m.sub.h(), m.pitch, m.sub.x0,
+                                     m.sub.y0, cfg.nx, cfg.ny, cfg.nz, cfg.fields, cfg.seed);
+    OD_CU(cudaGetLastError());
+    ++st_.kernel_launches;
+  }
+  rebuild_tables();
+  OD_CU(cudaStreamSynchronize(s0_));
+}
+
+Runtime::~Runtime() {
+  cudaSetDevice(device_);
+  if (s0_) cudaStreamSynchronize(s0_);
+  for (auto& m : chunks_)
+    if (m.base) cudaFree(m.base);
+  for (auto& kv : pool_) cudaFree(kv.second);
+  for (auto e : events_) cudaEventDestroy(e);
+  cudaFree(d_cbase_);
+  cudaFree(d_cstage_);
+  if (h_cstage_) cudaFreeHost(h_cstage_);
+  if (h_loads_) cudaFreeHost(h_loads_);
+  cudaFree(d_chunks_[0]);
+  cudaFree(d_chunks_[1]);
+  cudaFree(d_tiles_);
+  cudaFree(d_jobs_);
+  cudaFree(d_send_);
+  cudaFree(d_recv_);
+  cudaFree(d_ns_);
+  cudaFree(d_trips_);
+  cudaFree(d_gather_);
+  if (comm_) odb::nccl().CommDestroy(comm_);
+  if (s0_) cudaStreamDestroy(s0_);
+}
+
+// ------------------------------------------------------------------ model --
+
+int32_t Runtime::nbr(int32_t v, int d) const {
+  const int32_t kx = cfg_.decomposition_kind == OD_ONE_D ? 1 : cfg_.kx;
+  const int32_t ky = cfg_.ky;
+  const int32_t i = v % kx, j = v / kx;
+  switch (d) {
+    case kLeft: return i > 0 ? v - 1 : -1;
+    case kRight: return i + 1 < kx ? v + 1 : -1;
+    case kTop: return j > 0 ? v - kx : -1;
+    default: return j + 1 < ky ? v + kx : -1;
+  }
+}
+
+void Runtime::set_shift(int32_t rows) {
+  shift_ = rows;
+  field_ = shift_rows_down(base_, rows % cfg_.ny);
+}
+
+// engine.hpp:323-336
+void Runtime::advance_advection(int32_t epoch, int32_t step) {
+  if (cfg_.adv_epoch == 0 || cfg_.adv_total_shift_rows == 0) return;
+  int32_t target = shift_;
+  if (epoch > cfg_.adv_epoch) {
+    target = cfg_.adv_total_shift_rows;
+  } else if (epoch == cfg_.adv_epoch) {
+    const int32_t k = std::min(step + 1, cfg_.adv_duration_steps);
+    target = int32_t(std::lround(double(cfg_.adv_total_shift_rows) * k / cfg_.adv_duration_steps));
+  }
+  if (target != shift_) set_shift(target);
+}
+
+// engine.hpp:281-287
+std::vector<int32_t> Runtime::classify() const {
+  const double mid = 0.5 * (cfg_.heavy_value + cfg_.light_value);
+  std::vector<int32_t> out(K());
+  for (int32_t v = 0; v < K(); ++v) out[v] = field_.mean_over(subs_[v]) > mid ? kHeavy : kLight;
+  return out;
+}
+
+// ----------------------------------------------------------------- memory --
+
+ChunkMem Runtime::alloc_chunk(int32_t vp) {
+  ChunkMem m;
+  m.vp = vp;
+  m.sub = subs_[vp];
+  m.pitch = (m.sub.w() + 15) / 16 * 16;
+  const size_t plane = size_t(m.sub.h()) * m.pitch;
+  const size_t field_elems = plane * cfg_.nz * cfg_.fields;
+  m.bytes = (2 * field_elems + plane * cfg_.nz) * sizeof(double);
+  auto it = pool_.find(m.bytes);
+  if (it != pool_.end()) {
+    m.base = it->second;
+    pool_.erase(it);
+  } else {
+    OD_CU(cudaMalloc(&m.base, m.bytes));
+  }
+  m.u[0] = m.base;
+  m.u[1] = m.base + field_elems;
+  m.a = m.base + 2 * field_elems;
+  return m;
+}
+
+void Runtime::release_chunk(ChunkMem& m) {
+  if (m.base) pool_.emplace(m.bytes, m.base);
+  m = ChunkMem();
+}
+
+FaceDev Runtime::edge_of(const ChunkMem& s, int side, int par) const {
+  FaceDev f;
+  const double* b = s.u[par];
+  f.fs = s.kstride() * cfg_.nz;
+  f.ks = s.kstride();
+  switch (side) {
+    case kLeft: f.p = b; f.es = s.pitch; break;
+    case kRight: f.p = b + (s.sub.w() - 1); f.es = s.pitch; break;
+    case kTop: f.p = b; f.es = 1; break;
+    default: f.p = b + int64_t(s.sub.h() - 1) * s.pitch; f.es = 1; break;
+  }
+  return f;
+}
+
+template <typename T>
+static void upload(T*& dptr, size_t& cap, const std::vector<T>& h) {
+  if (h.size() > cap) {
+    cudaFree(dptr);
+    dptr = nullptr;
+    cap = std::max<size_t>(h.size(), 16);
+    OD_CU(cudaMalloc(&dptr, cap * sizeof(T)));
+  }
+  if (!h.empty()) OD_CU(cudaMemcpy(dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+void Runtime::rebuild_tables() {
+  resident_.clear();
+  for (int32_t v = 0; v < K(); ++v)
+    if (rank_of_vp(v) == rank_) resident_.push_back(v);
+  const int32_t nres = int32_t(resident_.size());
+  std::vector<int32_t> slot_of(K(), -1);
+  for (int32_t i = 0; i < nres; ++i) slot_of[resident_[i]] = i;
+
+  // tiles, grouped by slot
+  std::vector<TileDev> tiles;
+  tile_begin_.assign(nres, 0);
+  tile_count_.assign(nres, 0);
+  for (int32_t i = 0; i < nres; ++i) {
+    const Sub& s = subs_[resident_[i]];
+    tile_begin_[i] = int32_t(tiles.size());
+    for (int32_t ty = 0; ty < s.h(); ty += kTY)
+      for (int32_t tx = 0; tx < s.w(); tx += kTX) tiles.push_back(TileDev{i, tx, ty, 0});
+    tile_count_[i] = int32_t(tiles.size()) - tile_begin_[i];
+  }
+  ntiles_ = int32_t(tiles.size());
+  upload(d_tiles_, d_tiles_cap_, tiles);
+
+  // exchange schedule: per peer, faces in (sender vp, side) order
+  jobs_.clear();
+  send_off_.assign(world_, 0);
+  send_cnt_.assign(world_, 0);
+  recv_off_.assign(world_, 0);
+  recv_cnt_.assign(world_, 0);
+  recv_face_off_.assign(nres, {-1, -1, -1, -1});
+  const int64_t per_cell = int64_t(cfg_.nz) * cfg_.fields;
+  int64_t soff = 0, roff = 0;
+  for (int q = 0; q < world_; ++q) {
+    send_off_[q] = soff;
+    recv_off_[q] = roff;
+    if (q == rank_) continue;
+    for (int32_t v : resident_)
+      for (int d = 0; d < 4; ++d) {
+        const int32_t n = nbr(v, d);
+        if (n < 0 || rank_of_vp(n) != q) continue;
+        const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
+        jobs_.push_back(PackJob{slot_of[v], d, len, 0, soff});
+        soff += per_cell * len;
+      }
+    send_cnt_[q] = soff - send_off_[q];
+    for (int32_t v = 0; v < K(); ++v) {
+      if (rank_of_vp(v) != q) continue;
+      for (int d = 0; d < 4; ++d) {
+        const int32_t n = nbr(v, d);
+        if (n < 0 || rank_of_vp(n) != rank_) continue;
+        const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
+        recv_face_off_[slot_of[n]][opposite(d)] = roff;
+        roff += per_cell * len;
+      }
+    }
+    recv_cnt_[q] = roff - recv_off_[q];
+  }
+  if (size_t(soff) > send_cap_) {
+    cudaFree(d_send_);
+    d_send_ = nullptr;
+    send_cap_ = size_t(soff);
+    OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
+  }
+  if (size_t(roff) > recv_cap_) {
+    cudaFree(d_recv_);
+    d_recv_ = nullptr;
+    recv_cap_ = size_t(roff);
+    OD_CU(cudaMalloc(&d_recv_, recv_cap_ * sizeof(double)));
+  }
+  upload(d_jobs_, d_jobs_cap_, jobs_);
+
+  // chunk descriptors for both parities
+  for (int par = 0; par < 2; ++par) {
+    std::vector<ChunkDev> tab(nres);
+    for (int32_t i = 0; i < nres; ++i) {
+      const ChunkMem& m = chunks_[resident_[i]];
+      ChunkDev& c = tab[i];
+      std::memset(&c, 0, sizeof(c));
+      c.in = m.u[par];
+      c.out = m.u[par ^ 1];
+      c.a = m.a;
+      c.kstride = m.kstride();
+      c.fstride = c.kstride * cfg_.nz;
+      c.w = m.sub.w();
+      c.h = m.sub.h();
+      c.pitch = m.pitch;
+      c.x0 = m.sub.x0;
+      c.y0 = m.sub.y0;
+      c.vp = m.vp;
+      for (int d = 0; d < 4; ++d) {
+        const int32_t n = nbr(m.vp, d);
+        if (n < 0) {
+          c.face[d] = edge_of(m, d, par);  // zero-flux boundary: the cell itself
+        } else if (rank_of_vp(n) == rank_) {
+          c.face[d] = edge_of(chunks_[n], opposite(d), par);
+        } else {
+          const int32_t len = (d == kLeft || d == kRight) ? c.h : c.w;
+          c.face[d].p = d_recv_ + recv_face_off_[i][d];
+          c.face[d].fs = int64_t(cfg_.nz) * len;
+          c.face[d].ks = len;
+          c.face[d].es = 1;
+        }
+      }
+    }
+    upload(d_chunks_[par], d_chunks_cap_[par], tab);
+  }
+  if (!d_trips_ || ns_cols_ < nres) {
+    ns_cols_ = std::max(nres, 1);
+    cudaFree(d_trips_);
+    OD_CU(cudaMalloc(&d_trips_, size_t(ns_cols_) * sizeof(unsigned long long)));
+    cudaFree(d_ns_);
+    d_ns_ = nullptr;
+    ns_rows_ = 0;
+  }
+  st_.resident_chunks = nres;
+}
+
+// ------------------------------------------------------------------- steps --
+
+int Runtime::new_event() {
+  if (ev_used_ == int(events_.size())) {
+    cudaEvent_t e;
+    OD_CU(cudaEventCreate(&e));
+    events_.push_back(e);
+  }
+  return ev_used_++;
+}
+
+void Runtime::begin_window() {
+  window_.clear();
+  ev_used_ = 0;
+  ns_used_ = 0;
+  prof_j_.clear();
+  prof_p_.clear();
+  prof_pack_.clear();
+  prof_x_.clear();
+}
+
+void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
+  const auto t0 = std::chrono::steady_clock::now();
+  StepRec r;
+  r.mode = mode;
+  r.epoch_step = epoch_step;
+  r.slot_vps = resident_;
+  const int par = parity_;
+  const int32_t nres = int32_t(resident_.size());
+  const bool timer = host_io || (mode == kSync && cfg_.measure == OD_MEASURE_TIMER);
+  r.ev_begin = new_event();
+  OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
+
+  const double* cfield = d_cbase_;
+  int32_t shift = shift_ % cfg_.ny;
+  if (host_io) {
+    // the reference keeps the shifted load field on the host (engine.hpp:337-342)
+    std::memcpy(h_cstage_, field_.c.data(), field_.c.size() * sizeof(double));
+    OD_CU(cudaMemcpyAsync(d_cstage_, h_cstage_, field_.c.size() * sizeof(double),
+                          cudaMemcpyHostToDevice, s0_));
+    cfield = d_cstage_;
+    shift = 0;
+  }
+  unsigned long long* ns = nullptr;
+  if (timer) {
+    if (ns_used_ == ns_rows_) {
+      // grow the counter matrix (rare: first use or a longer window)
+      const int rows = std::max(ns_rows_ * 2, cfg_.sync_steps + 1);
+      unsigned long long* nd = nullptr;
+      OD_CU(cudaStreamSynchronize(s0_));
+      OD_CU(cudaMalloc(&nd, size_t(rows) * ns_cols_ * sizeof(unsigned long long)));
+      if (d_ns_) {
+        OD_CU(cudaMemcpy(nd, d_ns_, size_t(ns_rows_) * ns_cols_ * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToDevice));
+        cudaFree(d_ns_);
+      }
+      d_ns_ = nd;
+      ns_rows_ = rows;
+    }
+    r.ns_row = ns_used_++;
+    ns = d_ns_ + size_t(r.ns_row) * ns_cols_;
+    OD_CU(cudaMemsetAsync(ns, 0, size_t(ns_cols_) * sizeof(unsigned long long), s0_));
+  }
+
+  // boundaries of chunks that border another GPU: pack, then exchange
+  if (!jobs_.empty() || (world_ > 1 && std::any_of(recv_cnt_.begin(), recv_cnt_.end(),
+                                                   [](int64_t c) { return c > 0; }))) {
+    int e0 = -1, e1 = -1, e2 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    if (!jobs_.empty()) {
+      pack_faces<<<dim3(unsigned(jobs_.size()), unsigned(cfg_.fields)), 256, 0, s0_>>>(
+          d_chunks_[par], d_jobs_, d_send_, cfg_.nz);
+      OD_CU(cudaGetLastError());
+      ++st_.kernel_launches;
+    }
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+    }
+    OD_NC(odb::nccl().GroupStart());
+    for (int q = 0; q < world_; ++q) {
+      if (q == rank_) continue;
+      if (send_cnt_[q] > 0)
+        OD_NC(odb::nccl().Send(d_send_ + send_off_[q], size_t(send_cnt_[q]), ncclFloat64, q, comm_, s0_));
+      if (recv_cnt_[q] > 0)
+        OD_NC(odb::nccl().Recv(d_recv_ + recv_off_[q], size_t(recv_cnt_[q]), ncclFloat64, q, comm_, s0_));
+      st_.halo_bytes_sent += send_cnt_[q] * int64_t(sizeof(double));
+    }
+    OD_NC(odb::nccl().GroupEnd());
+    if (profiling_) {
+      e2 = new_event();
+      OD_CU(cudaEventRecord(events_[e2], s0_));
+      prof_pack_.push_back({e0, e1});
+      prof_x_.push_back({e1, e2});
+    }
+  }
+
+  const dim3 blk(kTX, kTY);
+  if (mode == kAsync || timer) {
+    int e0 = -1, e1 = -1, e2 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    if (ntiles_ > 0) {
+      if (timer)
+        jacobi_step<kTX, kTY, kPrefetch, true><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_, cfg_.nz, ns);
+      else
+        jacobi_step<kTX, kTY, kPrefetch, false><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_, cfg_.nz, nullptr);
+      OD_CU(cudaGetLastError());
+      if (profiling_) {
+        e1 = new_event();
+        OD_CU(cudaEventRecord(events_[e1], s0_));
+      }
+      if (timer)
+        physics_step<kTX, kTY, true, false><<<ntiles_, blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz, cfg_.n_inner, ns,
+            nullptr);
+      else
+        physics_step<kTX, kTY, false, false><<<ntiles_, blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz, cfg_.n_inner,
+            nullptr, nullptr);
+      OD_CU(cudaGetLastError());
+      st_.kernel_launches += 2;
+      st_.jacobi_launches += 1;
+      st_.physics_launches += 1;
+      if (profiling_) {
+        e2 = new_event();
+        OD_CU(cudaEventRecord(events_[e2], s0_));
+        prof_j_.push_back({e0, e1});
+        prof_p_.push_back({e1, e2});
+      }
+    }
+  } else {
+    // paper protocol: serialised per-chunk launches with
+    // an event pair around each chunk's Jacobi + physics
+    r.chunk_ev0 = ev_used_;
+    for (int32_t i = 0; i < nres; ++i) {
+      const int eb = new_event(), ee = new_event();
+      OD_CU(cudaEventRecord(events_[eb], s0_));
+      jacobi_step<kTX, kTY, kPrefetch, false>
+          <<<dim3(tile_count_[i], cfg_.fields), blk, 0, s0_>>>(
+              d_chunks_[par], d_tiles_ + tile_begin_[i], cfg_.nz, nullptr);
+      physics_step<kTX, kTY, false, false><<<tile_count_[i], blk, 0, s0_>>>(
+          d_chunks_[par], d_tiles_ + tile_begin_[i], cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
+          cfg_.n_inner, nullptr, nullptr);
+      OD_CU(cudaGetLastError());
+      OD_CU(cudaEventRecord(events_[ee], s0_));
+      st_.kernel_launches += 2;
+      st_.jacobi_launches += 1;
+      st_.physics_launches += 1;
+    }
+  }
+  if (host_io && nres > 0) {
+    // the step's per-chunk device times back to the host
+    OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(nres) * sizeof(unsigned long long),
+                          cudaMemcpyDeviceToHost, s0_));
+  }
+  r.ev_end = new_event();
+  OD_CU(cudaEventRecord(events_[r.ev_end], s0_));
+  parity_ ^= 1;
+  ++st_.steps;
+  r.host_launch_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  window_.push_back(std::move(r));
+}
+
+static double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  OD_CU(cudaEventElapsedTime(&ms, a, b));
+  return double(ms) * 1e-3;
+}
+
+void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) {
+  OD_CU(cudaStreamSynchronize(s0_));
+  const int32_t S = int32_t(window_.size());
+  const int32_t Kv = K();
+  std::vector<unsigned long long> ns;
+  if (ns_used_ > 0) {
+    ns.resize(size_t(ns_used_) * ns_cols_);
+    OD_CU(cudaMemcpy(ns.data(), d_ns_, ns.size() * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost));
+  }
+  // local rows: [S*K samples | S walls]
+  const size_t row = size_t(S) * Kv + S;
+  std::vector<double> local(row, 0.0);
+  for (int32_t s = 0; s < S; ++s) {
+    const StepRec& r = window_[s];
+    local[size_t(S) * Kv + s] = elapsed_s(events_[r.ev_begin], events_[r.ev_end]);
+    for (size_t i = 0; i < r.slot_vps.size(); ++i) {
+      double v;
+      if (r.ns_row >= 0 && r.mode == kSync)
+        v = double(ns[size_t(r.ns_row) * ns_cols_ + i]) * 1e-9;
+      else if (r.mode == kSync && r.chunk_ev0 >= 0)
+        v = elapsed_s(events_[r.chunk_ev0 + 2 * i], events_[r.chunk_ev0 + 2 * i + 1]);
+      else
+        v = r.host_launch_s;  // launch_only_sample: only the launch is visible
+      local[size_t(s) * Kv + r.slot_vps[i]] = v;
+    }
+  }
+  for (auto& p : prof_j_) st_.jacobi_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  for (auto& p : prof_p_) st_.physics_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  for (auto& p : prof_pack_) st_.pack_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  for (auto& p : prof_x_) st_.exchange_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+
+  walls.assign(S, 0.0);
+  samples.assign(size_t(S) * Kv, 0.0);
+  if (world_ == 1) {
+    std::copy(local.begin(), local.begin() + size_t(S) * Kv, samples.begin());
+    for (int32_t s = 0; s < S; ++s) walls[s] = local[size_t(S) * Kv + s];
+    return;
+  }
+  const size_t need = row * (world_ + 1);
+  if (need > gather_cap_) {
+    cudaFree(d_gather_);
+    d_gather_ = nullptr;
+    gather_cap_ = need;
+    OD_CU(cudaMalloc(&d_gather_, gather_cap_ * sizeof(double)));
+  }
+  OD_CU(cudaMemcpy(d_gather_, local.data(), row * sizeof(double), cudaMemcpyHostToDevice));
+  OD_NC(odb::nccl().AllGather(d_gather_, d_gather_ + row, row, ncclFloat64, comm_, s0_));
+  std::vector<double> all(row * world_);
+  OD_CU(cudaMemcpyAsync(all.data(), d_gather_ + row, all.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost, s0_));
+  OD_CU(cudaStreamSynchronize(s0_));
+  // values are taken from the owning rank (selection, no arithmetic)
+  for (int32_t s = 0; s < S; ++s) {
+    double mx = 0;
+    for (int q = 0; q < world_; ++q) mx = std::max(mx, all[q * row + size_t(S) * Kv + s]);
+    walls[s] = mx;
+    for (int32_t v = 0; v < Kv; ++v) {
+      const int q = rank_of_vp(v);
+      samples[size_t(s) * Kv + v] = all[q * row + size_t(s) * Kv + v];
+    }
+  }
+}
+
+void Runtime::step_api(int32_t mode, int32_t epoch_step, double* wall, od_sample* out) {
+  if (mode != kSync && mode != kAsync) throw ValidationError("unknown launch mode");
+  begin_window();
+  launch_step(mode, epoch_step, false);
+  std::vector<double> walls, samples;
+  collect(walls, samples);
+  if (wall) *wall = walls[0];
+  if (out)
+    for (int32_t v = 0; v < K(); ++v) out[v] = od_sample{v, epoch_step, mode, 0, samples[v]};
+}
+
+// engine.hpp:235-272 with measured samples and real migration
+void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
+  std::vector<double> samples;
+  collect(o.walls, samples);
+  SampleStore db(K(), cfg_.async_steps, cfg_.sync_steps);
+  for (int32_t s = 0; s < steps; ++s) {
+    const int32_t mode = s < cfg_.async_steps ? kAsync : kSync;
+    for (int32_t v = 0; v < K(); ++v) db.add(v, s, mode, samples[size_t(s) * K() + v]);
+  }
+  o.loads = db.sync_means();
+  o.totals = totals_per_proc(o.loads, map_, P());
+  o.imb_before = max_over_mean(o.totals);
+  o.imb_after = o.imb_before;
+  if (e < cfg_.epochs && balance_needed(o.totals, cfg_.trigger_threshold)) {
+    o.strategy = balance_calls_ == 0 ? cfg_.first_call_strategy : cfg_.later_call_strategy;
+    o.plan = o.strategy == kGreedy ? plan_greedy(o.loads, map_, P())
+                                   : plan_refine_swap(o.loads, map_, P(), cfg_.refine_tolerance);
+    ++balance_calls_;
+    if (!o.plan.empty()) {
+      const auto t0 = std::chrono::steady_clock::now();
+      migrate(o.plan);
+      o.mig_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      o.imb_after = max_over_mean(totals_per_proc(o.loads, map_, P()));
+    }
+  }
+}
+
+void Runtime::run_epoch(int32_t e, od_epoch_record* rec) {
+  const int32_t S = cfg_.async_steps + cfg_.sync_steps;
+  EpochOut o;
+  o.map_before = map_;
+  o.classes = classify();
+  begin_window();
+  for (int32_t s = 0; s < S; ++s) {
+    advance_advection(e, s);
+    launch_step(s < cfg_.async_steps ? kAsync : kSync, s, false);
+    ++global_step_;
+  }
+  finish_epoch(e, S, o);
+  if (!rec) return;
+  rec->epoch = e;
+  rec->n_steps = S;
+  rec->compute_total = 0;
+  for (int32_t s = 0; s < S; ++s) {
+    if (rec->step_times) rec->step_times[s] = o.walls[s];
+    rec->compute_total += o.walls[s];
+  }
+  rec->strategy = o.strategy;
+  rec->n_moves = int32_t(o.plan.size());
+  if (rec->moves) {
+    if (int32_t(o.plan.size()) > rec->moves_cap) throw ValidationError("moves_cap too small");
+    for (size_t i = 0; i < o.plan.size(); ++i)
+      rec->moves[i] = od_move{o.plan[i].vp, o.plan[i].from, o.plan[i].to};
+  }
+  rec->migration_seconds = o.mig_s;
+  rec->imbalance_before = o.imb_before;
+  rec->imbalance_after = o.imb_after;
+  if (rec->proc_loads) std::copy(o.totals.begin(), o.totals.end(), rec->proc_loads);
+  if (rec->vp_loads) std::copy(o.loads.begin(), o.loads.end(), rec->vp_loads);
+  if (rec->mapping) std::copy(o.map_before.begin(), o.map_before.end(), rec->mapping);
+  if (rec->classes) std::copy(o.classes.begin(), o.classes.end(), rec->classes);
+}
+
+void Runtime::advance(int32_t n, int32_t* epochs_done) {
+  const int32_t S = cfg_.async_steps + cfg_.sync_steps;
+  int32_t done = 0;
+  for (int32_t i = 0; i < n; ++i) {
+    if (cur_step_ == 0) begin_window();
+    advance_advection(cur_epoch_, cur_step_);
+    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, false);
+    ++global_step_;
+    if (++cur_step_ == S) {
+      EpochOut o;
+      finish_epoch(cur_epoch_, S, o);
+      ++cur_epoch_;
+      cur_step_ = 0;
+      ++done;
+    }
+  }
+  if (epochs_done) *epochs_done = done;
+}
+
+void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads) {
+  if (n < 0) throw ValidationError("negative step count");
+  const size_t cells = size_t(cfg_.nx) * cfg_.ny;
+  if (!h_cstage_) {
+    OD_CU(cudaMallocHost(&h_cstage_, cells * sizeof(double)));
+    OD_CU(cudaMalloc(&d_cstage_, cells * sizeof(double)));
+    OD_CU(cudaMallocHost(&h_loads_, std::max<size_t>(K(), 1) * sizeof(unsigned long long)));
+  }
+  if (host_c && n_fields > 0) {
+    // the caller's load multiplier field replaces the base field
+    base_.c.assign(host_c, host_c + cells);
+    OD_CU(cudaMemcpy(d_cbase_, host_c, cells * sizeof(double), cudaMemcpyHostToDevice));
+    set_shift(shift_);
+  }
+  const int32_t S = cfg_.async_steps + cfg_.sync_steps;
+  for (int32_t i = 0; i < n; ++i) {
+    if (cur_step_ == 0) begin_window();
+    advance_advection(cur_epoch_, cur_step_);
+    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true);
+    OD_CU(cudaStreamSynchronize(s0_));
+    if (host_loads) {
+      double* row = host_loads + size_t(i) * K();
+      std::fill(row, row + K(), 0.0);
+      const auto& vps = window_.back().slot_vps;
+      for (size_t j = 0; j < vps.size(); ++j) row[vps[j]] = double(h_loads_[j]) * 1e-9;
+    }
+    ++global_step_;
+    if (++cur_step_ == S) {
+      EpochOut o;
+      finish_epoch(cur_epoch_, S, o);
+      ++cur_epoch_;
+      cur_step_ = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- migrate --
+
+void Runtime::migrate(const std::vector<MoveRec>& plan) {
+  std::vector<int32_t> next = apply_moves(map_, P(), plan);  // throws before any data moves
+  if (world_ > 1) {
+    std::vector<int32_t> moved;
+    for (int32_t v = 0; v < K(); ++v)
+      if (rank_of_proc(map_[v]) != rank_of_proc(next[v])) moved.push_back(v);
+    std::vector<ChunkMem> incoming(K());
+    for (int32_t v : moved)
+      if (rank_of_proc(next[v]) == rank_) incoming[v] = alloc_chunk(v);
+    OD_CU(cudaStreamSynchronize(s0_));
+    OD_NC(odb::nccl().GroupStart());
+    for (int32_t v : moved) {
+      const int src = rank_of_proc(map_[v]), dst = rank_of_proc(next[v]);
+      const size_t plane = size_t(subs_[v].h()) * ((subs_[v].w() + 15) / 16 * 16);
+      const size_t ae = plane * cfg_.nz, fe = ae * cfg_.fields;
+      if (src == rank_) {
+        OD_NC(odb::nccl().Send(chunks_[v].u[parity_], fe, ncclFloat64, dst, comm_, s0_));
+        OD_NC(odb::nccl().Send(chunks_[v].a, ae, ncclFloat64, dst, comm_, s0_));
+        st_.migrated_bytes += int64_t((fe + ae) * sizeof(double));
+      }
+      if (dst == rank_) {
+        OD_NC(odb::nccl().Recv(incoming[v].u[parity_], fe, ncclFloat64, src, comm_, s0_));
+        OD_NC(odb::nccl().Recv(incoming[v].a, ae, ncclFloat64, src, comm_, s0_));
+      }
+    }
+    OD_NC(odb::nccl().GroupEnd());
+    OD_CU(cudaStreamSynchronize(s0_));
+    for (int32_t v : moved) {
+      if (rank_of_proc(map_[v]) == rank_) release_chunk(chunks_[v]);
+      if (rank_of_proc(next[v]) == rank_) chunks_[v] = incoming[v];
+    }
+  }
+  map_ = std::move(next);
+  rebuild_tables();
+}
+
+bool Runtime::read_chunk(int32_t vp, double* u, double* a) {
+  if (vp < 0 || vp >= K()) throw ValidationError("vp out of range");
+  if (rank_of_vp(vp) != rank_) return false;
+  OD_CU(cudaStreamSynchronize(s0_));
+  const ChunkMem& m = chunks_[vp];
+  const size_t w = m.sub.w(), h = m.sub.h();
+  const size_t rows_u = h * cfg_.nz * cfg_.fields, rows_a = h * cfg_.nz;
+  if (u)
+    OD_CU(cudaMemcpy2D(u, w * sizeof(double), m.u[parity_], m.pitch * sizeof(double),
+                       w * sizeof(double), rows_u, cudaMemcpyDeviceToHost));
+  if (a)
+    OD_CU(cudaMemcpy2D(a, w * sizeof(double), m.a, m.pitch * sizeof(double), w * sizeof(double),
+                       rows_a, cudaMemcpyDeviceToHost));
+  return true;
+}
+
+void Runtime::stats(od_rt_stats* s) {
+  // trips of the current load field over the resident columns (host count)
+  int64_t trips = 0;
+  for (int32_t v : resident_) {
+    const Sub& sb = subs_[v];
+    for (int32_t y = sb.y0; y < sb.y1; ++y)
+      for (int32_t x = sb.x0; x < sb.x1; ++x) {
+        const int32_t t = int32_t(std::floor(double(cfg_.nz) * field_.at(x, y))) - 1;
+        trips += t > 0 ? t : 0;
+      }
+  }
+  st_.physics_trips = trips;
+  *s = st_;
+}
+
+}  // namespace odb
+
+// ----------------------------------------------------------------- C ABI --
+
+using odb::guarded;
+using odb::Runtime;
+using odb::ValidationError;
+using odb::RuntimeFault;
+
+struct od_runtime {
+  Runtime* rt;
+};
+
+static Runtime& R(const od_runtime* h) {
+  if (!h || !h->rt) throw ValidationError("null runtime handle");
+  return *h->rt;
+}
+
+extern "C" {
+
+int od_nccl_unique_id(uint8_t* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null pointer: out");
+    ncclUniqueId id;
+    OD_NC(odb::nccl().GetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int od_rt_create(const od_config* cfg, int32_t rank, int32_t world, int32_t device,
+                 const uint8_t* nccl_id, od_runtime** out) {
+  return guarded([&] {
+    if (!cfg || !out) throw ValidationError("null pointer: cfg/out");
+    *out = nullptr;
+    auto* h = new od_runtime{nullptr};
+    try {
+      h->rt = new Runtime(*cfg, rank, world, device, nccl_id);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void od_rt_destroy(od_runtime* rt) {
+  if (!rt) return;
+  delete rt->rt;
+  delete rt;
+}
+
+int od_rt_vp_count(const od_runtime* rt, int32_t* k) {
+  return guarded([&] { *k = R(rt).K(); });
+}
+
+int od_rt_proc_count(const od_runtime* rt, int32_t* p) {
+  return guarded([&] { *p = R(rt).P(); });
+}
+
+int od_rt_mapping(const od_runtime* rt, int32_t* map) {
+  return guarded([&] {
+    const auto& m = R(rt).mapping();
+    std::copy(m.begin(), m.end(), map);
+  });
+}
+
+int od_rt_subdomains(const od_runtime* rt, od_subdomain* out) {
+  return guarded([&] {
+    const auto& s = R(rt).subs();
+    for (size_t i = 0; i < s.size(); ++i)
+      out[i] = od_subdomain{s[i].vp, s[i].x0, s[i].x1, s[i].y0, s[i].y1, s[i].boundary};
+  });
+}
+
+int od_rt_classify(const od_runtime* rt, int32_t* classes) {
+  return guarded([&] {
+    auto c = R(rt).classify();
+    std::copy(c.begin(), c.end(), classes);
+  });
+}
+
+int od_rt_load_field(const od_runtime* rt, double* c) {
+  return guarded([&] {
+    const auto& f = R(rt).field();
+    std::copy(f.c.begin(), f.c.end(), c);
+  });
+}
+
+int od_rt_step(od_runtime* rt, int32_t mode, int32_t epoch_step, int32_t /*global_step*/,
+               double* wall, od_sample* samples) {
+  return guarded([&] { R(rt).step_api(mode, epoch_step, wall, samples); });
+}
+
+int od_rt_run_epoch(od_runtime* rt, int32_t epoch_index, od_epoch_record* rec) {
+  return guarded([&] { R(rt).run_epoch(epoch_index, rec); });
+}
+
+int od_rt_advance(od_runtime* rt, int32_t n_steps, int32_t* epochs_done) {
+  return guarded([&] { R(rt).advance(n_steps, epochs_done); });
+}
+
+int od_rt_advance_host(od_runtime* rt, int32_t n_steps, const double* host_c_fields,
+                       int32_t n_fields, double* host_step_loads) {
+  return guarded([&] { R(rt).advance_host(n_steps, host_c_fields, n_fields, host_step_loads); });
+}
+
+int od_rt_migrate(od_runtime* rt, const od_move* moves, int32_t n_moves) {
+  return guarded([&] {
+    if (n_moves < 0) throw ValidationError("negative move count");
+    std::vector<odb::MoveRec> plan(n_moves);
+    for (int32_t i = 0; i < n_moves; ++i) plan[i] = {moves[i].vp, moves[i].from, moves[i].to};
+    R(rt).migrate(plan);
+  });
+}
+
+int od_rt_read_chunk(od_runtime* rt, int32_t vp, double* u, double* a, int32_t* resident) {
+  return guarded([&] {
+    const bool r = R(rt).read_chunk(vp, u, a);
+    if (resident) *resident = r ? 1 : 0;
+  });
+}
+
+int od_rt_stats_get(od_runtime* rt, od_rt_stats* out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null pointer: out");
+    R(rt).stats(out);
+  });
+}
+
+int od_rt_set_profiling(od_runtime* rt, int32_t on) {
+  return guarded([&] { R(rt).set_profiling(on != 0); });
+}
+
+int od_rt_synchronize(od_runtime* rt) {
+  return guarded([&] { R(rt).sync(); });
+}
+
+}  // extern "C"
