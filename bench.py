@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 column-update path (BASELINE.json metric: grid
+column-updates/s at 1/2/4/8 B200, LB on/off, post-LB max/avg GPU load).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+  python bench.py --impl reference ...                     (CPU reference arm)
+
+A "step" is one timestep of the application (Fig. 2): cross-GPU halo
+exchange, one batched Jacobi over all fields and one batched physics launch
+over every resident chunk; every window.async+sync steps an epoch ends with
+measured per-chunk loads, the load balancer and chunk migration.  The timed
+region is exactly K steps including those epoch boundaries.  The state
+(cfg4: 1M columns x 64 levels x 50 fields x 8 B, double buffered = 54 GB) is
+far larger than L2, so no flush is needed between steps.
+
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid column-updates/s"
+UNIT = "column-updates/s"
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=40)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="cfg4")
+    p.add_argument("--n-inner", type=int, default=None)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-lb-off", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks --
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms in the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------- CPU legs --
+
+def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=8, side=256, warmup=0):
+    """Column-updates/s of the CPU oracle port (oracle/field_oracle.c, OpenMP,
+    all host threads) on a side x side sub-grid with the workload's nz, F,
+    n_inner and load pattern."""
+    import numpy as np
+    from oracle import fields as of
+    d = cfg.domain
+    nx, ny = min(side, d.nx), min(side, d.ny)
+    U, A = of.init_state(nx, ny, d.nz, d.fields, cfg.seed)
+    base = np.ones((ny, nx))
+    if int(cfg.pattern) == 2:
+        base[: ny // 2] = cfg.heavy_value
+    elif int(cfg.pattern) == 1:
+        base[: ny // 2, : nx // 2] = cfg.heavy_value
+    for _ in range(warmup):
+        of.step(U, A, base, 0, cfg.n_inner)
+    steps, t0 = 0, time.perf_counter()
+    while steps < max_steps:
+        of.step(U, A, base, 0, cfg.n_inner)
+        steps += 1
+        if time.perf_counter() - t0 >= min_seconds:
+            break
+    dt = time.perf_counter() - t0
+    return nx * ny * steps / dt, {"grid": [nx, ny, d.nz], "fields": d.fields, "steps": steps,
+                                  "seconds": dt}
+
+
+def reference_arm(args, cfg):
+    """--impl reference: the oracle port (the reference simulator computes no
+    field values) timed on this host's cores for W + K steps of a
+    bounded sample of the same workload."""
+    import numpy as np
+    from oracle import fields as of
+    cores = os.cpu_count() or 1
+    d = cfg.domain
+    side = 128
+    nx, ny = min(side, d.nx), min(side, d.ny)
+    U, A = of.init_state(nx, ny, d.nz, d.fields, cfg.seed)
+    base = np.ones((ny, nx))
+    if int(cfg.pattern) == 2:
+        base[: ny // 2] = cfg.heavy_value
+    for _ in range(args.warmup):
+        of.step(U, A, base, 0, cfg.n_inner)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        of.step(U, A, base, 0, cfg.n_inner)
+    dt = time.perf_counter() - t0
+    value = nx * ny * args.steps / dt
+    sim = None
+    try:
+        from oracle import ref as oref
+        if oref.available():
+            t1 = time.perf_counter()
+            oref.run_json({"preset": "expC"})
+            sim = {"workload": "reference simulator run_experiment(expC)",
+                   "seconds": time.perf_counter() - t1}
+    except Exception as e:  # informational only
+        sim = {"error": str(e)}
+    sample = (f"oracle port, {nx}x{ny} columns x {d.nz} levels x {d.fields} fields, "
+              f"n_inner={cfg.n_inner}, {args.steps} steps")
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "sample_columns": nx * ny},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_simulator": sim,
+    }
+
+
+# ------------------------------------------------------------------ GPU leg --
+
+def physics_flops_per_trip(n_inner):
+    # f: 1 mul + 2 fma (setup) + n_inner x 2 fma  (kernels: column_f)
+    return 5 + 4 * n_inner
+
+
+def main():
+    args = parse_args()
+    rank, world, local = dist_env()
+    from paper_1310_4218_b200 import configs
+    make = configs.CONFIGS[args.config]
+    kw = {"epochs": 1 << 30}
+    if args.n_inner is not None:
+        kw["n_inner"] = args.n_inner
+    cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(reference_arm(args, cfg)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1310_4218_b200 as od
+    import numpy as np
+
+    nccl_id = None
+    if world > 1:
+        obj = [od.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        torch.cuda.synchronize()
+        e1.record()
+        e1.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1))
+
+    d = cfg.domain
+    cols = d.nx * d.ny
+    eng = od.Engine(cfg, rank, world, local, nccl_id)
+    eng.advance(args.warmup)
+    eng.synchronize()
+    eng.set_profiling(True)
+    st0 = eng.stats()
+    hist0 = len(eng.epoch_history())
+    with ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
+                      if world == 1 else local) as clk:
+        ms = timed(lambda: (eng.advance(args.steps), eng.synchronize()))
+    st1 = eng.stats()
+    hist = eng.epoch_history()[hist0:]
+    value = cols * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (physics: FP64 pipe) and of the Jacobi (HBM)
+    mapping = eng.mapping().assignment()
+    subs = eng.subdomains()
+    ppn = cfg.cluster.procs_per_node
+    res_cols = sum(s.cells() for v, s in enumerate(subs) if mapping[v] // ppn == rank)
+    n_phys = st1["physics_launches"] - st0["physics_launches"]
+    n_jac = st1["jacobi_launches"] - st0["jacobi_launches"]
+    phys_ms = (st1["physics_ms"] - st0["physics_ms"]) / max(n_phys, 1)
+    jac_ms = (st1["jacobi_ms"] - st0["jacobi_ms"]) / max(n_jac, 1)
+    flops = st1["physics_trips"] * physics_flops_per_trip(cfg.n_inner)
+    jac_bytes = 2.0 * res_cols * d.nz * d.fields * 8
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    own = {}
+    try:
+        own = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64.json")))
+    except Exception:
+        pass
+    fp64_peak = own.get("fp64_fma_tflops", 36.2)
+    hbm_peak = peaks.get("hbm_gbs", 6555.8)
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(
+            f"{args.config}:physics")
+    except Exception:
+        pass
+    phys_tf = flops / (phys_ms * 1e-3) / 1e12 if phys_ms > 0 else None
+    jac_gbs = jac_bytes / (jac_ms * 1e-3) / 1e9 if jac_ms > 0 else None
+    share = phys_ms * n_phys / ms if ms > 0 else None
+
+    launches = st1["kernel_launches"] - st0["kernel_launches"]
+    balanced = [h for h in hist if h["strategy"] >= 0 and h["n_moves"] > 0]
+    post_lb = None
+    if balanced:
+        last = balanced[-1]
+        nxt = [h for h in hist if h["epoch"] == last["epoch"] + 1]
+        post_lb = {"predicted": last["imbalance_after"],
+                   "measured_next_epoch": nxt[0]["imbalance_before"] if nxt else None,
+                   "before": last["imbalance_before"], "moves": last["n_moves"]}
+    eng_imb = [h["imbalance_before"] for h in hist]
+
+    # end to end through the host-facing C ABI call: per step H2D of the
+    # step's load multiplier field (pinned) and D2H of per-chunk loads
+    e2e = None
+    if not args.no_e2e:
+        K = eng.vp_count()
+        loads = np.zeros((args.steps, K))
+        base = np.ascontiguousarray(eng.load_field().as_array())
+        eng.advance_host(1, base, loads[:1])
+        ms_e2e = timed(lambda: eng.advance_host(args.steps, None, loads))
+        e2e = {"value": cols * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": cols * 8,
+               "d2h_bytes_per_step": int(st1["resident_chunks"]) * 8}
+    eng.close()
+    del eng
+
+    lb_off = None
+    if world > 1 and not args.no_lb_off:
+        cfg_off = cfg.replace(policy=cfg.policy.__class__(
+            cfg.policy.first_call_strategy, cfg.policy.later_call_strategy, 1e30,
+            cfg.policy.refine_tolerance))
+        eng2 = od.Engine(cfg_off, rank, world, local, nccl_id)
+        eng2.advance(args.warmup)
+        eng2.synchronize()
+        ms_off = timed(lambda: (eng2.advance(args.steps), eng2.synchronize()))
+        lb_off = {"value": cols * args.steps / (ms_off * 1e-3), "unit": UNIT,
+                  "ms_per_step": ms_off / args.steps,
+                  "imbalance": [h["imbalance_before"] for h in eng2.epoch_history()][-3:]}
+        eng2.close()
+    elif world == 1:
+        lb_off = {"note": "P=1: one processor never balances (imbalance_ratio = 1), "
+                          "LB on and off are the same run"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, info = cpu_sample_rate(cfg)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle/field_oracle.c (OpenMP) on {info['grid'][0]}x{info['grid'][1]}"
+                         f" columns x {info['grid'][2]} levels x {info['fields']} fields, "
+                         f"{info['steps']} steps, {info['seconds']:.1f} s"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "grid": [d.nx, d.ny, d.nz], "fields": d.fields,
+                   "chunks": cfg.vp_count(), "procs": cfg.proc_count(),
+                   "window": [cfg.window.async_steps, cfg.window.sync_steps],
+                   "policy": f"{cfg.policy.first_call_strategy.name}/"
+                             f"{cfg.policy.later_call_strategy.name}"
+                             f"@{cfg.policy.trigger_threshold}",
+                   "n_inner": cfg.n_inner, "measure": cfg.measure.name, "lb": "on",
+                   "l2": "state 54 GB >> 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "fp64", "kernel": "physics_step", "achieved": phys_tf,
+                     "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": phys_tf / fp64_peak if phys_tf else None, "traffic": traffic,
+                     "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)",
+                     "share_of_step": share, "avg_ms": phys_ms},
+        "roofline_jacobi": {"bound": "hbm", "kernel": "jacobi_step", "achieved": jac_gbs,
+                            "peak": hbm_peak, "unit": "GB/s",
+                            "frac": jac_gbs / hbm_peak if jac_gbs else None, "avg_ms": jac_ms,
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "lb_off": lb_off,
+        "post_lb_imbalance": post_lb,
+        "epoch_imbalance": eng_imb,
+        "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
+        "migrated_bytes": st1["migrated_bytes"] - st0["migrated_bytes"],
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

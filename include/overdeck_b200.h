@@ -242,6 +242,12 @@ typedef struct od_rt_stats {
   int32_t pad_;
 } od_rt_stats;
 int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
+/* one row per completed epoch (od_rt_run_epoch, od_rt_advance, ..._host) */
+typedef struct od_epoch_summary {
+  int32_t epoch, strategy, n_moves, n_steps;
+  double compute_total, migration_seconds, imbalance_before, imbalance_after;
+} od_epoch_summary;
+int od_rt_epoch_history(od_runtime* rt, od_epoch_summary* out, int32_t cap, int32_t* n);
 /* enable per-kernel event timing (adds events around each batched kernel) */
 int od_rt_set_profiling(od_runtime* rt, int32_t on);
 int od_rt_synchronize(od_runtime* rt);

@@ -42,6 +42,7 @@
 #define W1 0.125
 #define RMAP 3.984375
 #define EPS 0.001953125
+#define OBLK 64
 
 static uint64_t mix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ULL;
@@ -78,12 +79,21 @@ void oracle_jacobi(int nx, int ny, int nz, int F, const double* in, double* out)
       const double* row = c + (int64_t)y * nx;
       const double* rn = y > 0 ? row - nx : row;
       const double* rs = y + 1 < ny ? row + nx : row;
-      for (int x = 0; x < nx; ++x) {
+      const double* zd = dn + (int64_t)y * nx;
+      const double* zu = up + (int64_t)y * nx;
+      double* orow = o + (int64_t)y * nx;
+      /* x = 0 and x = nx-1 carry the zero-flux boundary; the interior loop is
+       * branch free so it vectorises */
+      for (int x = 0; x < nx; x += (nx > 1 ? nx - 1 : 1)) {
         const double u = row[x];
         const double xm = x > 0 ? row[x - 1] : u;
         const double xp = x + 1 < nx ? row[x + 1] : u;
-        const double s = ((xm + xp) + (rn[x] + rs[x])) + (dn[(int64_t)y * nx + x] + up[(int64_t)y * nx + x]);
-        o[(int64_t)y * nx + x] = fma(W1, s, W0 * u);
+        const double s = ((xm + xp) + (rn[x] + rs[x])) + (zd[x] + zu[x]);
+        orow[x] = fma(W1, s, W0 * row[x]);
+      }
+      for (int x = 1; x < nx - 1; ++x) {
+        const double s = ((row[x - 1] + row[x + 1]) + (rn[x] + rs[x])) + (zd[x] + zu[x]);
+        orow[x] = fma(W1, s, W0 * row[x]);
       }
     }
   }
@@ -114,8 +124,25 @@ static void physics_row(int nx, int ny, int nz, int n_inner, int y, const double
       eb[j] = fma(bv, EPS, EPS);
       yy[j] = fma(0.5, a[act[j]], 0.5 * bv);
     }
+    /* micro-steps on register blocks of OBLK columns (independent chains) */
+    int j0 = 0;
+    for (; j0 + OBLK <= n; j0 += OBLK) {
+      double yv[OBLK], ev[OBLK];
+      for (int j = 0; j < OBLK; ++j) {
+        yv[j] = yy[j0 + j];
+        ev[j] = eb[j0 + j];
+      }
+      for (int i = 0; i < n_inner; ++i) {
+#pragma omp simd
+        for (int j = 0; j < OBLK; ++j) {
+          const double u = fma(-yv[j], yv[j], yv[j]);
+          yv[j] = fma(RMAP, u, ev[j]);
+        }
+      }
+      for (int j = 0; j < OBLK; ++j) yy[j0 + j] = yv[j];
+    }
     for (int i = 0; i < n_inner; ++i)
-      for (int j = 0; j < n; ++j) {
+      for (int j = j0; j < n; ++j) {
         const double u = fma(-yy[j], yy[j], yy[j]);
         yy[j] = fma(RMAP, u, eb[j]);
       }

@@ -88,6 +88,13 @@ class od_rt_stats(C.Structure):
     ]
 
 
+class od_epoch_summary(C.Structure):
+    _fields_ = [("epoch", C.c_int32), ("strategy", C.c_int32), ("n_moves", C.c_int32),
+                ("n_steps", C.c_int32), ("compute_total", C.c_double),
+                ("migration_seconds", C.c_double), ("imbalance_before", C.c_double),
+                ("imbalance_after", C.c_double)]
+
+
 _I32, _I64, _D, _U64 = C.c_int32, C.c_int64, C.c_double, C.c_uint64
 _P = C.POINTER
 _VP = C.c_void_p
@@ -135,6 +142,7 @@ PROTOTYPES = {
     "od_rt_read_chunk": [_VP, _I32, _P(_D), _P(_D), _P(_I32)],
     "od_rt_stats_get": [_VP, _P(od_rt_stats)],
     "od_rt_set_profiling": [_VP, _I32],
+    "od_rt_epoch_history": [_VP, _P(od_epoch_summary), _I32, _P(_I32)],
     "od_rt_synchronize": [_VP],
 }
 _RESTYPE = {"od_last_error": C.c_char_p, "od_abi_version": _I32,

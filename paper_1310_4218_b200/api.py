@@ -26,6 +26,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (RuntimeFault, ValidationError, check, lib, od_config, od_epoch_record,
+                   od_epoch_summary,
                    od_kernel_work, od_move, od_rt_stats, od_sample, od_subdomain)
 
 __all__ = [
@@ -728,6 +729,14 @@ class Engine:
         st = od_rt_stats()
         check(lib.od_rt_stats_get(self._h, C.byref(st)))
         return {n: getattr(st, n) for n, _ in od_rt_stats._fields_ if n != "pad_"}
+
+    def epoch_history(self, last: int = 1 << 16) -> List[dict]:
+        """Summaries of completed epochs (oldest first, at most ``last``)."""
+        out = (od_epoch_summary * max(last, 1))()
+        n = C.c_int32()
+        check(lib.od_rt_epoch_history(self._h, out, last, C.byref(n)))
+        m = min(n.value, last)
+        return [{f: getattr(out[i], f) for f, _ in od_epoch_summary._fields_} for i in range(m)]
 
     def set_profiling(self, on: bool) -> None:
         check(lib.od_rt_set_profiling(self._h, 1 if on else 0))

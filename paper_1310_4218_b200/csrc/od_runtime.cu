@@ -97,6 +97,7 @@ class Runtime {
   bool read_chunk(int32_t vp, double* u, double* a);
   void stats(od_rt_stats* s);
   void set_profiling(bool on) { profiling_ = on; }
+  const std::vector<od_epoch_summary>& history() const { return history_; }
   void sync() { OD_CU(cudaStreamSynchronize(s0_)); }
 
  private:
@@ -171,6 +172,7 @@ class Runtime {
   bool profiling_ = false;
   std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_;
   od_rt_stats st_{};
+  std::vector<od_epoch_summary> history_;
 };
 
 // --------------------------------------------------------------- lifecycle --
@@ -755,6 +757,16 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
       o.imb_after = max_over_mean(totals_per_proc(o.loads, map_, P()));
     }
   }
+  od_epoch_summary h{};
+  h.epoch = e;
+  h.strategy = o.strategy;
+  h.n_moves = int32_t(o.plan.size());
+  h.n_steps = steps;
+  for (double w : o.walls) h.compute_total += w;
+  h.migration_seconds = o.mig_s;
+  h.imbalance_before = o.imb_before;
+  h.imbalance_after = o.imb_after;
+  history_.push_back(h);
 }
 
 void Runtime::run_epoch(int32_t e, od_epoch_record* rec) {
@@ -1044,6 +1056,16 @@ int od_rt_stats_get(od_runtime* rt, od_rt_stats* out) {
   return guarded([&] {
     if (!out) throw ValidationError("null pointer: out");
     R(rt).stats(out);
+  });
+}
+
+int od_rt_epoch_history(od_runtime* rt, od_epoch_summary* out, int32_t cap, int32_t* n) {
+  return guarded([&] {
+    const auto& h = R(rt).history();
+    if (!n) throw ValidationError("null pointer: n");
+    *n = int32_t(h.size());
+    const int32_t m = std::min<int32_t>(cap, int32_t(h.size()));
+    for (int32_t i = 0; i < m; ++i) out[i] = h[h.size() - m + i];
   });
 }
 

@@ -1,0 +1,20 @@
+"""Per-step / per-kernel timing diagnostic for one config on cuda:0."""
+import sys, os, json, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1310_4218_b200 as od
+from paper_1310_4218_b200 import configs
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
+kw = dict(a.split("=") for a in sys.argv[2:])
+kw = {k: int(v) for k, v in kw.items()}
+cfg = configs.CONFIGS[name](**kw)
+with od.Engine(cfg) as eng:
+    eng.set_profiling(True)
+    for e in range(1, 4):
+        t = time.perf_counter()
+        r = eng.run_epoch(e)
+        dt = time.perf_counter() - t
+        st = eng.stats()
+        print(json.dumps({"epoch": e, "host_s": dt, "steps_ms": [round(x * 1e3, 3) for x in r.step_times],
+                          "jacobi_ms_avg": st["jacobi_ms"] / max(st["jacobi_launches"], 1),
+                          "physics_ms_avg": st["physics_ms"] / max(st["physics_launches"], 1),
+                          "imb": [r.imbalance_before, r.imbalance_after], "moves": len(r.plan.moves)}))
