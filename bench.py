@@ -259,8 +259,8 @@ def main():
     subs = eng.subdomains()
     ppn = cfg.cluster.procs_per_node
     res_cols = sum(s.cells() for v, s in enumerate(subs) if mapping[v] // ppn == rank)
-    n_phys = st1["physics_launches"] - st0["physics_launches"]
-    n_jac = st1["jacobi_launches"] - st0["jacobi_launches"]
+    n_phys = st1["physics_timed"] - st0["physics_timed"]
+    n_jac = st1["jacobi_timed"] - st0["jacobi_timed"]
     phys_ms = (st1["physics_ms"] - st0["physics_ms"]) / max(n_phys, 1)
     jac_ms = (st1["jacobi_ms"] - st0["jacobi_ms"]) / max(n_jac, 1)
     flops = st1["physics_trips"] * physics_flops_per_trip(cfg.n_inner)
@@ -285,7 +285,7 @@ def main():
         pass
     phys_tf = flops / (phys_ms * 1e-3) / 1e12 if phys_ms > 0 else None
     jac_gbs = jac_bytes / (jac_ms * 1e-3) / 1e9 if jac_ms > 0 else None
-    share = phys_ms * n_phys / ms if ms > 0 else None
+    share = phys_ms / (ms / args.steps) if ms > 0 else None
 
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     balanced = [h for h in hist if h["strategy"] >= 0 and h["n_moves"] > 0]

@@ -240,6 +240,7 @@ typedef struct od_rt_stats {
   int64_t physics_trips;       /* sum of trips of resident columns, last step */
   int32_t resident_chunks;
   int32_t pad_;
+  int64_t jacobi_timed, physics_timed; /* launches whose event time is in *_ms */
 } od_rt_stats;
 int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
 /* one row per completed epoch (od_rt_run_epoch, od_rt_advance, ..._host) */

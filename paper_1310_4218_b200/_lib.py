@@ -85,6 +85,7 @@ class od_rt_stats(C.Structure):
         ("halo_bytes_sent", C.c_int64), ("migrated_bytes", C.c_int64),
         ("physics_trips", C.c_int64),
         ("resident_chunks", C.c_int32), ("pad_", C.c_int32),
+        ("jacobi_timed", C.c_int64), ("physics_timed", C.c_int64),
     ]
 
 

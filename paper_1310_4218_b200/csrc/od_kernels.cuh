@@ -203,6 +203,38 @@ __global__ void __launch_bounds__(TX* TY)
 // Physics.  Grid (tiles); block (TX, TY); one thread per column.  B is field 0
 // of U^t (read-only this step, so the kernel is independent of jacobi_step).
 // ---------------------------------------------------------------------------
+// One column of the recurrence; returns its trip count (0 for threads outside
+// the chunk).  A(l) = f(B(l), A(l-1)), l = t mod nz for t = 1..T.
+__device__ __forceinline__ int physics_column(const ChunkDev& c, const TileDev& tile, int lx,
+                                              int ly, const double* __restrict__ cfield,
+                                              int32_t nx, int32_t ny, int32_t shift, int32_t nz,
+                                              int32_t n_inner) {
+  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
+  if (x >= c.w || y >= c.h) return 0;
+  int row = c.y0 + y - shift;
+  if (row < 0) row += ny;
+  const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + x);
+  int T = int(floor(__dmul_rn(double(nz), cm))) - 1;
+  if (T < 0) T = 0;
+  const int64_t ks = c.kstride;
+  const double* B = c.in + int64_t(y) * c.pitch + x;  // field 0 of U^t
+  double* A = c.a + int64_t(y) * c.pitch + x;
+  double a = A[0];
+  int ln = nz > 1 ? 1 : 0;
+  double bn = T >= 1 ? B[ln * ks] : 0.0;
+  for (int t = 1; t <= T; ++t) {
+    const int l = ln;
+    const double b = bn;
+    ln = l + 1 == nz ? 0 : l + 1;
+    if (t < T) bn = B[ln * ks];  // prefetch the next level
+    a = column_f(b, a, n_inner);
+    A[l * ks] = a;
+  }
+  return T;
+}
+
+// Physics.  Grid (tiles); block (TX, TY); one thread per column.  B is field 0
+// of U^t (read-only this step, so the kernel is independent of jacobi_step).
 template <int TX, int TY, bool TIMED, bool COUNT>
 __global__ void __launch_bounds__(TX* TY)
     physics_step(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
@@ -211,34 +243,9 @@ __global__ void __launch_bounds__(TX* TY)
                  unsigned long long* __restrict__ trips) {
   uint64_t t_start = 0;
   if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
-
   const TileDev tile = tiles[blockIdx.x];
-  const ChunkDev& c = chunks[tile.slot];
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
-  int T = 0;
-  if (x < c.w && y < c.h) {
-    int row = c.y0 + y - shift;
-    if (row < 0) row += ny;
-    const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + x);
-    T = int(floor(__dmul_rn(double(nz), cm))) - 1;
-    if (T < 0) T = 0;
-    const int64_t ks = c.kstride;
-    const double* B = c.in + int64_t(y) * c.pitch + x;  // field 0
-    double* A = c.a + int64_t(y) * c.pitch + x;
-    double a = A[0];
-    int l = 0;
-    int ln = nz > 1 ? 1 : 0;
-    double bn = T >= 1 ? B[ln * ks] : 0.0;
-    for (int t = 1; t <= T; ++t) {
-      l = ln;
-      const double b = bn;
-      ln = l + 1 == nz ? 0 : l + 1;
-      if (t < T) bn = B[ln * ks];  // prefetch the next level
-      a = column_f(b, a, n_inner);
-      A[l * ks] = a;
-    }
-  }
+  const int T = physics_column(chunks[tile.slot], tile, threadIdx.x, threadIdx.y, cfield, nx, ny,
+                               shift, nz, n_inner);
   if (COUNT) {
     unsigned long long v = (unsigned long long)T;
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -247,6 +254,34 @@ __global__ void __launch_bounds__(TX* TY)
   if (TIMED) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// Persistent physics: a few CTAs per SM pull tiles from a counter so the
+// kernel co-resides with jacobi_step (launched on another stream) instead of
+// occupying every SM slot: the FP64 pipe runs the recurrences while the
+// Jacobi streams HBM.
+template <int TX, int TY, bool TIMED>
+__global__ void __launch_bounds__(TX* TY)
+    physics_persistent(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                       int32_t ntiles, unsigned int* __restrict__ counter,
+                       const double* __restrict__ cfield, int32_t nx, int32_t ny, int32_t shift,
+                       int32_t nz, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  __shared__ int s_tile;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  for (;;) {
+    if (lead) s_tile = int(atomicAdd(counter, 1u));
+    __syncthreads();
+    const int ti = s_tile;
+    if (ti >= ntiles) break;
+    uint64_t t_start = 0;
+    if (TIMED && lead) t_start = globaltimer_ns();
+    const TileDev tile = tiles[ti];
+    physics_column(chunks[tile.slot], tile, threadIdx.x, threadIdx.y, cfield, nx, ny, shift, nz,
+                   n_inner);
+    __syncthreads();  // tile done (and s_tile consumed) before the next claim
+    if (TIMED && lead)
       atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
   }
 }

@@ -23,6 +23,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -136,6 +137,9 @@ class Runtime {
   int32_t cur_epoch_ = 1, cur_step_ = 0;
 
   cudaStream_t s0_ = nullptr;
+  cudaStream_t s1_ = nullptr;       // physics stream (overlap), higher priority
+  unsigned int* d_counter_ = nullptr;
+  int phys_ctas_ = 0;               // persistent physics grid
   ncclComm_t comm_ = nullptr;
   double* d_cbase_ = nullptr;   // base load field (device copy)
   double* d_cstage_ = nullptr;  // host-staged shifted field (host_io path)
@@ -223,6 +227,27 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
 
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0, sms = 0;
+    OD_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    OD_CU(cudaStreamCreateWithPriority(&s1_, cudaStreamNonBlocking, hi));
+    OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
+    phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
+    OD_CU(cudaMalloc(&d_counter_, sizeof(unsigned int)));
+    // Concurrent kernels can share an SM only with the same L1/smem split:
+    // give the co-scheduled kernels one carveout so the Jacobi CTAs fit next
+    // to the persistent physics CTAs.
+    const char* cv = std::getenv("OD_SMEM_CARVEOUT");
+    const int carve = cv ? std::atoi(cv) : 100;
+    auto set_carve = [&](const void* fn) {
+      OD_CU(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    };
+    set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, true>));
+    set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, false>));
+    set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, true>));
+    set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, false>));
+  }
   if (world_ > 1) {
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
@@ -250,6 +275,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
 Runtime::~Runtime() {
   cudaSetDevice(device_);
   if (s0_) cudaStreamSynchronize(s0_);
+  if (s1_) cudaStreamSynchronize(s1_);
   for (auto& m : chunks_)
     if (m.base) cudaFree(m.base);
   for (auto& kv : pool_) cudaFree(kv.second);
@@ -268,6 +294,8 @@ Runtime::~Runtime() {
   cudaFree(d_trips_);
   cudaFree(d_gather_);
   if (comm_) odb::nccl().CommDestroy(comm_);
+  cudaFree(d_counter_);
+  if (s1_) cudaStreamDestroy(s1_);
   if (s0_) cudaStreamDestroy(s0_);
 }
 
@@ -581,7 +609,53 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   const dim3 blk(kTX, kTY);
-  if (mode == kAsync || timer) {
+  if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap) {
+    // physics (FP64 pipe) on s1 concurrently with the Jacobi (HBM) on s0;
+    // both read U^t only, so the fork/join per step is the only ordering
+    const int ef = new_event(), ej = new_event();
+    OD_CU(cudaEventRecord(events_[ef], s0_));
+    OD_CU(cudaStreamWaitEvent(s1_, events_[ef], 0));
+    int p0 = -1, p1 = -1, j0 = -1, j1 = -1;
+    if (profiling_) {
+      p0 = new_event();
+      OD_CU(cudaEventRecord(events_[p0], s1_));
+    }
+    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s1_));
+    const int grid = std::min(phys_ctas_, ntiles_);
+    if (timer)
+      physics_persistent<kTX, kTY, true><<<grid, blk, 0, s1_>>>(
+          d_chunks_[par], d_tiles_, ntiles_, d_counter_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
+          cfg_.n_inner, ns);
+    else
+      physics_persistent<kTX, kTY, false><<<grid, blk, 0, s1_>>>(
+          d_chunks_[par], d_tiles_, ntiles_, d_counter_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
+          cfg_.n_inner, nullptr);
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      p1 = new_event();
+      OD_CU(cudaEventRecord(events_[p1], s1_));
+      prof_p_.push_back({p0, p1});
+      j0 = new_event();
+      OD_CU(cudaEventRecord(events_[j0], s0_));
+    }
+    if (timer)
+      jacobi_step<kTX, kTY, kPrefetch, true><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
+          d_chunks_[par], d_tiles_, cfg_.nz, ns);
+    else
+      jacobi_step<kTX, kTY, kPrefetch, false><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
+          d_chunks_[par], d_tiles_, cfg_.nz, nullptr);
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      j1 = new_event();
+      OD_CU(cudaEventRecord(events_[j1], s0_));
+      prof_j_.push_back({j0, j1});
+    }
+    OD_CU(cudaEventRecord(events_[ej], s1_));
+    OD_CU(cudaStreamWaitEvent(s0_, events_[ej], 0));
+    st_.kernel_launches += 2;
+    st_.jacobi_launches += 1;
+    st_.physics_launches += 1;
+  } else if (mode == kAsync || timer) {
     int e0 = -1, e1 = -1, e2 = -1;
     if (profiling_) {
       e0 = new_event();
@@ -686,6 +760,8 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
   }
   for (auto& p : prof_j_) st_.jacobi_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
   for (auto& p : prof_p_) st_.physics_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  st_.jacobi_timed += int64_t(prof_j_.size());
+  st_.physics_timed += int64_t(prof_p_.size());
   for (auto& p : prof_pack_) st_.pack_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
   for (auto& p : prof_x_) st_.exchange_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
 

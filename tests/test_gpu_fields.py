@@ -13,19 +13,20 @@ pytestmark = pytest.mark.gpu
 
 def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps_window=(2, 1),
           pattern=od.LoadPattern.UpperHalfHeavy, n_inner=5, adv=(0, 0, 1), threshold=1e30,
-          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0):
+          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0, overlap=False):
     return od.ExperimentConfig(
         cluster=od.ClusterSpec(nodes, ppn), domain=od.Domain(nx, ny, nz, F),
         decomposition=od.Decomposition(kind, kx, ky), window=od.MeasurementWindow(*steps_window),
         epochs=1000, pattern=pattern, heavy_value=heavy, light_value=1.0,
         advection=od.AdvectionSchedule(*adv),
         policy=od.BalancePolicy(od.Strategy.Greedy, od.Strategy.RefineSwap, threshold, 0.02),
-        seed=seed, n_inner=n_inner, measure=measure)
+        seed=seed, n_inner=n_inner, measure=measure, overlap=overlap)
 
 
-@pytest.mark.parametrize("kx,ky", [(1, 1), (4, 3), (2, 5)])
-def test_fields_bitwise_2d(kx, ky):
-    cfg = small(kx=kx, ky=ky)
+@pytest.mark.parametrize("kx,ky,overlap", [(1, 1, False), (4, 3, False), (2, 5, False),
+                                           (4, 3, True), (1, 1, True)])
+def test_fields_bitwise_2d(kx, ky, overlap):
+    cfg = small(kx=kx, ky=ky, overlap=overlap)
     U, A, _ = device_fields(cfg, 3)
     Uo, Ao = oracle_fields(cfg, 3)
     assert_bitwise(U, Uo, "U")
@@ -42,7 +43,7 @@ def test_fields_bitwise_1d_strips():
 
 def test_fields_multi_tile_chunks_and_advection():
     # chunks wider than one 32-column tile and taller than 8 rows; moving band
-    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3)
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=True)
     U, A, _ = device_fields(cfg, 5)
     Uo, Ao = oracle_fields(cfg, 5)
     assert_bitwise(U, Uo, "U")
@@ -62,7 +63,7 @@ def test_fields_invariant_under_balancing_and_procs():
     # 3 processors sharing the GPU, balancing every epoch: mapping changes,
     # values must not
     cfg = small(nx=64, ny=40, kx=4, ky=4, ppn=3, threshold=1.0, steps_window=(1, 1),
-                adv=(20, 2, 2))
+                adv=(20, 2, 2), overlap=True)
     U, A, recs = device_fields(cfg, 6, use_epochs=True)
     assert any(r.plan.moves for r in recs)
     Uo, Ao = oracle_fields(cfg, 6)
