@@ -155,7 +155,8 @@ typedef struct od_config {
   /* B200 path parameters (no reference counterpart) */
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
   int32_t measure;      /* OD_MEASURE_EVENTS | OD_MEASURE_TIMER */
-  int32_t overlap;      /* 1: physics and Jacobi run concurrently in async steps */
+  int32_t overlap;      /* kernel mode: 0 Jacobi then physics (two launches),
+                           1 the two kernels on two streams, 2 fused column_step */
   int32_t reserved_[5];
 } od_config;
 
@@ -241,6 +242,8 @@ typedef struct od_rt_stats {
   int32_t resident_chunks;
   int32_t pad_;
   int64_t jacobi_timed, physics_timed; /* launches whose event time is in *_ms */
+  double fused_ms;
+  int64_t fused_launches, fused_timed;
 } od_rt_stats;
 int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
 /* one row per completed epoch (od_rt_run_epoch, od_rt_advance, ..._host) */

@@ -86,6 +86,7 @@ class od_rt_stats(C.Structure):
         ("physics_trips", C.c_int64),
         ("resident_chunks", C.c_int32), ("pad_", C.c_int32),
         ("jacobi_timed", C.c_int64), ("physics_timed", C.c_int64),
+        ("fused_ms", C.c_double), ("fused_launches", C.c_int64), ("fused_timed", C.c_int64),
     ]
 
 

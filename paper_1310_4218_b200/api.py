@@ -503,7 +503,9 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     seed: int = 1
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
-    overlap: bool = False
+    # kernel mode: 0 Jacobi then physics, 1 two streams, 2 fused (1 column/thread),
+    # 3 fused pair kernel, 4 fused pair kernel v2 (default)
+    overlap: int = 4
 
     def vp_count(self) -> int:
         return self.decomposition.vp_count()

@@ -47,7 +47,7 @@ struct TileDev {
 };
 
 struct PackJob {
-  int32_t slot, side, len, pad;  // side: which edge of the source chunk
+  int32_t slot, side, len, lenp;  // side: which edge of the source chunk; lenp: row stride
   int64_t dst;                   // element offset into the send buffer
 };
 
@@ -71,6 +71,10 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
@@ -287,6 +291,612 @@ __global__ void __launch_bounds__(TX* TY)
 }
 
 // ---------------------------------------------------------------------------
+// Fused step.  On B200 a kernel that saturates the FP64 pipe starves every
+// co-resident warp that needs that pipe (tools/overlap_probe.cu: a copy with 7
+// FP64 ops/element drops from 4.0 TB/s to 0.8 TB/s next to an FP64-FMA kernel),
+// so running the physics and the Jacobi as two concurrent kernels does not
+// overlap them.  Here the SAME warps interleave both: after every Jacobi level
+// step (one plane of one field) each thread advances its column recurrence by
+// a fixed quota of work units, so the Jacobi's loads are in flight while the
+// FP64 pipe runs the recurrence.  Results are bitwise identical to running
+// jacobi_step and physics_step back to back (same operations, same order per
+// value).  Grid (tiles); block (TX, TY).
+// ---------------------------------------------------------------------------
+struct ColumnState {
+  const double* B;  // field 0 of U^t at this column
+  double* A;
+  int64_t ks;
+  int T, t, i, l, nz, n_inner;
+  double a, y, eb, bn;
+};
+
+__device__ __forceinline__ void physics_init(ColumnState& s, const ChunkDev& c, int x, int y,
+                                             const double* __restrict__ cfield, int32_t nx,
+                                             int32_t ny, int32_t shift, int32_t nz,
+                                             int32_t n_inner) {
+  int row = c.y0 + y - shift;
+  if (row < 0) row += ny;
+  const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + x);
+  int T = int(floor(__dmul_rn(double(nz), cm))) - 1;
+  s.T = T < 0 ? 0 : T;
+  s.ks = c.kstride;
+  s.B = c.in + int64_t(y) * c.pitch + x;
+  s.A = c.a + int64_t(y) * c.pitch + x;
+  s.nz = nz;
+  s.n_inner = n_inner;
+  s.t = 1;
+  s.i = 0;
+  s.l = nz > 1 ? 1 : 0;
+  s.a = s.A[0];
+  s.y = 0.0;
+  s.eb = 0.0;
+  s.bn = s.T >= 1 ? s.B[s.l * s.ks] : 0.0;
+}
+
+// Advance by `budget` work units: a trip is 1 setup unit + n_inner micro-steps.
+// Callers pass budgets that are multiples of 8 (or "everything") so the common
+// case -- the budget ends inside the current trip -- is a fully unrolled loop.
+__device__ __forceinline__ void physics_advance(ColumnState& s, int budget) {
+  if (s.i > 0 && s.i + budget <= s.n_inner) {
+    double y = s.y;
+    const double eb = s.eb;
+    for (int j = 0; j < budget; j += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double u = __fma_rn(-y, y, y);
+        y = __fma_rn(kR, u, eb);
+      }
+    }
+    s.y = y;
+    s.i += budget;
+    return;
+  }
+  while (budget > 0 && s.t <= s.T) {
+    if (s.i == 0) {
+      const double b = s.bn;
+      const double hb = __dmul_rn(0.5, b);
+      s.eb = __fma_rn(b, kEps, kEps);
+      s.y = __fma_rn(0.5, s.a, hb);
+      s.i = 1;
+      --budget;
+      const int ln = s.l + 1 == s.nz ? 0 : s.l + 1;
+      if (s.t < s.T) s.bn = s.B[ln * s.ks];
+    }
+    const int m = min(budget, s.n_inner + 1 - s.i);
+    double y = s.y;
+    const double eb = s.eb;
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) {
+      const double u = __fma_rn(-y, y, y);
+      y = __fma_rn(kR, u, eb);
+    }
+    s.y = y;
+    s.i += m;
+    budget -= m;
+    if (s.i == s.n_inner + 1) {
+      s.a = y;
+      s.A[s.l * s.ks] = y;
+      s.l = s.l + 1 == s.nz ? 0 : s.l + 1;
+      ++s.t;
+      s.i = 0;
+    }
+  }
+}
+
+// Running pointer over the (field, level) planes of one column: +ks inside a
+// field, +(fs - (nz-1) ks) from the last level of a field to the next field.
+struct PlaneWalker {
+  const double* p;
+  int64_t step, wrap;
+  __device__ __forceinline__ void next(bool last_level) { p += last_level ? wrap : step; }
+};
+
+template <int TX, int TY, int S, bool TIMED>
+__global__ void __launch_bounds__(TX* TY, 4)
+    column_step(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  constexpr int R = 8;  // ring slots (power of two); S + 2 <= R
+  constexpr int PW = TX + 2;
+  constexpr int PLANE = (TY + 2) * PW;
+  static_assert(S + 2 <= R, "prefetch depth too large for the ring");
+  __shared__ __align__(16) double ring[R * PLANE];
+
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const TileDev tile = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[tile.slot];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride, fs = c.fstride;
+  const int wv = min(TX, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
+  const bool act = lx < wv && ly < hv;
+  const int64_t own = int64_t(y) * pitch + x;
+  const int64_t wrap = fs - int64_t(nz - 1) * ks;
+
+  // global sources (running pointers) and smem destinations of this thread
+  const double* pc = c.in + own;
+  const double* px = nullptr;
+  const double* py = nullptr;
+  int64_t xstep = 0, xwrap = 0, ystep = 0, ywrap = 0;
+  int ox = 0, oy = 0;
+  if (ly < hv && (lx == 0 || lx == TX - 1)) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    ox = (ly + 1) * PW + (left ? 0 : wv + 1);
+    if (xs >= 0 && xs < w) {
+      px = c.in + int64_t(y) * pitch + xs;
+      xstep = ks;
+      xwrap = wrap;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      px = fd.p + int64_t(y) * fd.es;
+      xstep = fd.ks;
+      xwrap = fd.fs - int64_t(nz - 1) * fd.ks;
+    }
+  }
+  if (lx < wv && (ly == 0 || ly == TY - 1)) {
+    const bool top = ly == 0;
+    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
+    oy = (top ? 0 : hv + 1) * PW + lx + 1;
+    if (ys >= 0 && ys < h) {
+      py = c.in + int64_t(ys) * pitch + x;
+      ystep = ks;
+      ywrap = wrap;
+    } else {
+      const FaceDev& fd = c.face[top ? kTop : kBottom];
+      py = fd.p + int64_t(x) * fd.es;
+      ystep = fd.ks;
+      ywrap = fd.fs - int64_t(nz - 1) * fd.ks;
+    }
+  }
+  const int oc = (ly + 1) * PW + lx + 1;
+
+  const int levels = F * nz;
+  int ki = 0;  // level (within its field) of the next plane to issue
+  auto issue = [&](int L) {
+    if (L < levels) {
+      double* slot = ring + (L & (R - 1)) * PLANE;
+      if (act) cp_async8(slot + oc, pc);
+      if (px) cp_async8(slot + ox, px);
+      if (py) cp_async8(slot + oy, py);
+      const bool last = ki == nz - 1;
+      pc += last ? wrap : ks;
+      px += last ? xwrap : xstep;
+      py += last ? ywrap : ystep;
+      ki = last ? 0 : ki + 1;
+    }
+    cp_async_commit();
+  };
+
+  ColumnState st;
+  int quota = 0;
+  if (act) {
+    physics_init(st, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+    const int64_t units = int64_t(st.T) * (n_inner + 1);
+    quota = int((units + levels - 1) / levels);
+    quota = (quota + 7) & ~7;
+  }
+
+#pragma unroll
+  for (int L = 0; L < S; ++L) issue(L);
+
+  double* pout = c.out + own;
+  const double* rc = ring + oc;
+  double zm = 0.0;
+  int k = 0;
+  for (int L = 0; L < levels; ++L) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    issue(L + S);
+    const bool last = k == nz - 1;
+    if (act) {
+      const double* pl = rc + (L & (R - 1)) * PLANE;
+      const double uc = pl[0];
+      const double xm = pl[-1];
+      const double xp = pl[1];
+      const double ym = pl[-PW];
+      const double yp = pl[PW];
+      const double zd = k > 0 ? zm : uc;
+      const double zu = last ? uc : rc[((L + 1) & (R - 1)) * PLANE];
+      const double sum =
+          __dadd_rn(__dadd_rn(__dadd_rn(xm, xp), __dadd_rn(ym, yp)), __dadd_rn(zd, zu));
+      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
+      zm = uc;
+      physics_advance(st, quota);
+    }
+    pout += last ? wrap : ks;
+    k = last ? 0 : k + 1;
+  }
+  cp_async_wait<0>();
+  if (act) physics_advance(st, 0x7fffffff);
+
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// Two chains side by side in the common case (both inside a trip with the
+// same budget): independent DFMA chains give the FP64 pipe ILP 2 per thread.
+__device__ __forceinline__ void physics_advance2(ColumnState& s0, int b0, ColumnState& s1,
+                                                 int b1) {
+  if (b0 == b1 && s0.i > 0 && s1.i > 0 && s0.i + b0 <= s0.n_inner && s1.i + b1 <= s1.n_inner) {
+    double y0 = s0.y, y1 = s1.y;
+    const double e0 = s0.eb, e1 = s1.eb;
+    for (int j = 0; j < b0; j += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double u0 = __fma_rn(-y0, y0, y0);
+        const double u1 = __fma_rn(-y1, y1, y1);
+        y0 = __fma_rn(kR, u0, e0);
+        y1 = __fma_rn(kR, u1, e1);
+      }
+    }
+    s0.y = y0;
+    s1.y = y1;
+    s0.i += b0;
+    s1.i += b1;
+    return;
+  }
+  physics_advance(s0, b0);
+  physics_advance(s1, b1);
+}
+
+// Fused step with two adjacent columns per thread: tile 64 x TY columns, 16-byte
+// plane loads and stores, two physics chains per thread.  Same arithmetic as
+// column_step / jacobi_step + physics_step.
+template <int TY, int S, bool TIMED, int MINB = 3>
+__global__ void __launch_bounds__(32 * TY, MINB)
+    column_step2(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  constexpr int R = 8;
+  constexpr int TXC = 64;
+  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
+  constexpr int PLANE = (TY + 2) * PW;
+  static_assert(S + 2 <= R, "prefetch depth too large for the ring");
+  __shared__ __align__(16) double ring[R * PLANE];
+
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const TileDev tile = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[tile.slot];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride, fs = c.fstride;
+  const int wv = min(TXC, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
+  const int ncell = ly < hv ? max(0, min(2, wv - 2 * lx)) : 0;  // active cells of the pair
+  const int64_t own = int64_t(y) * pitch + x;
+  const int64_t wrap = fs - int64_t(nz - 1) * ks;
+
+  const double* pc = c.in + own;
+  const double* px = nullptr;
+  const double* py = nullptr;
+  int64_t xstep = 0, xwrap = 0, ystep = 0, ywrap = 0;
+  int ox = 0, oy = 0, ny_cells = 0;
+  if (ly < hv && (lx == 0 || lx == 31)) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    ox = (ly + 1) * PW + (left ? 1 : wv + 2);
+    if (xs >= 0 && xs < w) {
+      px = c.in + int64_t(y) * pitch + xs;
+      xstep = ks;
+      xwrap = wrap;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      px = fd.p + int64_t(y) * fd.es;
+      xstep = fd.ks;
+      xwrap = fd.fs - int64_t(nz - 1) * fd.ks;
+    }
+  }
+  const int ycells = max(0, min(2, wv - 2 * lx));
+  if (ycells > 0 && (ly == 0 || ly == TY - 1)) {
+    const bool top = ly == 0;
+    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
+    oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
+    ny_cells = ycells;
+    if (ys >= 0 && ys < h) {
+      py = c.in + int64_t(ys) * pitch + x;
+      ystep = ks;
+      ywrap = wrap;
+    } else {
+      const FaceDev& fd = c.face[top ? kTop : kBottom];
+      py = fd.p + int64_t(x) * fd.es;
+      ystep = fd.ks;
+      ywrap = fd.fs - int64_t(nz - 1) * fd.ks;
+    }
+  }
+  const int oc = (ly + 1) * PW + 2 + 2 * lx;
+
+  const int levels = F * nz;
+  int ki = 0;
+  auto issue = [&](int L) {
+    if (L < levels) {
+      double* slot = ring + (L & (R - 1)) * PLANE;
+      if (ncell == 2) cp_async16(slot + oc, pc);
+      else if (ncell == 1) cp_async8(slot + oc, pc);
+      if (px) cp_async8(slot + ox, px);
+      if (ny_cells == 2) cp_async16(slot + oy, py);
+      else if (ny_cells == 1) cp_async8(slot + oy, py);
+      const bool last = ki == nz - 1;
+      pc += last ? wrap : ks;
+      px += last ? xwrap : xstep;
+      py += last ? ywrap : ystep;
+      ki = last ? 0 : ki + 1;
+    }
+    cp_async_commit();
+  };
+
+  ColumnState s0, s1;
+  int q0 = 0, q1 = 0;
+  if (ncell >= 1) {
+    physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+    q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
+    q0 = (q0 + 7) & ~7;
+  }
+  if (ncell == 2) {
+    physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
+    q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
+    q1 = (q1 + 7) & ~7;
+  }
+
+#pragma unroll
+  for (int L = 0; L < S; ++L) issue(L);
+
+  double* pout = c.out + own;
+  const double* rc = ring + oc;
+  double zm0 = 0.0, zm1 = 0.0;
+  int k = 0;
+  for (int L = 0; L < levels; ++L) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    issue(L + S);
+    const bool last = k == nz - 1;
+    if (ncell == 2) {
+      const double* pl = rc + (L & (R - 1)) * PLANE;
+      const double2 uc = *reinterpret_cast<const double2*>(pl);
+      const double xl = pl[-1], xr = pl[2];
+      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
+      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
+      double2 zu = uc;
+      if (!last) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
+      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                  __dadd_rn(zd0, zu.x));
+      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                  __dadd_rn(zd1, zu.y));
+      double2 o;
+      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+      __stcs(reinterpret_cast<double2*>(pout), o);
+      zm0 = uc.x;
+      zm1 = uc.y;
+      physics_advance2(s0, q0, s1, q1);
+    } else if (ncell == 1) {
+      const double* pl = rc + (L & (R - 1)) * PLANE;
+      const double uc = pl[0];
+      const double zu = last ? uc : rc[((L + 1) & (R - 1)) * PLANE];
+      const double zd = k > 0 ? zm0 : uc;
+      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
+                                   __dadd_rn(zd, zu));
+      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
+      zm0 = uc;
+      physics_advance(s0, q0);
+    }
+    pout += last ? wrap : ks;
+    k = last ? 0 : k + 1;
+  }
+  cp_async_wait<0>();
+  if (ncell >= 1) physics_advance(s0, 0x7fffffff);
+  if (ncell == 2) physics_advance(s1, 0x7fffffff);
+
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// Calls of physics_advance(s, budget) that stay inside the current trip.
+__device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
+  return (s.i > 0 && budget > 0 && s.t <= s.T) ? (s.n_inner - s.i) / budget : 0;
+}
+
+// Pair kernel, second generation: two levels per barrier, uniform plane
+// strides (fs == nz * ks holds for chunk buffers, neighbour faces and packed
+// receive faces alike, so every walker is p += ks), and a countdown that keeps
+// the two physics chains on the branch-free interleaved loop between trip
+// boundaries.  Same arithmetic as every other path.
+template <int TY, int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(32 * TY, MINB)
+    column_step3(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  constexpr int R = 8;
+  constexpr int TXC = 64;
+  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
+  constexpr int PLANE = (TY + 2) * PW;
+  static_assert(S + 2 <= R && S >= 3, "prefetch depth");
+  __shared__ __align__(16) double ring[R * PLANE];
+
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const TileDev tile = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[tile.slot];
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride;
+  const int wv = min(TXC, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
+  const int pair = max(0, min(2, wv - 2 * lx));  // cells of this thread's pair inside the chunk
+  const int ncell = ly < hv ? pair : 0;
+  const int64_t own = int64_t(y) * pitch + x;
+
+  const double* pc = c.in + own;
+  const double* px = nullptr;
+  const double* py = nullptr;
+  int64_t xstep = 0, ystep = 0;
+  int ox = 0, oy = 0, ny_cells = 0;
+  if (ly < hv && (lx == 0 || lx == 31)) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    ox = (ly + 1) * PW + (left ? 1 : wv + 2);
+    if (xs >= 0 && xs < w) {
+      px = c.in + int64_t(y) * pitch + xs;
+      xstep = ks;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      px = fd.p + int64_t(y) * fd.es;
+      xstep = fd.ks;
+    }
+  }
+  if (pair > 0 && (ly == 0 || ly == TY - 1)) {
+    const bool top = ly == 0;
+    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
+    oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
+    ny_cells = pair;
+    if (ys >= 0 && ys < h) {
+      py = c.in + int64_t(ys) * pitch + x;
+      ystep = ks;
+    } else {
+      const FaceDev& fd = c.face[top ? kTop : kBottom];
+      py = fd.p + int64_t(x) * fd.es;
+      ystep = fd.ks;
+    }
+  }
+  const int oc = (ly + 1) * PW + 2 + 2 * lx;
+  const int levels = F * nz;
+
+  auto issue = [&](int L) {
+    if (L < levels) {
+      double* slot = ring + (L & (R - 1)) * PLANE;
+      if (ncell == 2) cp_async16(slot + oc, pc);
+      else if (ncell == 1) cp_async8(slot + oc, pc);
+      if (px) cp_async8(slot + ox, px);
+      if (ny_cells == 2) cp_async16(slot + oy, py);
+      else if (ny_cells == 1) cp_async8(slot + oy, py);
+      pc += ks;
+      px += xstep;
+      py += ystep;
+    }
+    cp_async_commit();
+  };
+
+  ColumnState s0, s1;
+  int q0 = 0, q1 = 0;
+  if (ncell >= 1) {
+    physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+    q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
+    q0 = (q0 + 7) & ~7;
+  }
+  if (ncell == 2) {
+    physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
+    q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
+    q1 = (q1 + 7) & ~7;
+  }
+  int fast = 0;  // interleaved iterations left before a trip boundary
+  auto physics = [&](int b0, int b1) {
+    if (fast > 0) {
+      double y0 = s0.y, y1 = s1.y;
+      const double e0 = s0.eb, e1 = s1.eb;
+      for (int j = 0; j < b0; j += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double u0 = __fma_rn(-y0, y0, y0);
+          const double u1 = __fma_rn(-y1, y1, y1);
+          y0 = __fma_rn(kR, u0, e0);
+          y1 = __fma_rn(kR, u1, e1);
+        }
+      }
+      s0.y = y0;
+      s1.y = y1;
+      s0.i += b0;
+      s1.i += b0;
+      --fast;
+      return;
+    }
+    if (ncell >= 1) physics_advance(s0, b0);
+    if (ncell == 2) {
+      physics_advance(s1, b1);
+      if (b0 == b1) fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
+    }
+  };
+
+  // one level of one field for this thread's cells (plane in slot L & 7)
+  double zm0 = 0.0, zm1 = 0.0;
+  double* pout = c.out + own;
+  const double* rc = ring + oc;
+  auto level = [&](int L, int k) {
+    const double* pl = rc + (L & (R - 1)) * PLANE;
+    if (ncell == 2) {
+      const double2 uc = *reinterpret_cast<const double2*>(pl);
+      const double xl = pl[-1], xr = pl[2];
+      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
+      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
+      double2 zu = uc;
+      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
+      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                  __dadd_rn(zd0, zu.x));
+      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                  __dadd_rn(zd1, zu.y));
+      double2 o;
+      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+      __stcs(reinterpret_cast<double2*>(pout), o);
+      zm0 = uc.x;
+      zm1 = uc.y;
+    } else if (ncell == 1) {
+      const double uc = pl[0];
+      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
+      const double zd = k > 0 ? zm0 : uc;
+      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
+                                   __dadd_rn(zd, zu));
+      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
+      zm0 = uc;
+    }
+    pout += ks;
+  };
+
+#pragma unroll
+  for (int L = 0; L < S; ++L) issue(L);
+
+  int k = 0, L = 0;
+  for (; L + 1 < levels; L += 2) {
+    cp_async_wait<S - 3>();  // planes <= L+2 landed
+    __syncthreads();
+    issue(L + S);
+    issue(L + S + 1);
+    level(L, k);
+    if (++k == nz) k = 0;
+    level(L + 1, k);
+    if (++k == nz) k = 0;
+    physics(2 * q0, 2 * q1);
+  }
+  if (L < levels) {
+    cp_async_wait<0>();
+    __syncthreads();
+    level(L, k);
+  }
+  cp_async_wait<0>();
+  if (ncell >= 1) physics_advance(s0, 0x7fffffff);
+  if (ncell == 2) physics_advance(s1, 0x7fffffff);
+
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Face packing: grid (jobs, F); the strip of one field, all levels.
 // Send layout per face: [f][k][e].
 // ---------------------------------------------------------------------------
@@ -303,11 +913,11 @@ __global__ void pack_faces(const ChunkDev* __restrict__ chunks, const PackJob* _
     case kTop: off = 0; es = 1; break;
     default: off = int64_t(c.h - 1) * c.pitch; es = 1; break;
   }
-  double* out = sendbuf + j.dst + int64_t(f) * nz * j.len;
+  double* out = sendbuf + j.dst + int64_t(f) * nz * j.lenp;
   const int64_t n = int64_t(nz) * j.len;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t k = i / j.len, e = i - k * j.len;
-    out[i] = base[off + k * c.kstride + e * es];
+    out[k * j.lenp + e] = base[off + k * c.kstride + e * es];
   }
 }
 

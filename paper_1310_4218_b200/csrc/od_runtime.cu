@@ -53,7 +53,7 @@ namespace odb {
                          #expr);                                                         \
   } while (0)
 
-constexpr int kTX = 32, kTY = 8, kPrefetch = 4;
+constexpr int kTX = 32, kTY = 8, kPrefetch = 4, kFusedPrefetch = 6;
 
 static int opposite(int d) { return d ^ 1; }
 
@@ -150,6 +150,11 @@ class Runtime {
   std::vector<int32_t> resident_;  // slot -> vp
   std::vector<int32_t> tile_begin_, tile_count_;
   int32_t ntiles_ = 0;
+  // 64-column tiles of the pair kernel (column_step2)
+  std::vector<int32_t> tile2_begin_, tile2_count_;
+  int32_t ntiles2_ = 0;
+  TileDev* d_tiles2_ = nullptr;
+  size_t d_tiles2_cap_ = 0;
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
   size_t d_chunks_cap_[2] = {0, 0};
   TileDev* d_tiles_ = nullptr;
@@ -174,7 +179,7 @@ class Runtime {
   size_t gather_cap_ = 0;
   // stats
   bool profiling_ = false;
-  std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_;
+  std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_, prof_f_;
   od_rt_stats st_{};
   std::vector<od_epoch_summary> history_;
 };
@@ -209,6 +214,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       cfg.later_call_strategy < 0 || cfg.later_call_strategy > 1)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
+  if (cfg.overlap < 0 || cfg.overlap > 4) throw ValidationError("unknown kernel mode (overlap)");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER)
     throw ValidationError("unknown measurement mode");
   if (world != cfg.nodes)
@@ -287,6 +293,7 @@ Runtime::~Runtime() {
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
   cudaFree(d_tiles_);
+  cudaFree(d_tiles2_);
   cudaFree(d_jobs_);
   cudaFree(d_send_);
   cudaFree(d_recv_);
@@ -413,6 +420,18 @@ void Runtime::rebuild_tables() {
   }
   ntiles_ = int32_t(tiles.size());
   upload(d_tiles_, d_tiles_cap_, tiles);
+  std::vector<TileDev> tiles2;
+  tile2_begin_.assign(nres, 0);
+  tile2_count_.assign(nres, 0);
+  for (int32_t i = 0; i < nres; ++i) {
+    const Sub& s = subs_[resident_[i]];
+    tile2_begin_[i] = int32_t(tiles2.size());
+    for (int32_t ty = 0; ty < s.h(); ty += kTY)
+      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) tiles2.push_back(TileDev{i, tx, ty, 0});
+    tile2_count_[i] = int32_t(tiles2.size()) - tile2_begin_[i];
+  }
+  ntiles2_ = int32_t(tiles2.size());
+  upload(d_tiles2_, d_tiles2_cap_, tiles2);
 
   // exchange schedule: per peer, faces in (sender vp, side) order
   jobs_.clear();
@@ -432,8 +451,9 @@ void Runtime::rebuild_tables() {
         const int32_t n = nbr(v, d);
         if (n < 0 || rank_of_vp(n) != q) continue;
         const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
-        jobs_.push_back(PackJob{slot_of[v], d, len, 0, soff});
-        soff += per_cell * len;
+        const int32_t lenp = (len + 1) & ~1;  // even row stride: 16-byte aligned pairs
+        jobs_.push_back(PackJob{slot_of[v], d, len, lenp, soff});
+        soff += per_cell * lenp;
       }
     send_cnt_[q] = soff - send_off_[q];
     for (int32_t v = 0; v < K(); ++v) {
@@ -443,7 +463,7 @@ void Runtime::rebuild_tables() {
         if (n < 0 || rank_of_vp(n) != rank_) continue;
         const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
         recv_face_off_[slot_of[n]][opposite(d)] = roff;
-        roff += per_cell * len;
+        roff += per_cell * ((len + 1) & ~1);
       }
     }
     recv_cnt_[q] = roff - recv_off_[q];
@@ -489,8 +509,9 @@ void Runtime::rebuild_tables() {
         } else {
           const int32_t len = (d == kLeft || d == kRight) ? c.h : c.w;
           c.face[d].p = d_recv_ + recv_face_off_[i][d];
-          c.face[d].fs = int64_t(cfg_.nz) * len;
-          c.face[d].ks = len;
+          const int32_t lenp = (len + 1) & ~1;
+          c.face[d].fs = int64_t(cfg_.nz) * lenp;
+          c.face[d].ks = lenp;
           c.face[d].es = 1;
         }
       }
@@ -525,6 +546,7 @@ void Runtime::begin_window() {
   ns_used_ = 0;
   prof_j_.clear();
   prof_p_.clear();
+  prof_f_.clear();
   prof_pack_.clear();
   prof_x_.clear();
 }
@@ -609,7 +631,83 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   const dim3 blk(kTX, kTY);
-  if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap) {
+  if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 3) {
+    int e0 = -1, e1 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    static const int variant = std::getenv("OD_FUSED_MINB") ? std::atoi(std::getenv("OD_FUSED_MINB")) : 3;
+#define OD_LAUNCH_CS2(MB)                                                                  \
+  if (timer)                                                                              \
+    column_step2<kTY, kFusedPrefetch, true, MB><<<ntiles2_, blk, 0, s0_>>>(               \
+        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
+        cfg_.n_inner, ns);                                                                \
+  else                                                                                    \
+    column_step2<kTY, kFusedPrefetch, false, MB><<<ntiles2_, blk, 0, s0_>>>(              \
+        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
+        cfg_.n_inner, nullptr);
+    if (variant == 2) { OD_LAUNCH_CS2(2) } else if (variant == 4) { OD_LAUNCH_CS2(4) } else { OD_LAUNCH_CS2(3) }
+#undef OD_LAUNCH_CS2
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+      prof_f_.push_back({e0, e1});
+    }
+    st_.kernel_launches += 1;
+    st_.fused_launches += 1;
+  } else if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 4) {
+    int e0 = -1, e1 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    static const int variant3 =
+        std::getenv("OD_FUSED_MINB") ? std::atoi(std::getenv("OD_FUSED_MINB")) : 3;
+#define OD_LAUNCH_CS3(MB)                                                                  \
+  if (timer)                                                                              \
+    column_step3<kTY, kFusedPrefetch, true, MB><<<ntiles2_, blk, 0, s0_>>>(               \
+        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
+        cfg_.n_inner, ns);                                                                \
+  else                                                                                    \
+    column_step3<kTY, kFusedPrefetch, false, MB><<<ntiles2_, blk, 0, s0_>>>(              \
+        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
+        cfg_.n_inner, nullptr);
+    if (variant3 == 2) { OD_LAUNCH_CS3(2) } else { OD_LAUNCH_CS3(3) }
+#undef OD_LAUNCH_CS3
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+      prof_f_.push_back({e0, e1});
+    }
+    st_.kernel_launches += 1;
+    st_.fused_launches += 1;
+  } else if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap == 2) {
+    // fused: Jacobi level steps and the column recurrence in the same warps
+    int e0 = -1, e1 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    if (timer)
+      column_step<kTX, kTY, kFusedPrefetch, true><<<ntiles_, blk, 0, s0_>>>(
+          d_chunks_[par], d_tiles_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+          cfg_.n_inner, ns);
+    else
+      column_step<kTX, kTY, kFusedPrefetch, false><<<ntiles_, blk, 0, s0_>>>(
+          d_chunks_[par], d_tiles_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+          cfg_.n_inner, nullptr);
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+      prof_f_.push_back({e0, e1});
+    }
+    st_.kernel_launches += 1;
+    st_.fused_launches += 1;
+  } else if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap == 1) {
     // physics (FP64 pipe) on s1 concurrently with the Jacobi (HBM) on s0;
     // both read U^t only, so the fork/join per step is the only ordering
     const int ef = new_event(), ej = new_event();
@@ -699,12 +797,26 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     for (int32_t i = 0; i < nres; ++i) {
       const int eb = new_event(), ee = new_event();
       OD_CU(cudaEventRecord(events_[eb], s0_));
-      jacobi_step<kTX, kTY, kPrefetch, false>
-          <<<dim3(tile_count_[i], cfg_.fields), blk, 0, s0_>>>(
-              d_chunks_[par], d_tiles_ + tile_begin_[i], cfg_.nz, nullptr);
-      physics_step<kTX, kTY, false, false><<<tile_count_[i], blk, 0, s0_>>>(
-          d_chunks_[par], d_tiles_ + tile_begin_[i], cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
-          cfg_.n_inner, nullptr, nullptr);
+      if (cfg_.overlap == 4) {
+        column_step3<kTY, kFusedPrefetch, false, 3><<<tile2_count_[i], blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      } else if (cfg_.overlap == 3) {
+        column_step2<kTY, kFusedPrefetch, false><<<tile2_count_[i], blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      } else if (cfg_.overlap == 2) {
+        column_step<kTX, kTY, kFusedPrefetch, false><<<tile_count_[i], blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_ + tile_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      } else {
+        jacobi_step<kTX, kTY, kPrefetch, false>
+            <<<dim3(tile_count_[i], cfg_.fields), blk, 0, s0_>>>(
+                d_chunks_[par], d_tiles_ + tile_begin_[i], cfg_.nz, nullptr);
+        physics_step<kTX, kTY, false, false><<<tile_count_[i], blk, 0, s0_>>>(
+            d_chunks_[par], d_tiles_ + tile_begin_[i], cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
+            cfg_.n_inner, nullptr, nullptr);
+      }
       OD_CU(cudaGetLastError());
       OD_CU(cudaEventRecord(events_[ee], s0_));
       st_.kernel_launches += 2;
@@ -760,6 +872,8 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
   }
   for (auto& p : prof_j_) st_.jacobi_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
   for (auto& p : prof_p_) st_.physics_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  for (auto& p : prof_f_) st_.fused_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;
+  st_.fused_timed += int64_t(prof_f_.size());
   st_.jacobi_timed += int64_t(prof_j_.size());
   st_.physics_timed += int64_t(prof_p_.size());
   for (auto& p : prof_pack_) st_.pack_ms += elapsed_s(events_[p.first], events_[p.second]) * 1e3;

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps_window=(2, 1),
           pattern=od.LoadPattern.UpperHalfHeavy, n_inner=5, adv=(0, 0, 1), threshold=1e30,
-          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0, overlap=False):
+          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0, overlap=2):
     return od.ExperimentConfig(
         cluster=od.ClusterSpec(nodes, ppn), domain=od.Domain(nx, ny, nz, F),
         decomposition=od.Decomposition(kind, kx, ky), window=od.MeasurementWindow(*steps_window),
@@ -23,8 +23,9 @@ def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps
         seed=seed, n_inner=n_inner, measure=measure, overlap=overlap)
 
 
-@pytest.mark.parametrize("kx,ky,overlap", [(1, 1, False), (4, 3, False), (2, 5, False),
-                                           (4, 3, True), (1, 1, True)])
+@pytest.mark.parametrize("kx,ky,overlap", [(1, 1, 0), (4, 3, 0), (2, 5, 0), (4, 3, 1), (1, 1, 1),
+                                           (1, 1, 2), (4, 3, 2), (2, 5, 2), (1, 1, 3), (4, 3, 3),
+                                           (2, 5, 3), (1, 1, 4), (4, 3, 4), (2, 5, 4)])
 def test_fields_bitwise_2d(kx, ky, overlap):
     cfg = small(kx=kx, ky=ky, overlap=overlap)
     U, A, _ = device_fields(cfg, 3)
@@ -33,8 +34,9 @@ def test_fields_bitwise_2d(kx, ky, overlap):
     assert_bitwise(A, Ao, "A")
 
 
-def test_fields_bitwise_1d_strips():
-    cfg = small(nx=45, ny=30, kind=ONE_D, kx=1, ky=7)
+@pytest.mark.parametrize("overlap", [0, 2, 3, 4])
+def test_fields_bitwise_1d_strips(overlap):
+    cfg = small(nx=45, ny=30, kind=ONE_D, kx=1, ky=7, overlap=overlap)
     U, A, _ = device_fields(cfg, 4)
     Uo, Ao = oracle_fields(cfg, 4)
     assert_bitwise(U, Uo, "U")
@@ -43,16 +45,18 @@ def test_fields_bitwise_1d_strips():
 
 def test_fields_multi_tile_chunks_and_advection():
     # chunks wider than one 32-column tile and taller than 8 rows; moving band
-    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=True)
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=4)
     U, A, _ = device_fields(cfg, 5)
     Uo, Ao = oracle_fields(cfg, 5)
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")
 
 
-def test_fields_edge_shapes():
+@pytest.mark.parametrize("overlap,n_inner", [(0, 5), (2, 5), (2, 0), (2, 40), (3, 5), (3, 0),
+                                             (3, 40), (4, 5), (4, 0), (4, 40)])
+def test_fields_edge_shapes(overlap, n_inner):
     # nz = 1 (no vertical neighbours, physics trips 0 or 1), single field
-    cfg = small(nx=33, ny=9, nz=1, F=1, kx=3, ky=2, heavy=3.0)
+    cfg = small(nx=33, ny=9, nz=1, F=1, kx=3, ky=2, heavy=3.0, overlap=overlap, n_inner=n_inner)
     U, A, _ = device_fields(cfg, 2)
     Uo, Ao = oracle_fields(cfg, 2)
     assert_bitwise(U, Uo, "U")
@@ -63,7 +67,7 @@ def test_fields_invariant_under_balancing_and_procs():
     # 3 processors sharing the GPU, balancing every epoch: mapping changes,
     # values must not
     cfg = small(nx=64, ny=40, kx=4, ky=4, ppn=3, threshold=1.0, steps_window=(1, 1),
-                adv=(20, 2, 2), overlap=True)
+                adv=(20, 2, 2), overlap=4)
     U, A, recs = device_fields(cfg, 6, use_epochs=True)
     assert any(r.plan.moves for r in recs)
     Uo, Ao = oracle_fields(cfg, 6)
@@ -71,8 +75,9 @@ def test_fields_invariant_under_balancing_and_procs():
     assert_bitwise(A, Ao, "A")
 
 
-def test_events_measurement_mode():
-    cfg = small(nx=64, ny=32, kx=4, ky=2, measure=od.MeasureMode.Events)
+@pytest.mark.parametrize("overlap", [0, 2, 3, 4])
+def test_events_measurement_mode(overlap):
+    cfg = small(nx=64, ny=32, kx=4, ky=2, measure=od.MeasureMode.Events, overlap=overlap)
     with od.Engine(cfg) as eng:
         wall, samples = eng.step_time(od.LaunchMode.Sync, 0)
         assert wall > 0
@@ -81,5 +86,17 @@ def test_events_measurement_mode():
         assert all(s.mode == od.LaunchMode.Async for s in asamples)
         U, A, _ = eng.gather_fields()
     Uo, Ao = oracle_fields(cfg, 2)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+
+
+@pytest.mark.parametrize("mode", [2, 3, 4])
+@pytest.mark.parametrize("n_inner,F,nz", [(0, 2, 5), (1, 3, 7), (13, 1, 4), (200, 2, 3)])
+def test_fused_quota_edge_cases(n_inner, F, nz, mode):
+    # quota rounding: recurrences longer/shorter than the Jacobi level count;
+    # odd chunk widths exercise the single-cell tail of the pair kernel
+    cfg = small(nx=41, ny=17, nz=nz, F=F, kx=2, ky=2, n_inner=n_inner, heavy=2.5, overlap=mode)
+    U, A, _ = device_fields(cfg, 3)
+    Uo, Ao = oracle_fields(cfg, 3)
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")

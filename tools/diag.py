@@ -15,6 +15,7 @@ with od.Engine(cfg) as eng:
         dt = time.perf_counter() - t
         st = eng.stats()
         print(json.dumps({"epoch": e, "host_s": dt, "steps_ms": [round(x * 1e3, 3) for x in r.step_times],
-                          "jacobi_ms_avg": st["jacobi_ms"] / max(st["jacobi_launches"], 1),
-                          "physics_ms_avg": st["physics_ms"] / max(st["physics_launches"], 1),
+                          "jacobi_ms_avg": st["jacobi_ms"] / max(st["jacobi_timed"], 1),
+                          "physics_ms_avg": st["physics_ms"] / max(st["physics_timed"], 1),
+                          "fused_ms_avg": st["fused_ms"] / max(st["fused_timed"], 1),
                           "imb": [r.imbalance_before, r.imbalance_after], "moves": len(r.plan.moves)}))
