@@ -22,7 +22,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -58,34 +57,45 @@ def dist_env():
 # ------------------------------------------------------------------ clocks --
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 200 ms in the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled every 50 ms through
+    NVML during the timed region (nvidia-smi's clocks query, in-process)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self._nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
 
     def _run(self):
+        nv = self._nv
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                    timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.rows.append((sm, r))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
@@ -96,19 +106,17 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        nv = self._nv
+        reasons = sorted({name for _, r in self.rows for name, attr in self.REASONS
+                          if r & getattr(nv, attr, 0)})
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.rows),
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.rows),
+                "source": "NVML, 50 ms"}
 
 
 # --------------------------------------------------------------- CPU legs --
 
-def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=8, side=256, warmup=0):
+def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=64, side=256, warmup=0):
     """Column-updates/s of the CPU oracle port (oracle/field_oracle.c, OpenMP,
     all host threads) on a side x side sub-grid with the workload's nz, F,
     n_inner and load pattern."""
@@ -247,8 +255,7 @@ def main():
     eng.set_profiling(True)
     st0 = eng.stats()
     hist0 = len(eng.epoch_history())
-    with ClockSampler(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[0])
-                      if world == 1 else local) as clk:
+    with ClockSampler(local) as clk:
         ms = timed(lambda: (eng.advance(args.steps), eng.synchronize()))
     st1 = eng.stats()
     hist = eng.epoch_history()[hist0:]
@@ -261,10 +268,14 @@ def main():
     res_cols = sum(s.cells() for v, s in enumerate(subs) if mapping[v] // ppn == rank)
     n_phys = st1["physics_timed"] - st0["physics_timed"]
     n_jac = st1["jacobi_timed"] - st0["jacobi_timed"]
+    n_fus = st1["fused_timed"] - st0["fused_timed"]
     phys_ms = (st1["physics_ms"] - st0["physics_ms"]) / max(n_phys, 1)
     jac_ms = (st1["jacobi_ms"] - st0["jacobi_ms"]) / max(n_jac, 1)
-    flops = st1["physics_trips"] * physics_flops_per_trip(cfg.n_inner)
-    jac_bytes = 2.0 * res_cols * d.nz * d.fields * 8
+    fus_ms = (st1["fused_ms"] - st0["fused_ms"]) / max(n_fus, 1)
+    phys_flops = st1["physics_trips"] * physics_flops_per_trip(cfg.n_inner)
+    jac_cells = float(res_cols) * d.nz * d.fields
+    jac_flops = 8.0 * jac_cells  # 5 add + 1 mul + 1 fma per cell
+    jac_bytes = 16.0 * jac_cells  # read U^t and write U^{t+1} once (FP64)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -279,13 +290,27 @@ def main():
     hbm_peak = peaks.get("hbm_gbs", 6555.8)
     traffic = None
     try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(
-            f"{args.config}:physics")
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
     except Exception:
         pass
-    phys_tf = flops / (phys_ms * 1e-3) / 1e12 if phys_ms > 0 else None
-    jac_gbs = jac_bytes / (jac_ms * 1e-3) / 1e9 if jac_ms > 0 else None
-    share = phys_ms / (ms / args.steps) if ms > 0 else None
+    step_ms = ms / args.steps
+    if n_fus > 0:
+        kname, kms, kflops = "column_step3 (fused Jacobi + physics)", fus_ms, phys_flops + jac_flops
+    else:
+        kname, kms, kflops = "physics_step", phys_ms, phys_flops
+    k_tf = kflops / (kms * 1e-3) / 1e12 if kms > 0 else None
+    roofline = {"bound": "fp64", "kernel": kname, "achieved": k_tf, "peak": fp64_peak,
+                "unit": "TFLOP/s", "frac": k_tf / fp64_peak if k_tf else None,
+                "traffic": traffic,
+                "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)",
+                "share_of_step": kms / step_ms if step_ms > 0 else None, "avg_ms": kms,
+                "flops_per_launch": kflops}
+    hbm_ms = fus_ms if n_fus > 0 else jac_ms
+    hbm_gbs = jac_bytes / (hbm_ms * 1e-3) / 1e9 if hbm_ms > 0 else None
+    roofline_hbm = {"bound": "hbm", "kernel": kname if n_fus > 0 else "jacobi_step",
+                    "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": hbm_gbs / hbm_peak if hbm_gbs else None, "avg_ms": hbm_ms,
+                    "bytes_per_launch": jac_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
     launches = st1["kernel_launches"] - st0["kernel_launches"]
     balanced = [h for h in hist if h["strategy"] >= 0 and h["n_moves"] > 0]
@@ -353,16 +378,10 @@ def main():
                              f"{cfg.policy.later_call_strategy.name}"
                              f"@{cfg.policy.trigger_threshold}",
                    "n_inner": cfg.n_inner, "measure": cfg.measure.name, "lb": "on",
+                   "kernel_mode": cfg.overlap,
                    "l2": "state 54 GB >> 126 MB L2 (no flush needed)"},
-        "roofline": {"bound": "fp64", "kernel": "physics_step", "achieved": phys_tf,
-                     "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": phys_tf / fp64_peak if phys_tf else None, "traffic": traffic,
-                     "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)",
-                     "share_of_step": share, "avg_ms": phys_ms},
-        "roofline_jacobi": {"bound": "hbm", "kernel": "jacobi_step", "achieved": jac_gbs,
-                            "peak": hbm_peak, "unit": "GB/s",
-                            "frac": jac_gbs / hbm_peak if jac_gbs else None, "avg_ms": jac_ms,
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+        "roofline": roofline,
+        "roofline_hbm": roofline_hbm,
         "clocks": clk.summary(),
         "gpu_launches": launches,
         "e2e": e2e,
