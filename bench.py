@@ -199,6 +199,9 @@ def physics_flops_per_trip(n_inner):
 def main():
     args = parse_args()
     rank, world, local = dist_env()
+    # keep stdout for the single JSON line: libraries (NCCL, torch) may print
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     from paper_1310_4218_b200 import configs
     make = configs.CONFIGS[args.config]
     kw = {"epochs": 1 << 30}
@@ -208,7 +211,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(reference_arm(args, cfg)), flush=True)
+            print(json.dumps(reference_arm(args, cfg)), file=json_out, flush=True)
         return
 
     import torch
@@ -219,11 +222,15 @@ def main():
     import paper_1310_4218_b200 as od
     import numpy as np
 
-    nccl_id = None
-    if world > 1:
+    def new_nccl_id():
+        # one fresh id per communicator (an id must not be reused)
+        if world == 1:
+            return None
         obj = [od.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = new_nccl_id()
 
     def barrier():
         if world > 1:
@@ -343,7 +350,7 @@ def main():
         cfg_off = cfg.replace(policy=cfg.policy.__class__(
             cfg.policy.first_call_strategy, cfg.policy.later_call_strategy, 1e30,
             cfg.policy.refine_tolerance))
-        eng2 = od.Engine(cfg_off, rank, world, local, nccl_id)
+        eng2 = od.Engine(cfg_off, rank, world, local, new_nccl_id())
         eng2.advance(args.warmup)
         eng2.synchronize()
         ms_off = timed(lambda: (eng2.advance(args.steps), eng2.synchronize()))
@@ -389,10 +396,12 @@ def main():
         "lb_off": lb_off,
         "post_lb_imbalance": post_lb,
         "epoch_imbalance": eng_imb,
+        "epochs": [{k: (round(v, 6) if isinstance(v, float) else v) for k, v in h.items()}
+                   for h in hist],
         "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
         "migrated_bytes": st1["migrated_bytes"] - st0["migrated_bytes"],
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=json_out, flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -120,6 +120,36 @@ int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
                       int32_t vp_count, int32_t proc_count, double tolerance,
                       od_move* out, int32_t cap, int32_t* n_out);
 
+/* Engine::run_epoch decision (engine.hpp:257-268) on given per-VP loads:
+ * totals, imbalance before/after, trigger (never on the last epoch), first
+ * triggered call -> first strategy, later -> later strategy.  *balance_calls
+ * is read and incremented on every triggered call.  *strategy = -1 when no
+ * strategy was called. */
+int od_epoch_decision(const double* loads, int32_t n_loads, const int32_t* map,
+                      int32_t vp_count, int32_t proc_count, int32_t epoch_index,
+                      int32_t epochs, int32_t* balance_calls, int32_t first_strategy,
+                      int32_t later_strategy, double trigger_threshold,
+                      double refine_tolerance, int32_t* strategy, od_move* moves,
+                      int32_t cap, int32_t* n_moves, double* totals /* P */,
+                      double* imbalance_before, double* imbalance_after);
+
+/* ------------------------------------------------------------ halo exchange */
+/* Face of a chunk bordering a chunk on another rank (B200 path; the reference
+ * models this traffic at engine.hpp:207-217).  Layout of a packed strip:
+ * [field][level][position], row stride lenp (len rounded up to even). */
+typedef struct od_face_xfer {
+  int32_t peer, vp, side, nbr, len, lenp;  /* vp owns the strip; side 0 L 1 R 2 T 3 B */
+  int64_t offset;                          /* elements into the send / recv buffer */
+} od_face_xfer;
+/* neighbour of vp across side, -1 at the domain edge   engine.hpp:290-309 */
+int od_chunk_neighbor(int32_t kind, int32_t kx, int32_t ky, int32_t vp, int32_t side,
+                      int32_t* out);
+int od_exchange_schedule(const od_subdomain* subs, int32_t vp_count, int32_t kind,
+                         int32_t kx, int32_t ky, const int32_t* rank_of_vp, int32_t world,
+                         int32_t rank, int64_t per_cell, od_face_xfer* sends, int32_t send_cap,
+                         int32_t* n_sends, od_face_xfer* recvs, int32_t recv_cap,
+                         int32_t* n_recvs);
+
 /* ------------------------------------------------------------- measurement */
 /* LoadDB                                             measurement.hpp:40-70 */
 typedef struct od_loaddb od_loaddb;

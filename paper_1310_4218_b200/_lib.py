@@ -97,6 +97,12 @@ class od_epoch_summary(C.Structure):
                 ("imbalance_after", C.c_double)]
 
 
+class od_face_xfer(C.Structure):
+    _fields_ = [("peer", C.c_int32), ("vp", C.c_int32), ("side", C.c_int32),
+                ("nbr", C.c_int32), ("len", C.c_int32), ("lenp", C.c_int32),
+                ("offset", C.c_int64)]
+
+
 _I32, _I64, _D, _U64 = C.c_int32, C.c_int64, C.c_double, C.c_uint64
 _P = C.POINTER
 _VP = C.c_void_p
@@ -121,6 +127,13 @@ PROTOTYPES = {
     "od_should_balance": [_P(_D), _I32, _D, _P(_I32)],
     "od_greedy_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _P(od_move), _I32, _P(_I32)],
     "od_refine_swap_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _P(od_move), _I32, _P(_I32)],
+    "od_epoch_decision": [_P(_D), _I32, _P(_I32), _I32, _I32, _I32, _I32, _P(_I32), _I32, _I32,
+                          _D, _D, _P(_I32), _P(od_move), _I32, _P(_I32), _P(_D), _P(_D),
+                          _P(_D)],
+    "od_chunk_neighbor": [_I32, _I32, _I32, _I32, _I32, _P(_I32)],
+    "od_exchange_schedule": [_P(od_subdomain), _I32, _I32, _I32, _I32, _P(_I32), _I32, _I32,
+                             _I64, _P(od_face_xfer), _I32, _P(_I32), _P(od_face_xfer), _I32,
+                             _P(_I32)],
     "od_loaddb_create": [_I32, _I32, _I32, _P(_VP)],
     "od_loaddb_record": [_VP, _P(od_sample)],
     "od_loaddb_clear": [_VP],

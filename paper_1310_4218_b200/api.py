@@ -26,7 +26,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (RuntimeFault, ValidationError, check, lib, od_config, od_epoch_record,
-                   od_epoch_summary,
+                   od_epoch_summary, od_face_xfer,
                    od_kernel_work, od_move, od_rt_stats, od_sample, od_subdomain)
 
 __all__ = [
@@ -38,7 +38,8 @@ __all__ = [
     "should_balance", "greedy_lb", "refine_swap_lb", "StepSample", "MeasurementWindow",
     "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
-    "run_experiment", "nccl_unique_id",
+    "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
+    "FaceXfer", "exchange_schedule",
 ]
 
 
@@ -383,6 +384,75 @@ def refine_swap_lb(loads: Sequence[float], mapping: Mapping,
     check(lib.od_refine_swap_lb(_dptr(l), int(l.size), _iptr(mapping._a), mapping.vp_count(),
                                 mapping.proc_count(), float(tolerance), out, cap, C.byref(n)))
     return _plan_from(out, n.value, Strategy.RefineSwap)
+
+
+@dataclass
+class EpochDecision:
+    strategy: Optional[Strategy]
+    plan: MigrationPlan
+    proc_loads: List[float]
+    imbalance_before: float
+    imbalance_after: float
+    balance_calls: int
+
+
+def epoch_decision(loads: Sequence[float], mapping: Mapping, epoch_index: int, epochs: int,
+                   balance_calls: int, policy: BalancePolicy) -> EpochDecision:
+    """The balancing decision of Engine::run_epoch (engine.hpp:257-268) on a
+    given load vector: the same call the B200 runtime makes at every epoch end."""
+    l = np.ascontiguousarray(loads, dtype=np.float64)
+    cap = max(2 * mapping.vp_count() * mapping.proc_count(), mapping.vp_count(), 1)
+    out = (od_move * cap)()
+    n = C.c_int32()
+    bc = C.c_int32(int(balance_calls))
+    st = C.c_int32()
+    tot = np.zeros(max(mapping.proc_count(), 1))
+    ib, ia = C.c_double(), C.c_double()
+    check(lib.od_epoch_decision(_dptr(l), int(l.size), _iptr(mapping._a), mapping.vp_count(),
+                                mapping.proc_count(), int(epoch_index), int(epochs),
+                                C.byref(bc), int(policy.first_call_strategy),
+                                int(policy.later_call_strategy), float(policy.trigger_threshold),
+                                float(policy.refine_tolerance), C.byref(st), out, cap,
+                                C.byref(n), _dptr(tot), C.byref(ib), C.byref(ia)))
+    strategy = Strategy(st.value) if st.value >= 0 else None
+    plan = _plan_from(out, n.value, strategy if strategy is not None else Strategy.Greedy)
+    return EpochDecision(strategy, plan, tot[:mapping.proc_count()].tolist(), ib.value,
+                         ia.value, bc.value)
+
+
+def chunk_neighbor(kind: DecompositionKind, kx: int, ky: int, vp: int, side: int) -> int:
+    out = C.c_int32()
+    check(lib.od_chunk_neighbor(int(kind), int(kx), int(ky), int(vp), int(side), C.byref(out)))
+    return out.value
+
+
+@dataclass(frozen=True)
+class FaceXfer:
+    peer: int
+    vp: int
+    side: int
+    nbr: int
+    len: int
+    lenp: int
+    offset: int
+
+
+def exchange_schedule(subs: Sequence[SubDomain], kind: DecompositionKind, kx: int, ky: int,
+                      rank_of_vp: Sequence[int], world: int, rank: int,
+                      per_cell: int) -> Tuple[List[FaceXfer], List[FaceXfer]]:
+    """Cross-rank halo faces of `rank` (what it packs and sends, what it
+    receives), in the order both sides agree on."""
+    K = len(subs)
+    sc = (od_subdomain * K)(*[s._c() for s in subs])
+    r = np.ascontiguousarray(rank_of_vp, dtype=np.int32)
+    cap = 4 * K
+    so, ro = (od_face_xfer * cap)(), (od_face_xfer * cap)()
+    ns, nr = C.c_int32(), C.c_int32()
+    check(lib.od_exchange_schedule(sc, K, int(kind), int(kx), int(ky), _iptr(r), int(world),
+                                   int(rank), int(per_cell), so, cap, C.byref(ns), ro, cap,
+                                   C.byref(nr)))
+    cv = lambda f: FaceXfer(f.peer, f.vp, f.side, f.nbr, f.len, f.lenp, f.offset)  # noqa: E731
+    return [cv(so[i]) for i in range(ns.value)], [cv(ro[i]) for i in range(nr.value)]
 
 
 # --------------------------------------------------------------- measurement --

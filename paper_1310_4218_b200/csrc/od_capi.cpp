@@ -247,6 +247,77 @@ int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
   });
 }
 
+int od_epoch_decision(const double* loads, int32_t n_loads, const int32_t* map,
+                      int32_t vp_count, int32_t proc_count, int32_t epoch_index, int32_t epochs,
+                      int32_t* balance_calls, int32_t first_strategy, int32_t later_strategy,
+                      double trigger_threshold, double refine_tolerance, int32_t* strategy,
+                      od_move* moves, int32_t cap, int32_t* n_moves, double* totals,
+                      double* imbalance_before, double* imbalance_after) {
+  return guarded([&] {
+    need(balance_calls, "balance_calls");
+    need(strategy, "strategy");
+    if (first_strategy < 0 || first_strategy > 1 || later_strategy < 0 || later_strategy > 1)
+      throw ValidationError("unknown strategy");
+    if (trigger_threshold < 1.0) throw ValidationError("policy.trigger_threshold must be >= 1");
+    if (refine_tolerance < 0.0) throw ValidationError("policy.refine_tolerance must be >= 0");
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    Decision d = decide_epoch(l, m, proc_count, epoch_index, epochs, *balance_calls,
+                              first_strategy, later_strategy, trigger_threshold,
+                              refine_tolerance);
+    *strategy = d.strategy;
+    if (totals) std::memcpy(totals, d.totals.data(), d.totals.size() * sizeof(double));
+    if (imbalance_before) *imbalance_before = d.imbalance_before;
+    if (imbalance_after) *imbalance_after = d.imbalance_after;
+    return emit_moves(d.plan, moves, cap, n_moves);
+  });
+}
+
+int od_chunk_neighbor(int32_t kind, int32_t kx, int32_t ky, int32_t vp, int32_t side,
+                      int32_t* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (side < 0 || side > 3) throw ValidationError("side must be 0..3");
+    if (kx < 1 || ky < 1 || vp < 0 || vp >= (kind == OD_ONE_D ? 1 : kx) * ky)
+      throw ValidationError("vp outside the decomposition");
+    *out = chunk_neighbor(kind, kx, ky, vp, side);
+  });
+}
+
+int od_exchange_schedule(const od_subdomain* subs, int32_t vp_count, int32_t kind, int32_t kx,
+                         int32_t ky, const int32_t* rank_of_vp, int32_t world, int32_t rank,
+                         int64_t per_cell, od_face_xfer* sends, int32_t send_cap,
+                         int32_t* n_sends, od_face_xfer* recvs, int32_t recv_cap,
+                         int32_t* n_recvs) {
+  return guarded([&] {
+    if (vp_count < 1) throw ValidationError("vp count must be >= 1");
+    if (world < 1 || rank < 0 || rank >= world) throw ValidationError("rank out of range");
+    need(subs, "subs");
+    need(rank_of_vp, "rank_of_vp");
+    need(n_sends, "n_sends");
+    need(n_recvs, "n_recvs");
+    if ((kind == OD_ONE_D ? ky : kx * ky) != vp_count)
+      throw ValidationError("decomposition does not match vp count");
+    std::vector<Sub> sv(vp_count);
+    std::vector<int32_t> rv(rank_of_vp, rank_of_vp + vp_count);
+    for (int32_t v = 0; v < vp_count; ++v) {
+      sv[v] = to_sub(subs[v]);
+      if (rv[v] < 0 || rv[v] >= world) throw ValidationError("rank id out of range");
+    }
+    std::vector<FaceXfer> s, r;
+    exchange_schedule(sv, kind, kx, ky, rv, world, rank, per_cell, s, r);
+    *n_sends = int32_t(s.size());
+    *n_recvs = int32_t(r.size());
+    if (int32_t(s.size()) > send_cap || int32_t(r.size()) > recv_cap)
+      throw ValidationError("face buffer too small");
+    auto put = [](const FaceXfer& f) {
+      return od_face_xfer{f.peer, f.vp, f.side, f.nbr, f.len, f.lenp, f.offset};
+    };
+    for (size_t i = 0; i < s.size(); ++i) sends[i] = put(s[i]);
+    for (size_t i = 0; i < r.size(); ++i) recvs[i] = put(r[i]);
+  });
+}
+
 struct od_loaddb {
   SampleStore store;
 };

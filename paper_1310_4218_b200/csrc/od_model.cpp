@@ -302,6 +302,77 @@ std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
   return plan;
 }
 
+// ------------------------------------------------------------ epoch policy --
+
+Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
+                      int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
+                      int32_t first_strategy, int32_t later_strategy, double threshold,
+                      double tolerance) {
+  Decision d;
+  d.totals = totals_per_proc(loads, map, P);
+  d.imbalance_before = max_over_mean(d.totals);
+  d.imbalance_after = d.imbalance_before;
+  if (epoch < epochs && balance_needed(d.totals, threshold)) {
+    d.strategy = balance_calls == 0 ? first_strategy : later_strategy;
+    d.plan = d.strategy == kGreedy ? plan_greedy(loads, map, P)
+                                   : plan_refine_swap(loads, map, P, tolerance);
+    ++balance_calls;
+    if (!d.plan.empty())
+      d.imbalance_after = max_over_mean(totals_per_proc(loads, apply_moves(map, P, d.plan), P));
+  }
+  return d;
+}
+
+// -------------------------------------------------------- exchange schedule --
+
+int32_t chunk_neighbor(int32_t kind, int32_t kx, int32_t ky, int32_t vp, int32_t side) {
+  if (kind == 0) kx = 1;  // strips: vertical neighbours only
+  const int32_t i = vp % kx, j = vp / kx;
+  switch (side) {
+    case 0: return i > 0 ? vp - 1 : -1;
+    case 1: return i + 1 < kx ? vp + 1 : -1;
+    case 2: return j > 0 ? vp - kx : -1;
+    default: return j + 1 < ky ? vp + kx : -1;
+  }
+}
+
+void exchange_schedule(const std::vector<Sub>& subs, int32_t kind, int32_t kx, int32_t ky,
+                       const std::vector<int32_t>& rank_of_vp, int32_t world, int32_t rank,
+                       int64_t per_cell, std::vector<FaceXfer>& sends,
+                       std::vector<FaceXfer>& recvs) {
+  sends.clear();
+  recvs.clear();
+  const int32_t K = int32_t(subs.size());
+  int64_t soff = 0, roff = 0;
+  for (int32_t q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    // strips this rank sends to q: my chunk v, face d bordering a chunk on q
+    for (int32_t v = 0; v < K; ++v) {
+      if (rank_of_vp[v] != rank) continue;
+      for (int32_t d = 0; d < 4; ++d) {
+        const int32_t n = chunk_neighbor(kind, kx, ky, v, d);
+        if (n < 0 || rank_of_vp[n] != q) continue;
+        const int32_t len = d < 2 ? subs[v].h() : subs[v].w();
+        const int32_t lenp = (len + 1) & ~1;
+        sends.push_back({q, v, d, n, len, lenp, soff});
+        soff += per_cell * lenp;
+      }
+    }
+    // strips q sends to this rank, in q's (sender vp, side) order
+    for (int32_t v = 0; v < K; ++v) {
+      if (rank_of_vp[v] != q) continue;
+      for (int32_t d = 0; d < 4; ++d) {
+        const int32_t n = chunk_neighbor(kind, kx, ky, v, d);
+        if (n < 0 || rank_of_vp[n] != rank) continue;
+        const int32_t len = d < 2 ? subs[v].h() : subs[v].w();
+        const int32_t lenp = (len + 1) & ~1;
+        recvs.push_back({q, v, d, n, len, lenp, roff});
+        roff += per_cell * lenp;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- measurement --
 
 SampleStore::SampleStore(int32_t K, int32_t async_steps, int32_t sync_steps)

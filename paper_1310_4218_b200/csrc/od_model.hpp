@@ -89,6 +89,37 @@ std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
                                       const std::vector<int32_t>& map, int32_t P,
                                       double tol);                            // :68-152
 
+// ---- epoch policy (Engine::run_epoch, engine.hpp:257-268) --------------------
+struct Decision {
+  int32_t strategy = -1;  // -1: no strategy called
+  std::vector<MoveRec> plan;
+  std::vector<double> totals;
+  double imbalance_before = 1, imbalance_after = 1;
+};
+// Given the epoch's per-VP loads: totals, imbalance, trigger check (never on
+// the last epoch), first call -> first strategy, later calls -> later
+// strategy; balance_calls is incremented on every triggered call.
+Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
+                      int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
+                      int32_t first_strategy, int32_t later_strategy, double threshold,
+                      double tolerance);
+
+// ---- halo exchange schedule -------------------------------------------------
+// Faces between chunks owned by different ranks.  Both sides enumerate the
+// faces in (sender vp, side) order, so the packed buffers line up without any
+// metadata exchange.  Layout of one face: [field][level][position], row
+// stride lenp = len rounded up to even (16-byte aligned pairs).
+struct FaceXfer {
+  int32_t peer, vp, side, nbr, len, lenp;  // vp: owner of the strip (sender side)
+  int64_t offset;                          // element offset in the send/recv buffer
+};
+// Neighbour of vp across `side` (0 left, 1 right, 2 top, 3 bottom) or -1.
+int32_t chunk_neighbor(int32_t kind, int32_t kx, int32_t ky, int32_t vp, int32_t side);
+void exchange_schedule(const std::vector<Sub>& subs, int32_t kind, int32_t kx, int32_t ky,
+                       const std::vector<int32_t>& rank_of_vp, int32_t world, int32_t rank,
+                       int64_t per_cell, std::vector<FaceXfer>& sends,
+                       std::vector<FaceXfer>& recvs);
+
 // ---- measurement --------------------------------------------------------------
 // Per-epoch sample store (measurement.hpp:40-70) + epoch_loads (:75-91).
 class SampleStore {

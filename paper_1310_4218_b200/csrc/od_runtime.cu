@@ -258,6 +258,22 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
     OD_NC(odb::nccl().CommInitRank(&comm_, world_, id, rank_));
+    // NCCL connects peers lazily on first use; pay that here, not inside the
+    // first exchange/migration/gather of the run: one all-gather and one
+    // send/recv with every peer
+    double* tmp = nullptr;
+    OD_CU(cudaMalloc(&tmp, sizeof(double) * 2 * (world_ + 1)));
+    OD_CU(cudaMemset(tmp, 0, sizeof(double) * 2 * (world_ + 1)));
+    OD_NC(odb::nccl().AllGather(tmp, tmp + 1, 1, ncclFloat64, comm_, s0_));
+    OD_NC(odb::nccl().GroupStart());
+    for (int q = 0; q < world_; ++q) {
+      if (q == rank_) continue;
+      OD_NC(odb::nccl().Send(tmp, 1, ncclFloat64, q, comm_, s0_));
+      OD_NC(odb::nccl().Recv(tmp + world_ + 1 + q, 1, ncclFloat64, q, comm_, s0_));
+    }
+    OD_NC(odb::nccl().GroupEnd());
+    OD_CU(cudaStreamSynchronize(s0_));
+    cudaFree(tmp);
   }
   const size_t cbytes = base_.c.size() * sizeof(double);
   OD_CU(cudaMalloc(&d_cbase_, cbytes));
@@ -309,15 +325,7 @@ Runtime::~Runtime() {
 // ------------------------------------------------------------------ model --
 
 int32_t Runtime::nbr(int32_t v, int d) const {
-  const int32_t kx = cfg_.decomposition_kind == OD_ONE_D ? 1 : cfg_.kx;
-  const int32_t ky = cfg_.ky;
-  const int32_t i = v % kx, j = v / kx;
-  switch (d) {
-    case kLeft: return i > 0 ? v - 1 : -1;
-    case kRight: return i + 1 < kx ? v + 1 : -1;
-    case kTop: return j > 0 ? v - kx : -1;
-    default: return j + 1 < ky ? v + kx : -1;
-  }
+  return chunk_neighbor(cfg_.decomposition_kind, cfg_.kx, cfg_.ky, v, d);
 }
 
 void Runtime::set_shift(int32_t rows) {
@@ -441,32 +449,28 @@ void Runtime::rebuild_tables() {
   recv_cnt_.assign(world_, 0);
   recv_face_off_.assign(nres, {-1, -1, -1, -1});
   const int64_t per_cell = int64_t(cfg_.nz) * cfg_.fields;
+  std::vector<int32_t> rank_of(K());
+  for (int32_t v = 0; v < K(); ++v) rank_of[v] = rank_of_vp(v);
+  std::vector<FaceXfer> sends, recvs;
+  exchange_schedule(subs_, cfg_.decomposition_kind, cfg_.kx, cfg_.ky, rank_of, world_, rank_,
+                    per_cell, sends, recvs);
   int64_t soff = 0, roff = 0;
+  for (const FaceXfer& f : sends) {
+    jobs_.push_back(PackJob{slot_of[f.vp], f.side, f.len, f.lenp, f.offset});
+    send_cnt_[f.peer] += per_cell * f.lenp;
+    soff = f.offset + per_cell * f.lenp;
+  }
+  for (const FaceXfer& f : recvs) {
+    recv_face_off_[slot_of[f.nbr]][opposite(f.side)] = f.offset;
+    recv_cnt_[f.peer] += per_cell * f.lenp;
+    roff = f.offset + per_cell * f.lenp;
+  }
+  int64_t so = 0, ro = 0;
   for (int q = 0; q < world_; ++q) {
-    send_off_[q] = soff;
-    recv_off_[q] = roff;
-    if (q == rank_) continue;
-    for (int32_t v : resident_)
-      for (int d = 0; d < 4; ++d) {
-        const int32_t n = nbr(v, d);
-        if (n < 0 || rank_of_vp(n) != q) continue;
-        const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
-        const int32_t lenp = (len + 1) & ~1;  // even row stride: 16-byte aligned pairs
-        jobs_.push_back(PackJob{slot_of[v], d, len, lenp, soff});
-        soff += per_cell * lenp;
-      }
-    send_cnt_[q] = soff - send_off_[q];
-    for (int32_t v = 0; v < K(); ++v) {
-      if (rank_of_vp(v) != q) continue;
-      for (int d = 0; d < 4; ++d) {
-        const int32_t n = nbr(v, d);
-        if (n < 0 || rank_of_vp(n) != rank_) continue;
-        const int32_t len = (d == kLeft || d == kRight) ? subs_[v].h() : subs_[v].w();
-        recv_face_off_[slot_of[n]][opposite(d)] = roff;
-        roff += per_cell * ((len + 1) & ~1);
-      }
-    }
-    recv_cnt_[q] = roff - recv_off_[q];
+    send_off_[q] = so;
+    recv_off_[q] = ro;
+    so += send_cnt_[q];
+    ro += recv_cnt_[q];
   }
   if (size_t(soff) > send_cap_) {
     cudaFree(d_send_);
@@ -932,20 +936,18 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
     for (int32_t v = 0; v < K(); ++v) db.add(v, s, mode, samples[size_t(s) * K() + v]);
   }
   o.loads = db.sync_means();
-  o.totals = totals_per_proc(o.loads, map_, P());
-  o.imb_before = max_over_mean(o.totals);
-  o.imb_after = o.imb_before;
-  if (e < cfg_.epochs && balance_needed(o.totals, cfg_.trigger_threshold)) {
-    o.strategy = balance_calls_ == 0 ? cfg_.first_call_strategy : cfg_.later_call_strategy;
-    o.plan = o.strategy == kGreedy ? plan_greedy(o.loads, map_, P())
-                                   : plan_refine_swap(o.loads, map_, P(), cfg_.refine_tolerance);
-    ++balance_calls_;
-    if (!o.plan.empty()) {
-      const auto t0 = std::chrono::steady_clock::now();
-      migrate(o.plan);
-      o.mig_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      o.imb_after = max_over_mean(totals_per_proc(o.loads, map_, P()));
-    }
+  Decision d = decide_epoch(o.loads, map_, P(), e, cfg_.epochs, balance_calls_,
+                            cfg_.first_call_strategy, cfg_.later_call_strategy,
+                            cfg_.trigger_threshold, cfg_.refine_tolerance);
+  o.totals = d.totals;
+  o.imb_before = d.imbalance_before;
+  o.imb_after = d.imbalance_after;
+  o.strategy = d.strategy;
+  o.plan = d.plan;
+  if (!o.plan.empty()) {
+    const auto t0 = std::chrono::steady_clock::now();
+    migrate(o.plan);
+    o.mig_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   od_epoch_summary h{};
   h.epoch = e;

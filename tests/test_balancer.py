@@ -1,0 +1,185 @@
+"""Product load balancers (C++ behind the C ABI) against the reference:
+bit-exact plans on the reference's unit-test vectors, on golden plans made by
+the reference itself, and on fresh random vectors through oracle/_ref;
+properties of proj/tests/test_balancer.cpp, test_properties.cpp and the
+acceptance criteria 1, 7, 8."""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1310_4218_b200 as od
+from oracle import lb_oracle as lbo
+from oracle import ref as oref
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def M(assign, P):
+    return od.Mapping(proc_count=P, assignment=assign)
+
+
+def moves(plan):
+    return [tuple(m) for m in plan.moves]
+
+
+def test_greedy_tie_breaking():  # test_balancer.cpp:62-76
+    m = od.initial_block_mapping(4, 2)
+    plan = od.greedy_lb([1.0, 1.0, 1.0, 1.0], m)
+    after = od.apply_plan(m, plan)
+    assert [after.proc_of(v) for v in range(4)] == [0, 1, 0, 1]
+    assert moves(plan) == [(1, 0, 1), (2, 1, 0)]
+    assert plan.strategy == od.Strategy.Greedy
+
+
+def test_greedy_move_order():  # :78-90
+    m = od.initial_block_mapping(4, 2)
+    plan = od.greedy_lb([4.0, 1.0, 3.0, 1.0], m)
+    assert moves(plan) == [(1, 0, 1), (3, 1, 0)]
+
+
+def test_refine_single_move():  # :92-104
+    plan = od.refine_swap_lb([4.0, 1.0, 3.0, 4.0, 4.0], M([0, 0, 1, 2, 3], 4), 0.02)
+    assert moves(plan) == [(1, 0, 1)] and plan.strategy == od.Strategy.RefineSwap
+
+
+def test_refine_swap_fallback():  # :106-122
+    m = M([0, 0, 1, 1], 2)
+    plan = od.refine_swap_lb([3.5, 2.5, 2.5, 1.5], m, 0.02)
+    assert moves(plan) == [(0, 0, 1), (2, 1, 0)]
+    assert od.proc_loads([3.5, 2.5, 2.5, 1.5], od.apply_plan(m, plan)) == [5.0, 5.0]
+
+
+def test_refine_within_tolerance():  # :124-127
+    assert od.refine_swap_lb([1.0, 1.01, 1.0, 1.0], od.initial_block_mapping(4, 2)).empty()
+
+
+def test_refine_plans_stay_applicable():  # :129-141
+    for s in range(50):
+        rng = np.random.default_rng(s)
+        loads = rng.uniform(0.1, 5.0, 8)
+        m = M(rng.integers(0, 3, 8), 3)
+        od.apply_plan(m, od.refine_swap_lb(loads, m, 0.02))
+
+
+def test_errors():
+    with pytest.raises(od.ValidationError):
+        od.greedy_lb([1.0], od.initial_block_mapping(4, 2))
+    with pytest.raises(od.ValidationError):
+        od.refine_swap_lb([1.0] * 4, od.initial_block_mapping(4, 2), -0.1)
+
+
+def test_plans_match_reference_goldens():
+    for c in json.load(open(os.path.join(GOLD, "lb_cases.json"))):
+        loads = [float.fromhex(x) for x in c["loads"]]
+        m = M(c["mapping"], c["P"])
+        assert [list(x) for x in moves(od.greedy_lb(loads, m))] == c["greedy"]
+        assert [list(x) for x in moves(od.refine_swap_lb(loads, m, c["tol"]))] == c["refine"]
+        tot = od.proc_loads(loads, m)
+        assert tot == [float.fromhex(x) for x in c["totals"]]
+        assert od.imbalance_ratio(tot) == float.fromhex(c["imbalance"])
+
+
+@pytest.mark.skipif(not oref.available(), reason="oracle/_ref not built")
+def test_plans_match_reference_random_large():
+    rng = np.random.default_rng(424242)
+    for t in range(400):
+        K = int(rng.choice([16, 64, 256, 1024])) if t % 4 == 0 else int(rng.integers(2, 64))
+        P = int(rng.integers(1, min(K, 8) + 1))
+        kind = t % 3
+        loads = (rng.uniform(0.01, 10, K) if kind == 0 else
+                 rng.integers(1, 5, K).astype(float) if kind == 1 else
+                 np.where(rng.random(K) < 0.5, 2.0, 1.0) * (1 + 0.005 * rng.standard_normal(K)))
+        mp = rng.integers(0, P, K).astype(np.int32)
+        m = M(mp, P)
+        assert moves(od.greedy_lb(loads, m)) == oref.greedy_lb(loads, mp, P)
+        tol = float(rng.choice([0.0, 0.02, 0.1]))
+        assert moves(od.refine_swap_lb(loads, m, tol)) == oref.refine_swap_lb(loads, mp, P, tol)
+
+
+def optimal_max(loads, P):
+    best = 1e300
+    for a in itertools.product(range(P), repeat=len(loads)):
+        acc = [0.0] * P
+        for v, p in enumerate(a):
+            acc[p] += loads[v]
+        best = min(best, max(acc))
+    return best
+
+
+def test_greedy_bound_exhaustive():
+    # acceptance.cpp:43-69 (K <= 5 here, loads in {1..4}): conservation and the
+    # 4/3 - 1/(3P) bound against the brute-force optimum
+    n = 0
+    for P in range(1, 4):
+        for K in range(P, 6):
+            for digits in itertools.product(range(1, 5), repeat=K):
+                loads = [float(d) for d in digits]
+                m = od.initial_block_mapping(K, P)
+                after = od.apply_plan(m, od.greedy_lb(loads, m))
+                acc = od.proc_loads(loads, after)
+                assert abs(sum(acc) - sum(loads)) < 1e-9
+                assert max(acc) <= (4 / 3 - 1 / (3 * P)) * optimal_max(loads, P) + 1e-12
+                n += 1
+    assert n > 1000
+
+
+def test_refine_monotone_and_idempotent():
+    # test_properties.cpp:10-34 (1200 random instances)
+    rng = np.random.default_rng(424242)
+    for _ in range(1200):
+        P = int(rng.integers(2, 6))
+        K = max(P, int(rng.integers(2, 13)))
+        loads = rng.uniform(0.05, 10.0, K)
+        m = M(rng.integers(0, P, K), P)
+        after = od.apply_plan(m, od.refine_swap_lb(loads, m, 0.02))
+        assert max(od.proc_loads(loads, after)) <= max(od.proc_loads(loads, m)) + 1e-12
+        assert od.refine_swap_lb(loads, after, 0.02).empty()
+
+
+def test_greedy_conservation_and_no_empty_proc():
+    # test_properties.cpp:79-96
+    rng = np.random.default_rng(99)
+    for _ in range(300):
+        P = 2 + int(rng.integers(0, 4))
+        K = P + int(rng.integers(0, 10))
+        loads = rng.uniform(0.05, 10.0, K)
+        m = od.initial_block_mapping(K, P)
+        acc = od.proc_loads(loads, od.apply_plan(m, od.greedy_lb(loads, m)))
+        assert sum(acc) == pytest.approx(loads.sum(), rel=1e-12)
+        assert all(a > 0 for a in acc)
+
+
+def test_async_samples_are_inert():
+    # test_properties.cpp:51-77 / acceptance 7: junk async values never change
+    # loads or plans
+    rng = np.random.default_rng(2024)
+    w = od.MeasurementWindow(6, 4)
+    for _ in range(50):
+        K, P = 8, 4
+        clean, poisoned = od.LoadDB(K, w), od.LoadDB(K, w)
+        for v in range(K):
+            for s in range(w.epoch_steps()):
+                mode = w.mode_of_step(s)
+                val = rng.uniform(0.01, 9.0) if mode == od.LaunchMode.Sync else 1e-4
+                clean.record(od.StepSample(v, s, mode, val))
+                junk = val if mode == od.LaunchMode.Sync else rng.uniform(0, 1e9)
+                poisoned.record(od.StepSample(v, s, mode, junk))
+        a, b = od.epoch_loads(clean), od.epoch_loads(poisoned)
+        assert a == b
+        m = M(rng.integers(0, P, K), P)
+        assert moves(od.greedy_lb(a, m)) == moves(od.greedy_lb(b, m))
+        assert moves(od.refine_swap_lb(a, m)) == moves(od.refine_swap_lb(b, m))
+
+
+def test_product_matches_python_restatement():
+    rng = np.random.default_rng(77)
+    for _ in range(300):
+        K = int(rng.integers(2, 30))
+        P = int(rng.integers(1, min(K, 7) + 1))
+        loads = list(rng.uniform(0.1, 4, K))
+        mp = rng.integers(0, P, K).tolist()
+        assert moves(od.greedy_lb(loads, M(mp, P))) == lbo.greedy_lb(loads, mp, P)
+        assert moves(od.refine_swap_lb(loads, M(mp, P))) == lbo.refine_swap_lb(loads, mp, P)
