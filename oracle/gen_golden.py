@@ -153,20 +153,25 @@ def timelines():
 
 
 def fields():
-    """Small field-oracle runs (hex values) pinning the CPU restatement."""
+    """Small field-oracle runs (hex values) pinning the CPU restatement; the
+    shift sequence is the reference advection schedule of the stored config
+    (engine.hpp:323-342) so the device can be checked against them directly."""
+    from oracle import schedule as osch
     out = []
-    for (nx, ny, nz, F, n_inner, seed, steps, pat) in [(8, 6, 3, 2, 4, 11, 3, 2),
-                                                      (5, 7, 4, 1, 0, 3, 2, 2),
-                                                      (12, 4, 2, 3, 17, 99, 4, 0)]:
+    for (nx, ny, nz, F, n_inner, seed, steps, pat, kx, ky, adv) in [
+            (8, 6, 3, 2, 4, 11, 3, 2, 2, 2, (3, 1, 3)),
+            (5, 7, 4, 1, 0, 3, 2, 2, 1, 3, (0, 0, 1)),
+            (12, 4, 2, 3, 17, 99, 4, 0, 3, 1, (2, 1, 2)),
+            (70, 20, 5, 2, 33, 5, 4, 2, 2, 2, (7, 1, 4))]:
         U, A = of.init_state(nx, ny, nz, F, seed)
         base = np.ones((ny, nx))
         if pat == 2:
             base[: ny // 2] = 2.0
-        shifts = [s % ny for s in range(steps)]
+        shifts = osch.shifts(adv[0], adv[1], adv[2], 1, 1, steps, ny)
         of.run(U, A, base, shifts, n_inner)
         out.append({"nx": nx, "ny": ny, "nz": nz, "fields": F, "n_inner": n_inner, "seed": seed,
-                    "steps": steps, "pattern": pat, "shifts": shifts, "U": hexs(U),
-                    "A": hexs(A)})
+                    "steps": steps, "pattern": pat, "kx": kx, "ky": ky, "advection": adv,
+                    "window": [1, 1], "shifts": shifts, "U": hexs(U), "A": hexs(A)})
     return out
 
 

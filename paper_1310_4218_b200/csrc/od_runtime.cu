@@ -144,7 +144,7 @@ class Runtime {
   double* d_cbase_ = nullptr;   // base load field (device copy)
   double* d_cstage_ = nullptr;  // host-staged shifted field (host_io path)
   double* h_cstage_ = nullptr;  // pinned
-  double* h_loads_ = nullptr;   // pinned, per-step chunk times (host_io path)
+  unsigned long long* h_loads_ = nullptr;  // pinned, per-step chunk ns (host_io path)
   std::vector<ChunkMem> chunks_;  // indexed by vp; base == nullptr if not local
   std::multimap<size_t, double*> pool_;
   std::vector<int32_t> resident_;  // slot -> vp

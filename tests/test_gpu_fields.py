@@ -100,3 +100,56 @@ def test_fused_quota_edge_cases(n_inner, F, nz, mode):
     Uo, Ao = oracle_fields(cfg, 3)
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")
+
+
+def test_device_matches_committed_golden_fields():
+    # the committed golden vectors (tests/golden/fields.json, made by
+    # oracle/gen_golden.py) -- no oracle call at run time
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fields.json")))
+    for g in gold:
+        for mode in (0, 4):
+            cfg = small(nx=g["nx"], ny=g["ny"], nz=g["nz"], F=g["fields"], kx=g["kx"], ky=g["ky"],
+                        steps_window=tuple(g["window"]), n_inner=g["n_inner"], seed=g["seed"],
+                        adv=tuple(g["advection"]),
+                        pattern=od.LoadPattern(g["pattern"]), overlap=mode)
+            U, A, _ = device_fields(cfg, g["steps"])
+            want_u = np.array([float.fromhex(x) for x in g["U"]]).reshape(U.shape)
+            want_a = np.array([float.fromhex(x) for x in g["A"]]).reshape(A.shape)
+            assert_bitwise(U, want_u, "U")
+            assert_bitwise(A, want_a, "A")
+
+
+def test_host_io_path_matches_device_path():
+    # od_rt_advance_host (per-step H2D of the load field, D2H of per-chunk
+    # loads) computes the same fields as od_rt_advance
+    cfg = small(nx=96, ny=40, kx=3, ky=2, adv=(9, 1, 3), n_inner=7)
+    with od.Engine(cfg) as eng:
+        loads = np.zeros((5, cfg.vp_count()))
+        eng.advance_host(5, None, loads)
+        U, A, _ = eng.gather_fields()
+    Uo, Ao = oracle_fields(cfg, 5)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+    assert (loads > 0).all()
+
+
+def test_measured_loads_track_work_and_balancing_helps():
+    # per-chunk loads from the in-kernel timers rank chunks like their exact
+    # work; balancing on them lowers the next epoch's measured imbalance
+    cfg = od.ExperimentConfig(
+        cluster=od.ClusterSpec(1, 4), domain=od.Domain(256, 256, 16, 4),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 8, 8),
+        window=od.MeasurementWindow(1, 2), epochs=100, pattern=od.LoadPattern.UpperHalfHeavy,
+        heavy_value=3.0,
+        policy=od.BalancePolicy(od.Strategy.Greedy, od.Strategy.RefineSwap, 1.02, 0.02),
+        seed=3, n_inner=256)
+    with od.Engine(cfg) as eng:
+        r1 = eng.run_epoch(1)
+        heavy = [l for l, c in zip(r1.vp_loads, eng.subdomains()) if c.y_end <= 128]
+        light = [l for l, c in zip(r1.vp_loads, eng.subdomains()) if c.y_begin >= 128]
+        assert min(heavy) > 1.5 * max(light)
+        assert r1.imbalance_before > 1.3 and r1.plan.moves
+        r2 = eng.run_epoch(2)
+        assert r2.imbalance_before < 1.05

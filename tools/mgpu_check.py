@@ -45,12 +45,17 @@ same = all(x == allm[0] for x in allm)
 owned = int(own.sum())
 tot = [0] * world
 dist.all_gather_object(tot, owned)
-print(json.dumps({"rank": rank, "mode": mode, "fields_ok": ok_u and ok_a, "U_ok": ok_u,
+row = ({"rank": rank, "mode": mode, "fields_ok": ok_u and ok_a, "U_ok": ok_u,
                   "A_ok": ok_a, "consistent_plans": same, "owned_columns": owned,
                   "all_columns_covered": sum(tot) == 97 * 61,
                   "moves": [len(r.plan.moves) for r in recs],
                   "halo_bytes": st["halo_bytes_sent"], "migrated_bytes": st["migrated_bytes"],
                   "imbalance": [[round(r.imbalance_before, 3), round(r.imbalance_after, 3)]
-                                for r in recs]}), flush=True)
+                                for r in recs]})
+rows = [None] * world
+dist.all_gather_object(rows, row)
+if rank == 0:
+    for r in rows:
+        print(json.dumps(r), flush=True)
 eng.close()
 dist.destroy_process_group()
