@@ -399,6 +399,8 @@ def main():
         "epochs": [{k: (round(v, 6) if isinstance(v, float) else v) for k, v in h.items()}
                    for h in hist],
         "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
+        "pack_ms_total": st1["pack_ms"] - st0["pack_ms"],
+        "exchange_ms_total": st1["exchange_ms"] - st0["exchange_ms"],
         "migrated_bytes": st1["migrated_bytes"] - st0["migrated_bytes"],
     }
     print(json.dumps(line), file=json_out, flush=True)
