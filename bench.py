@@ -41,6 +41,8 @@ def parse_args():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="cfg4")
     p.add_argument("--n-inner", type=int, default=None)
+    p.add_argument("--kernel-mode", type=int, default=None,
+                   help="0 separate kernels, 4 fused, 5 fused persistent (default)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-lb-off", action="store_true")
@@ -207,6 +209,8 @@ def main():
     kw = {"epochs": 1 << 30}
     if args.n_inner is not None:
         kw["n_inner"] = args.n_inner
+    if args.kernel_mode is not None:
+        kw["overlap"] = args.kernel_mode
     cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
 
     if args.impl == "reference":
@@ -320,6 +324,14 @@ def main():
                     "bytes_per_launch": jac_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
 
     launches = st1["kernel_launches"] - st0["kernel_launches"]
+    mine = {"rank": rank, "kernel_avg_ms": round(kms, 3), "resident_chunks": st1["resident_chunks"],
+            "exchange_ms_total": round(st1["exchange_ms"] - st0["exchange_ms"], 2),
+            "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
+            "physics_trips": st1["physics_trips"]}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     balanced = [h for h in hist if h["strategy"] >= 0 and h["n_moves"] > 0]
     post_lb = None
     if balanced:
@@ -353,10 +365,17 @@ def main():
         eng2 = od.Engine(cfg_off, rank, world, local, new_nccl_id())
         eng2.advance(args.warmup)
         eng2.synchronize()
+        eng2.set_profiling(True)
+        s20 = eng2.stats()
         ms_off = timed(lambda: (eng2.advance(args.steps), eng2.synchronize()))
+        s21 = eng2.stats()
+        kt = (s21["fused_ms"] - s20["fused_ms"]) / max(s21["fused_timed"] - s20["fused_timed"], 1)
+        kts = [None] * world
+        dist.all_gather_object(kts, round(kt, 3))
         lb_off = {"value": cols * args.steps / (ms_off * 1e-3), "unit": UNIT,
                   "ms_per_step": ms_off / args.steps,
-                  "imbalance": [h["imbalance_before"] for h in eng2.epoch_history()][-3:]}
+                  "imbalance": [h["imbalance_before"] for h in eng2.epoch_history()][-3:],
+                  "kernel_avg_ms_per_rank": kts}
         eng2.close()
     elif world == 1:
         lb_off = {"note": "P=1: one processor never balances (imbalance_ratio = 1), "
@@ -400,6 +419,7 @@ def main():
                    for h in hist],
         "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
         "pack_ms_total": st1["pack_ms"] - st0["pack_ms"],
+        "per_rank": per_rank,
         "exchange_ms_total": st1["exchange_ms"] - st0["exchange_ms"],
         "migrated_bytes": st1["migrated_bytes"] - st0["migrated_bytes"],
     }

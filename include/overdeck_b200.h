@@ -280,6 +280,7 @@ int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
 typedef struct od_epoch_summary {
   int32_t epoch, strategy, n_moves, n_steps;
   double compute_total, migration_seconds, imbalance_before, imbalance_after;
+  double boundary_seconds; /* host wall time of the epoch end: gather, decide, migrate */
 } od_epoch_summary;
 int od_rt_epoch_history(od_runtime* rt, od_epoch_summary* out, int32_t cap, int32_t* n);
 /* enable per-kernel event timing (adds events around each batched kernel) */

@@ -94,7 +94,7 @@ class od_epoch_summary(C.Structure):
     _fields_ = [("epoch", C.c_int32), ("strategy", C.c_int32), ("n_moves", C.c_int32),
                 ("n_steps", C.c_int32), ("compute_total", C.c_double),
                 ("migration_seconds", C.c_double), ("imbalance_before", C.c_double),
-                ("imbalance_after", C.c_double)]
+                ("imbalance_after", C.c_double), ("boundary_seconds", C.c_double)]
 
 
 class od_face_xfer(C.Structure):

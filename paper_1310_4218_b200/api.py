@@ -574,8 +574,8 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
     # kernel mode: 0 Jacobi then physics, 1 two streams, 2 fused (1 column/thread),
-    # 3 fused pair kernel, 4 fused pair kernel v2 (default)
-    overlap: int = 4
+    # 3 fused pair kernel, 4 fused pair kernel v2, 5 persistent fused (default)
+    overlap: int = 5
 
     def vp_count(self) -> int:
         return self.decomposition.vp_count()

@@ -48,13 +48,15 @@ def cfg3(nodes: int = 8, **kw) -> ExperimentConfig:
     return c.replace(**kw)
 
 
-def cfg4(nodes: int = 1, **kw) -> ExperimentConfig:
-    """1024x1024x64, RefineSwapLB, cross-GPU halo exchange, strong scaling."""
+def cfg4(nodes: int = 1, moving: bool = False, **kw) -> ExperimentConfig:
+    """1024x1024x64, RefineSwapLB, cross-GPU halo exchange, strong scaling.
+    Hotspot: the upper half of the grid (static, BASELINE gives none for cfg4);
+    moving=True advects it half a domain during epoch 2 as cfg3 does."""
     c = ExperimentConfig(
         cluster=ClusterSpec(nodes, 1), domain=Domain(1024, 1024, 64, 50),
         decomposition=Decomposition(TWO_D, 16, 16), window=MeasurementWindow(6, 4), epochs=4,
         pattern=LoadPattern.UpperHalfHeavy, heavy_value=2.0, light_value=1.0,
-        advection=AdvectionSchedule(512, 2, 10),
+        advection=AdvectionSchedule(512, 2, 10) if moving else AdvectionSchedule(),
         policy=BalancePolicy(Strategy.RefineSwap, Strategy.RefineSwap, 1.05, 0.02), seed=54)
     return c.replace(**kw)
 

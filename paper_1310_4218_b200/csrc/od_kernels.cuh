@@ -713,22 +713,22 @@ __device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
 // receive faces alike, so every walker is p += ks), and a countdown that keeps
 // the two physics chains on the branch-free interleaved loop between trip
 // boundaries.  Same arithmetic as every other path.
-template <int TY, int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(32 * TY, MINB)
-    column_step3(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+// One 64 x TY column tile, all fields and levels (shared by the one-CTA-per-
+// tile launch and the persistent launch).
+template <int TY, int S, bool TIMED>
+__device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileDev tile,
+                                          const ChunkDev* __restrict__ chunks, int32_t nz,
+                                          int32_t F, const double* __restrict__ cfield,
+                                          int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
+                                          unsigned long long* __restrict__ chunk_ns) {
   constexpr int R = 8;
   constexpr int TXC = 64;
   constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
   constexpr int PLANE = (TY + 2) * PW;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  __shared__ __align__(16) double ring[R * PLANE];
-
   uint64_t t_start = 0;
   if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
 
-  const TileDev tile = tiles[blockIdx.x];
   const ChunkDev& c = chunks[tile.slot];
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int w = c.w, h = c.h, pitch = c.pitch;
@@ -893,6 +893,391 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
       atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+template <int TY, int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(32 * TY, MINB)
+    column_step3(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
+  tile_step<TY, S, TIMED>(ring, tiles[blockIdx.x], chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                          chunk_ns);
+}
+
+// Persistent variant: a fixed grid (one wave) pulls tiles, heaviest first,
+// from a counter, so the per-GPU time follows the work even when the GPU holds
+// few tiles (strong scaling) and heavy tiles do not end up in a ragged tail.
+template <int TY, int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(32 * TY, MINB)
+    column_step_persistent(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                           int32_t ntiles, unsigned int* __restrict__ counter, int32_t nz,
+                           int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                           int32_t shift, int32_t n_inner,
+                           unsigned long long* __restrict__ chunk_ns) {
+  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
+  __shared__ int s_next;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  for (;;) {
+    if (lead) s_next = int(atomicAdd(counter, 1u));
+    __syncthreads();
+    const int ti = s_next;
+    __syncthreads();  // everyone has read s_next and left the previous tile's ring
+    if (ti >= ntiles) break;
+    tile_step<TY, S, TIMED>(ring, tiles[ti], chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                            chunk_ns);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Four columns per thread: a 64 x 8 tile on 32 x 4 threads, each thread owning
+// columns (x, x+1) of rows y and y+4.  Four independent FP64 chains per thread
+// (the pipe saturates with one warp per SMSP) and twice the columns per CTA of
+// the pair kernel, so a GPU's whole share of columns fits in one wave at
+// strong-scaling sizes: the time follows the work, not the wave count.
+// Same arithmetic as every other path.
+// ---------------------------------------------------------------------------
+struct Chain {  // one column's recurrence; y doubles as A(l-1) between trips
+  double y, eb;
+  int l, i, r;  // level of the current trip, unit within it, trips left
+};
+
+__device__ __forceinline__ void chain_init(Chain& q, const double* B, const double* A, int T,
+                                           int nz, int64_t ks) {
+  q.y = A[0];
+  q.eb = 0.0;
+  q.l = nz > 1 ? 1 : 0;
+  q.i = 0;
+  q.r = T;
+  (void)B;
+  (void)ks;
+}
+
+// advance one chain by `budget` units (general path: trip setup / finish)
+__device__ __forceinline__ void chain_advance(Chain& q, int budget, const double* B, double* A,
+                                              int nz, int64_t ks, int n_inner) {
+  while (budget > 0 && q.r > 0) {
+    if (q.i == 0) {
+      const double b = B[q.l * ks];
+      q.eb = __fma_rn(b, kEps, kEps);
+      q.y = __fma_rn(0.5, q.y, __dmul_rn(0.5, b));
+      q.i = 1;
+      --budget;
+    }
+    const int m = min(budget, n_inner + 1 - q.i);
+    double y = q.y;
+    const double eb = q.eb;
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) {
+      const double u = __fma_rn(-y, y, y);
+      y = __fma_rn(kR, u, eb);
+    }
+    q.y = y;
+    q.i += m;
+    budget -= m;
+    if (q.i == n_inner + 1) {
+      A[q.l * ks] = y;
+      q.l = q.l + 1 == nz ? 0 : q.l + 1;
+      --q.r;
+      q.i = 0;
+    }
+  }
+}
+
+__device__ __forceinline__ int chain_fast(const Chain& q, int budget, int n_inner) {
+  return (q.i > 0 && q.r > 0 && budget > 0) ? (n_inner - q.i) / budget : 0;
+}
+
+template <int S, bool TIMED>
+__device__ __forceinline__ void tile_step4(double* __restrict__ ring, const TileDev tile,
+                                           const ChunkDev* __restrict__ chunks, int32_t nz,
+                                           int32_t F, const double* __restrict__ cfield,
+                                           int32_t nx, int32_t ny, int32_t shift,
+                                           int32_t n_inner,
+                                           unsigned long long* __restrict__ chunk_ns) {
+  constexpr int TY = 8, HALF = 4;
+  constexpr int R = 8;
+  constexpr int PW = 68;
+  constexpr int PLANE = (TY + 2) * PW;
+  static_assert(S + 2 <= R && S >= 3, "prefetch depth");
+  uint64_t t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+
+  const ChunkDev& c = chunks[tile.slot];
+  const int lx = threadIdx.x, ly = threadIdx.y;  // ly in [0, 4)
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride;
+  const int wv = min(64, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  const int x = tile.tx0 + 2 * lx;
+  const int ya = tile.ty0 + ly, yb = ya + HALF;
+  const int pair = max(0, min(2, wv - 2 * lx));
+  const int na = ly < hv ? pair : 0;          // active cells, row a
+  const int nb = ly + HALF < hv ? pair : 0;   // row b
+  const int64_t own_a = int64_t(ya) * pitch + x;
+  const int64_t own_b = own_a + int64_t(HALF) * pitch;
+
+  const double* pa = c.in + own_a;
+  const double* pb = c.in + own_b;
+  // x halos: lane 0 (left) / lane 31 (right), for both rows of this thread
+  const double* pxa = nullptr;
+  const double* pxb = nullptr;
+  int64_t xstep = 0;
+  int oxa = 0, oxb = 0;
+  if (lx == 0 || lx == 31) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    const int col = left ? 1 : wv + 2;
+    oxa = (ly + 1) * PW + col;
+    oxb = (ly + 1 + HALF) * PW + col;
+    if (xs >= 0 && xs < w) {
+      if (ly < hv) pxa = c.in + int64_t(ya) * pitch + xs;
+      if (ly + HALF < hv) pxb = c.in + int64_t(yb) * pitch + xs;
+      xstep = ks;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      if (ly < hv) pxa = fd.p + int64_t(ya) * fd.es;
+      if (ly + HALF < hv) pxb = fd.p + int64_t(yb) * fd.es;
+      xstep = fd.ks;
+    }
+  }
+  // y halos: row -1 by ly == 0, row hv by the thread owning row hv - 1
+  const double* py = nullptr;
+  int64_t ystep = 0;
+  int oy = 0, ycells = 0;
+  const bool top_duty = ly == 0;
+  const bool bot_duty = (hv - 1) == ly || (hv - 1) == ly + HALF;
+  const double* py2 = nullptr;
+  int64_t ystep2 = 0;
+  int oy2 = 0;
+  if (pair > 0 && top_duty) {
+    const int ys = tile.ty0 - 1;
+    oy = pair > 0 ? 2 + 2 * lx : 0;
+    ycells = pair;
+    if (ys >= 0) {
+      py = c.in + int64_t(ys) * pitch + x;
+      ystep = ks;
+    } else {
+      const FaceDev& fd = c.face[kTop];
+      py = fd.p + int64_t(x) * fd.es;
+      ystep = fd.ks;
+    }
+  }
+  if (pair > 0 && bot_duty) {
+    const int ys = tile.ty0 + hv;
+    oy2 = (hv + 1) * PW + 2 + 2 * lx;
+    ycells = pair;
+    if (ys < h) {
+      py2 = c.in + int64_t(ys) * pitch + x;
+      ystep2 = ks;
+    } else {
+      const FaceDev& fd = c.face[kBottom];
+      py2 = fd.p + int64_t(x) * fd.es;
+      ystep2 = fd.ks;
+    }
+  }
+  const int oca = (ly + 1) * PW + 2 + 2 * lx;
+  const int ocb = oca + HALF * PW;
+  const int levels = F * nz;
+
+  auto cp_cells = [&](double* dst, const double* src, int n) {
+    if (n == 2) cp_async16(dst, src);
+    else if (n == 1) cp_async8(dst, src);
+  };
+  auto issue = [&](int L) {
+    if (L < levels) {
+      double* slot = ring + (L & (R - 1)) * PLANE;
+      cp_cells(slot + oca, pa, na);
+      cp_cells(slot + ocb, pb, nb);
+      if (pxa) cp_async8(slot + oxa, pxa);
+      if (pxb) cp_async8(slot + oxb, pxb);
+      if (py) cp_cells(slot + oy, py, ycells);
+      if (py2) cp_cells(slot + oy2, py2, ycells);
+      pa += ks;
+      pb += ks;
+      if (pxa) pxa += xstep;  // a null duty pointer must stay null
+      if (pxb) pxb += xstep;
+      if (py) py += ystep;
+      if (py2) py2 += ystep2;
+    }
+    cp_async_commit();
+  };
+
+  // physics: chains 0,1 = row a (x, x+1); 2,3 = row b
+  const double* Bb = c.in;  // field 0 of U^t
+  double* Ab = c.a;
+  Chain ch[4];
+  int quota[4] = {0, 0, 0, 0};
+  int64_t off[4];
+  const int ncells[4] = {na >= 1, na == 2, nb >= 1, nb == 2};
+  off[0] = own_a;
+  off[1] = own_a + 1;
+  off[2] = own_b;
+  off[3] = own_b + 1;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int T = 0;
+    if (ncells[j]) {
+      const int cx = x + (j & 1), cy = (j < 2 ? ya : yb);
+      int row = c.y0 + cy - shift;
+      if (row < 0) row += ny;
+      const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + cx);
+      T = int(floor(__dmul_rn(double(nz), cm))) - 1;
+      if (T < 0) T = 0;
+      chain_init(ch[j], Bb + off[j], Ab + off[j], T, nz, ks);
+      quota[j] = int((int64_t(T) * (n_inner + 1) + levels - 1) / levels);
+      quota[j] = (quota[j] + 7) & ~7;
+    } else {
+      ch[j] = Chain{0.0, 0.0, 0, 0, 0};
+    }
+  }
+  const bool uniform = quota[0] == quota[1] && quota[1] == quota[2] && quota[2] == quota[3] &&
+                       ncells[0] && ncells[1] && ncells[2] && ncells[3];
+  int fast = 0;
+  auto physics = [&](int mult) {
+    if (fast > 0) {
+      const int b = quota[0] * mult;
+      double y0 = ch[0].y, y1 = ch[1].y, y2 = ch[2].y, y3 = ch[3].y;
+      const double e0 = ch[0].eb, e1 = ch[1].eb, e2 = ch[2].eb, e3 = ch[3].eb;
+      for (int j = 0; j < b; j += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double u0 = __fma_rn(-y0, y0, y0);
+          const double u1 = __fma_rn(-y1, y1, y1);
+          const double u2 = __fma_rn(-y2, y2, y2);
+          const double u3 = __fma_rn(-y3, y3, y3);
+          y0 = __fma_rn(kR, u0, e0);
+          y1 = __fma_rn(kR, u1, e1);
+          y2 = __fma_rn(kR, u2, e2);
+          y3 = __fma_rn(kR, u3, e3);
+        }
+      }
+      ch[0].y = y0;
+      ch[1].y = y1;
+      ch[2].y = y2;
+      ch[3].y = y3;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) ch[j].i += b;
+      --fast;
+      return;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ncells[j]) chain_advance(ch[j], quota[j] * mult, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+    if (uniform) {
+      const int b = quota[0] * mult;
+      int f = chain_fast(ch[0], b, n_inner);
+#pragma unroll
+      for (int j = 1; j < 4; ++j) f = min(f, chain_fast(ch[j], b, n_inner));
+      fast = f;
+    }
+  };
+
+  double zma0 = 0, zma1 = 0, zmb0 = 0, zmb1 = 0;
+  double* pouta = c.out + own_a;
+  double* poutb = c.out + own_b;
+  const double* rca = ring + oca;
+  const double* rcb = ring + ocb;
+  auto cell_pair = [&](const double* rc, int L, int k, int n, double& zm0, double& zm1,
+                       double* pout) {
+    const double* pl = rc + (L & (R - 1)) * PLANE;
+    if (n == 2) {
+      const double2 uc = *reinterpret_cast<const double2*>(pl);
+      const double xl = pl[-1], xr = pl[2];
+      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
+      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
+      double2 zu = uc;
+      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
+      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                  __dadd_rn(zd0, zu.x));
+      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                  __dadd_rn(zd1, zu.y));
+      double2 o;
+      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+      __stcs(reinterpret_cast<double2*>(pout), o);
+      zm0 = uc.x;
+      zm1 = uc.y;
+    } else if (n == 1) {
+      const double uc = pl[0];
+      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
+      const double zd = k > 0 ? zm0 : uc;
+      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
+                                   __dadd_rn(zd, zu));
+      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
+      zm0 = uc;
+    }
+  };
+
+#pragma unroll
+  for (int L = 0; L < S; ++L) issue(L);
+
+  int k = 0, L = 0;
+  for (; L + 1 < levels; L += 2) {
+    cp_async_wait<S - 3>();
+    __syncthreads();
+    issue(L + S);
+    issue(L + S + 1);
+    cell_pair(rca, L, k, na, zma0, zma1, pouta);
+    cell_pair(rcb, L, k, nb, zmb0, zmb1, poutb);
+    pouta += ks;
+    poutb += ks;
+    if (++k == nz) k = 0;
+    cell_pair(rca, L + 1, k, na, zma0, zma1, pouta);
+    cell_pair(rcb, L + 1, k, nb, zmb0, zmb1, poutb);
+    pouta += ks;
+    poutb += ks;
+    if (++k == nz) k = 0;
+    physics(2);
+  }
+  if (L < levels) {
+    cp_async_wait<0>();
+    __syncthreads();
+    cell_pair(rca, L, k, na, zma0, zma1, pouta);
+    cell_pair(rcb, L, k, nb, zmb0, zmb1, poutb);
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (ncells[j]) chain_advance(ch[j], 0x7fffffff, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+
+  if (TIMED) {
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+  }
+}
+
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    column_step4(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
+  __shared__ __align__(16) double ring[8 * 10 * 68];
+  tile_step4<S, TIMED>(ring, tiles[blockIdx.x], chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                       chunk_ns);
+}
+
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    column_step4_persistent(const ChunkDev* __restrict__ chunks,
+                            const TileDev* __restrict__ tiles, int32_t ntiles,
+                            unsigned int* __restrict__ counter, int32_t nz, int32_t F,
+                            const double* __restrict__ cfield, int32_t nx, int32_t ny,
+                            int32_t shift, int32_t n_inner,
+                            unsigned long long* __restrict__ chunk_ns) {
+  __shared__ __align__(16) double ring[8 * 10 * 68];
+  __shared__ int s_next;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  for (;;) {
+    if (lead) s_next = int(atomicAdd(counter, 1u));
+    __syncthreads();
+    const int ti = s_next;
+    __syncthreads();
+    if (ti >= ntiles) break;
+    tile_step4<S, TIMED>(ring, tiles[ti], chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                         chunk_ns);
   }
 }
 

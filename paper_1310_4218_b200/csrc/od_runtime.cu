@@ -146,7 +146,12 @@ class Runtime {
   double* h_cstage_ = nullptr;  // pinned
   unsigned long long* h_loads_ = nullptr;  // pinned, per-step chunk ns (host_io path)
   std::vector<ChunkMem> chunks_;  // indexed by vp; base == nullptr if not local
-  std::multimap<size_t, double*> pool_;
+  std::multimap<size_t, double*> pool_;  // individually allocated (fallback) buffers
+  double* slab_ = nullptr;                // preallocated chunk slots
+  size_t slot_bytes_ = 0;
+  std::vector<double*> free_slots_;
+  size_t slab_slots_ = 0;
+  void init_slab();
   std::vector<int32_t> resident_;  // slot -> vp
   std::vector<int32_t> tile_begin_, tile_count_;
   int32_t ntiles_ = 0;
@@ -155,6 +160,20 @@ class Runtime {
   int32_t ntiles2_ = 0;
   TileDev* d_tiles2_ = nullptr;
   size_t d_tiles2_cap_ = 0;
+  // persistent fused kernel: 64 x kTY4 tiles in descending-work order
+  int kTY4 = 4;  // persistent tile height: 4 (mode 5) or 8 (mode 6)
+  std::vector<TileDev> tiles4_;          // grouped by chunk
+  std::vector<int32_t> tile4_begin_, tile4_count_;
+  TileDev* d_tiles4_ = nullptr;          // grouped (per-chunk launches)
+  TileDev* d_tiles4s_[2] = {nullptr, nullptr};  // sorted, double buffered
+  TileDev* h_tiles4s_[2] = {nullptr, nullptr};  // pinned staging
+  cudaEvent_t tiles4s_ev_[2] = {nullptr, nullptr};
+  size_t tiles4_cap_ = 0;
+  int tiles4s_cur_ = 0;
+  bool order_dirty_ = true;
+  int persist_grid_ = 0;
+  int persist_minb_ = 5;
+  void refresh_tile_order();
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
   size_t d_chunks_cap_[2] = {0, 0};
   TileDev* d_tiles_ = nullptr;
@@ -214,7 +233,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       cfg.later_call_strategy < 0 || cfg.later_call_strategy > 1)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
-  if (cfg.overlap < 0 || cfg.overlap > 4) throw ValidationError("unknown kernel mode (overlap)");
+  if (cfg.overlap < 0 || cfg.overlap > 6) throw ValidationError("unknown kernel mode (overlap)");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER)
     throw ValidationError("unknown measurement mode");
   if (world != cfg.nodes)
@@ -253,6 +272,21 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, false>));
     set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, true>));
     set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, false>));
+    int per_sm = 0;
+    const char* pm = std::getenv("OD_PERSIST_MINB");
+    persist_minb_ = pm ? std::atoi(pm) : 5;
+    if (persist_minb_ == 6)
+      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, column_step_persistent<4, kFusedPrefetch, false, 6>, kTX * 4, 0));
+    else
+      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, column_step_persistent<4, kFusedPrefetch, false, 5>, kTX * 4, 0));
+    if (cfg.overlap == 6) {
+      kTY4 = 8;
+      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, column_step4_persistent<kFusedPrefetch, false, 4>, kTX * 4, 0));
+    }
+    persist_grid_ = sms * std::max(per_sm, 1);
   }
   if (world_ > 1) {
     ncclUniqueId id;
@@ -280,6 +314,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   OD_CU(cudaMemcpy(d_cbase_, base_.c.data(), cbytes, cudaMemcpyHostToDevice));
   set_shift(0);
 
+  init_slab();
   chunks_.resize(K());
   for (int32_t v = 0; v < K(); ++v) {
     if (rank_of_vp(v) != rank_) continue;
@@ -299,7 +334,10 @@ Runtime::~Runtime() {
   if (s0_) cudaStreamSynchronize(s0_);
   if (s1_) cudaStreamSynchronize(s1_);
   for (auto& m : chunks_)
-    if (m.base) cudaFree(m.base);
+    if (m.base && !(slab_ && m.base >= slab_ &&
+                    m.base < slab_ + slab_slots_ * (slot_bytes_ / sizeof(double))))
+      cudaFree(m.base);
+  cudaFree(slab_);
   for (auto& kv : pool_) cudaFree(kv.second);
   for (auto e : events_) cudaEventDestroy(e);
   cudaFree(d_cbase_);
@@ -310,6 +348,12 @@ Runtime::~Runtime() {
   cudaFree(d_chunks_[1]);
   cudaFree(d_tiles_);
   cudaFree(d_tiles2_);
+  cudaFree(d_tiles4_);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(d_tiles4s_[b]);
+    if (h_tiles4s_[b]) cudaFreeHost(h_tiles4s_[b]);
+    if (tiles4s_ev_[b]) cudaEventDestroy(tiles4s_ev_[b]);
+  }
   cudaFree(d_jobs_);
   cudaFree(d_send_);
   cudaFree(d_recv_);
@@ -331,6 +375,38 @@ int32_t Runtime::nbr(int32_t v, int d) const {
 void Runtime::set_shift(int32_t rows) {
   shift_ = rows;
   field_ = shift_rows_down(base_, rows % cfg_.ny);
+  order_dirty_ = true;
+}
+
+// Heaviest tiles first (longest-processing-time order) for the persistent
+// kernel: estimated work = physics units + Jacobi cells, from the current field.
+void Runtime::refresh_tile_order() {
+  const size_t n = tiles4_.size();
+  if (n == 0) return;
+  std::vector<std::pair<double, int32_t>> key(n);
+  const double jac = 2.0 * cfg_.nz * cfg_.fields;  // a Jacobi cell ~ 2 micro-steps
+  for (size_t t = 0; t < n; ++t) {
+    const TileDev& td = tiles4_[t];
+    const Sub& s = subs_[resident_[td.slot]];
+    const int32_t x0 = s.x0 + td.tx0, x1 = std::min(s.x1, x0 + 2 * kTX);
+    const int32_t y0 = s.y0 + td.ty0, y1 = std::min(s.y1, y0 + kTY4);
+    double w = 0;
+    for (int32_t y = y0; y < y1; ++y)
+      for (int32_t x = x0; x < x1; ++x) {
+        const int32_t T = int32_t(std::floor(double(cfg_.nz) * field_.at(x, y))) - 1;
+        w += double(T > 0 ? T : 0) * (cfg_.n_inner + 1) + jac;
+      }
+    key[t] = {-w, int32_t(t)};
+  }
+  std::stable_sort(key.begin(), key.end());
+  const int b = tiles4s_cur_ ^ 1;
+  OD_CU(cudaEventSynchronize(tiles4s_ev_[b]));  // previous upload from this buffer done
+  for (size_t t = 0; t < n; ++t) h_tiles4s_[b][t] = tiles4_[key[t].second];
+  OD_CU(cudaMemcpyAsync(d_tiles4s_[b], h_tiles4s_[b], n * sizeof(TileDev),
+                        cudaMemcpyHostToDevice, s0_));
+  OD_CU(cudaEventRecord(tiles4s_ev_[b], s0_));
+  tiles4s_cur_ = b;
+  order_dirty_ = false;
 }
 
 // engine.hpp:323-336
@@ -356,6 +432,29 @@ std::vector<int32_t> Runtime::classify() const {
 
 // ----------------------------------------------------------------- memory --
 
+// One slab of equal chunk slots, sized at creation for the resident chunks plus
+// migration headroom (bounded by free HBM), so migrations do not cudaMalloc.
+void Runtime::init_slab() {
+  for (const Sub& sb : subs_) {
+    const size_t plane = size_t(sb.h()) * ((sb.w() + 15) / 16 * 16);
+    const size_t b = (2 * plane * cfg_.nz * cfg_.fields + plane * cfg_.nz) * sizeof(double);
+    slot_bytes_ = std::max(slot_bytes_, (b + 4095) / 4096 * 4096);
+  }
+  size_t resident = 0;
+  for (int32_t v = 0; v < K(); ++v) resident += rank_of_vp(v) == rank_;
+  size_t want = world_ == 1 ? resident : std::min<size_t>(K(), 2 * resident + 4);
+  size_t free_b = 0, total_b = 0;
+  OD_CU(cudaMemGetInfo(&free_b, &total_b));
+  const size_t margin = size_t(6) << 30;
+  const size_t fit = free_b > margin ? (free_b - margin) / slot_bytes_ : 0;
+  want = std::max(resident, std::min(want, fit));
+  if (want == 0) return;
+  OD_CU(cudaMalloc(&slab_, want * slot_bytes_));
+  slab_slots_ = want;
+  free_slots_.reserve(want);
+  for (size_t i = want; i-- > 0;) free_slots_.push_back(slab_ + i * (slot_bytes_ / sizeof(double)));
+}
+
 ChunkMem Runtime::alloc_chunk(int32_t vp) {
   ChunkMem m;
   m.vp = vp;
@@ -364,12 +463,17 @@ ChunkMem Runtime::alloc_chunk(int32_t vp) {
   const size_t plane = size_t(m.sub.h()) * m.pitch;
   const size_t field_elems = plane * cfg_.nz * cfg_.fields;
   m.bytes = (2 * field_elems + plane * cfg_.nz) * sizeof(double);
-  auto it = pool_.find(m.bytes);
-  if (it != pool_.end()) {
-    m.base = it->second;
-    pool_.erase(it);
+  if (!free_slots_.empty() && m.bytes <= slot_bytes_) {
+    m.base = free_slots_.back();
+    free_slots_.pop_back();
   } else {
-    OD_CU(cudaMalloc(&m.base, m.bytes));
+    auto it = pool_.find(m.bytes);
+    if (it != pool_.end()) {
+      m.base = it->second;
+      pool_.erase(it);
+    } else {
+      OD_CU(cudaMalloc(&m.base, m.bytes));
+    }
   }
   m.u[0] = m.base;
   m.u[1] = m.base + field_elems;
@@ -378,7 +482,14 @@ ChunkMem Runtime::alloc_chunk(int32_t vp) {
 }
 
 void Runtime::release_chunk(ChunkMem& m) {
-  if (m.base) pool_.emplace(m.bytes, m.base);
+  if (m.base) {
+    const bool slab = slab_ && m.base >= slab_ &&
+                      m.base < slab_ + slab_slots_ * (slot_bytes_ / sizeof(double));
+    if (slab)
+      free_slots_.push_back(m.base);
+    else
+      pool_.emplace(m.bytes, m.base);
+  }
   m = ChunkMem();
 }
 
@@ -401,7 +512,7 @@ static void upload(T*& dptr, size_t& cap, const std::vector<T>& h) {
   if (h.size() > cap) {
     cudaFree(dptr);
     dptr = nullptr;
-    cap = std::max<size_t>(h.size(), 16);
+    cap = std::max<size_t>(h.size() * 2, 16);
     OD_CU(cudaMalloc(&dptr, cap * sizeof(T)));
   }
   if (!h.empty()) OD_CU(cudaMemcpy(dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
@@ -440,6 +551,38 @@ void Runtime::rebuild_tables() {
   }
   ntiles2_ = int32_t(tiles2.size());
   upload(d_tiles2_, d_tiles2_cap_, tiles2);
+  tiles4_.clear();
+  tile4_begin_.assign(nres, 0);
+  tile4_count_.assign(nres, 0);
+  for (int32_t i = 0; i < nres; ++i) {
+    const Sub& s = subs_[resident_[i]];
+    tile4_begin_[i] = int32_t(tiles4_.size());
+    for (int32_t ty = 0; ty < s.h(); ty += kTY4)
+      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) tiles4_.push_back(TileDev{i, tx, ty, 0});
+    tile4_count_[i] = int32_t(tiles4_.size()) - tile4_begin_[i];
+  }
+  if (tiles4_.size() > tiles4_cap_) {
+    OD_CU(cudaStreamSynchronize(s0_));
+    cudaFree(d_tiles4_);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(d_tiles4s_[b]);
+      if (h_tiles4s_[b]) cudaFreeHost(h_tiles4s_[b]);
+    }
+    size_t all = 0;
+    for (const Sub& sb : subs_)
+      all += size_t((sb.h() + kTY4 - 1) / kTY4) * size_t((sb.w() + 2 * kTX - 1) / (2 * kTX));
+    tiles4_cap_ = std::max<size_t>({tiles4_.size(), all, 16});
+    OD_CU(cudaMalloc(&d_tiles4_, tiles4_cap_ * sizeof(TileDev)));
+    for (int b = 0; b < 2; ++b) {
+      OD_CU(cudaMalloc(&d_tiles4s_[b], tiles4_cap_ * sizeof(TileDev)));
+      OD_CU(cudaMallocHost(&h_tiles4s_[b], tiles4_cap_ * sizeof(TileDev)));
+      if (!tiles4s_ev_[b]) OD_CU(cudaEventCreateWithFlags(&tiles4s_ev_[b], cudaEventDisableTiming));
+    }
+  }
+  if (!tiles4_.empty())
+    OD_CU(cudaMemcpy(d_tiles4_, tiles4_.data(), tiles4_.size() * sizeof(TileDev),
+                     cudaMemcpyHostToDevice));
+  order_dirty_ = true;
 
   // exchange schedule: per peer, faces in (sender vp, side) order
   jobs_.clear();
@@ -475,13 +618,13 @@ void Runtime::rebuild_tables() {
   if (size_t(soff) > send_cap_) {
     cudaFree(d_send_);
     d_send_ = nullptr;
-    send_cap_ = size_t(soff);
+    send_cap_ = std::max(size_t(soff) * 3 / 2, send_cap_ * 2);
     OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
   }
   if (size_t(roff) > recv_cap_) {
     cudaFree(d_recv_);
     d_recv_ = nullptr;
-    recv_cap_ = size_t(roff);
+    recv_cap_ = std::max(size_t(roff) * 3 / 2, recv_cap_ * 2);
     OD_CU(cudaMalloc(&d_recv_, recv_cap_ * sizeof(double)));
   }
   upload(d_jobs_, d_jobs_cap_, jobs_);
@@ -661,6 +804,62 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
     st_.kernel_launches += 1;
     st_.fused_launches += 1;
+  } else if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6) {
+    if (order_dirty_) refresh_tile_order();
+    int e0 = -1, e1 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
+    const int nt = int(tiles4_.size());
+    const int grid = std::min(nt, persist_grid_);
+    if (timer)
+      column_step4_persistent<kFusedPrefetch, true, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
+          d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
+          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns);
+    else
+      column_step4_persistent<kFusedPrefetch, false, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
+          d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
+          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr);
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+      prof_f_.push_back({e0, e1});
+    }
+    st_.kernel_launches += 1;
+    st_.fused_launches += 1;
+  } else if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 5) {
+    if (order_dirty_) refresh_tile_order();
+    int e0 = -1, e1 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
+    const int nt = int(tiles4_.size());
+    const int grid = std::min(nt, persist_grid_);
+    const dim3 blk4(kTX, 4);
+#define OD_LAUNCH_PS(MB)                                                                    \
+  if (timer)                                                                                \
+    column_step_persistent<4, kFusedPrefetch, true, MB><<<grid, blk4, 0, s0_>>>(         \
+        d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
+        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns);                                 \
+  else                                                                                      \
+    column_step_persistent<4, kFusedPrefetch, false, MB><<<grid, blk4, 0, s0_>>>(        \
+        d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
+        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr);
+    if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
+#undef OD_LAUNCH_PS
+    OD_CU(cudaGetLastError());
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+      prof_f_.push_back({e0, e1});
+    }
+    st_.kernel_launches += 1;
+    st_.fused_launches += 1;
   } else if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 4) {
     int e0 = -1, e1 = -1;
     if (profiling_) {
@@ -801,7 +1000,15 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     for (int32_t i = 0; i < nres; ++i) {
       const int eb = new_event(), ee = new_event();
       OD_CU(cudaEventRecord(events_[eb], s0_));
-      if (cfg_.overlap == 4) {
+      if (cfg_.overlap == 6) {
+        column_step4<kFusedPrefetch, false, 4><<<tile4_count_[i], dim3(kTX, 4), 0, s0_>>>(
+            d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      } else if (cfg_.overlap == 5) {
+        column_step3<4, kFusedPrefetch, false, 6><<<tile4_count_[i], dim3(kTX, 4), 0, s0_>>>(
+            d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      } else if (cfg_.overlap == 4) {
         column_step3<kTY, kFusedPrefetch, false, 3><<<tile2_count_[i], blk, 0, s0_>>>(
             d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
             cfg_.ny, shift, cfg_.n_inner, nullptr);
@@ -928,6 +1135,7 @@ void Runtime::step_api(int32_t mode, int32_t epoch_step, double* wall, od_sample
 
 // engine.hpp:235-272 with measured samples and real migration
 void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
+  const auto tb = std::chrono::steady_clock::now();
   std::vector<double> samples;
   collect(o.walls, samples);
   SampleStore db(K(), cfg_.async_steps, cfg_.sync_steps);
@@ -958,6 +1166,7 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
   h.migration_seconds = o.mig_s;
   h.imbalance_before = o.imb_before;
   h.imbalance_after = o.imb_after;
+  h.boundary_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - tb).count();
   history_.push_back(h);
 }
 

@@ -25,7 +25,9 @@ def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps
 
 @pytest.mark.parametrize("kx,ky,overlap", [(1, 1, 0), (4, 3, 0), (2, 5, 0), (4, 3, 1), (1, 1, 1),
                                            (1, 1, 2), (4, 3, 2), (2, 5, 2), (1, 1, 3), (4, 3, 3),
-                                           (2, 5, 3), (1, 1, 4), (4, 3, 4), (2, 5, 4)])
+                                           (2, 5, 3), (1, 1, 4), (4, 3, 4), (2, 5, 4),
+                                           (1, 1, 5), (4, 3, 5), (2, 5, 5),
+                                           (1, 1, 6), (4, 3, 6), (2, 5, 6)])
 def test_fields_bitwise_2d(kx, ky, overlap):
     cfg = small(kx=kx, ky=ky, overlap=overlap)
     U, A, _ = device_fields(cfg, 3)
@@ -34,7 +36,7 @@ def test_fields_bitwise_2d(kx, ky, overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 2, 3, 4])
+@pytest.mark.parametrize("overlap", [0, 2, 3, 4, 5, 6])
 def test_fields_bitwise_1d_strips(overlap):
     cfg = small(nx=45, ny=30, kind=ONE_D, kx=1, ky=7, overlap=overlap)
     U, A, _ = device_fields(cfg, 4)
@@ -45,7 +47,7 @@ def test_fields_bitwise_1d_strips(overlap):
 
 def test_fields_multi_tile_chunks_and_advection():
     # chunks wider than one 32-column tile and taller than 8 rows; moving band
-    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=4)
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=5)
     U, A, _ = device_fields(cfg, 5)
     Uo, Ao = oracle_fields(cfg, 5)
     assert_bitwise(U, Uo, "U")
@@ -53,7 +55,7 @@ def test_fields_multi_tile_chunks_and_advection():
 
 
 @pytest.mark.parametrize("overlap,n_inner", [(0, 5), (2, 5), (2, 0), (2, 40), (3, 5), (3, 0),
-                                             (3, 40), (4, 5), (4, 0), (4, 40)])
+                                             (3, 40), (4, 5), (4, 0), (4, 40), (5, 5), (5, 0), (5, 40), (6, 5), (6, 0), (6, 40)])
 def test_fields_edge_shapes(overlap, n_inner):
     # nz = 1 (no vertical neighbours, physics trips 0 or 1), single field
     cfg = small(nx=33, ny=9, nz=1, F=1, kx=3, ky=2, heavy=3.0, overlap=overlap, n_inner=n_inner)
@@ -67,7 +69,7 @@ def test_fields_invariant_under_balancing_and_procs():
     # 3 processors sharing the GPU, balancing every epoch: mapping changes,
     # values must not
     cfg = small(nx=64, ny=40, kx=4, ky=4, ppn=3, threshold=1.0, steps_window=(1, 1),
-                adv=(20, 2, 2), overlap=4)
+                adv=(20, 2, 2), overlap=6)
     U, A, recs = device_fields(cfg, 6, use_epochs=True)
     assert any(r.plan.moves for r in recs)
     Uo, Ao = oracle_fields(cfg, 6)
@@ -75,7 +77,7 @@ def test_fields_invariant_under_balancing_and_procs():
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 2, 3, 4])
+@pytest.mark.parametrize("overlap", [0, 2, 3, 4, 5, 6])
 def test_events_measurement_mode(overlap):
     cfg = small(nx=64, ny=32, kx=4, ky=2, measure=od.MeasureMode.Events, overlap=overlap)
     with od.Engine(cfg) as eng:
@@ -90,7 +92,7 @@ def test_events_measurement_mode(overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("mode", [2, 3, 4])
+@pytest.mark.parametrize("mode", [2, 3, 4, 5, 6])
 @pytest.mark.parametrize("n_inner,F,nz", [(0, 2, 5), (1, 3, 7), (13, 1, 4), (200, 2, 3)])
 def test_fused_quota_edge_cases(n_inner, F, nz, mode):
     # quota rounding: recurrences longer/shorter than the Jacobi level count;
@@ -109,7 +111,7 @@ def test_device_matches_committed_golden_fields():
     import os
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fields.json")))
     for g in gold:
-        for mode in (0, 4):
+        for mode in (0, 4, 5, 6):
             cfg = small(nx=g["nx"], ny=g["ny"], nz=g["nz"], F=g["fields"], kx=g["kx"], ky=g["ky"],
                         steps_window=tuple(g["window"]), n_inner=g["n_inner"], seed=g["seed"],
                         adv=tuple(g["advection"]),
