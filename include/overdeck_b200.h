@@ -40,8 +40,10 @@ enum { OD_UNIFORM = 0, OD_STATIC_NODE0 = 1, OD_UPPER_HALF_HEAVY = 2 };
 enum { OD_ONE_D = 0, OD_TWO_D = 1 };
 /* per-chunk load measurement in Sync steps */
 enum {
-  OD_MEASURE_EVENTS = 0, /* paper protocol: one launch per chunk, cudaEvent pair */
-  OD_MEASURE_TIMER = 1   /* batched launch, in-kernel per-chunk SM-time accumulation */
+  OD_MEASURE_EVENTS = 0,   /* paper protocol: one launch per chunk, cudaEvent pair */
+  OD_MEASURE_TIMER = 1,    /* batched launch; in-kernel per-chunk SM time apportions the
+                              GPU's event-timed kernel time (per-GPU sums = busy time) */
+  OD_MEASURE_TIMER_RAW = 2 /* batched launch, raw per-chunk SM-time sums */
 };
 
 /* Move{vp, from, to}                                   cluster.hpp:62-67 */

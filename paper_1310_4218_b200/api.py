@@ -70,8 +70,9 @@ class DecompositionKind(enum.IntEnum):  # engine.hpp:18
 
 
 class MeasureMode(enum.IntEnum):
-    Events = 0  # paper protocol: serialised per-chunk launches, cudaEvent pairs
-    Timer = 1   # batched launch, in-kernel per-chunk SM time
+    Events = 0    # paper protocol: serialised per-chunk launches, cudaEvent pairs
+    Timer = 1     # batched launch, chunk SM-time shares of the GPU's measured kernel time
+    TimerRaw = 2  # batched launch, raw per-chunk SM-time sums
 
 
 def _dptr(a: np.ndarray):

@@ -715,7 +715,7 @@ __device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
 // boundaries.  Same arithmetic as every other path.
 // One 64 x TY column tile, all fields and levels (shared by the one-CTA-per-
 // tile launch and the persistent launch).
-template <int TY, int S, bool TIMED>
+template <int TY, int S, bool TIMED, bool FULL = false>
 __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileDev tile,
                                           const ChunkDev* __restrict__ chunks, int32_t nz,
                                           int32_t F, const double* __restrict__ cfield,
@@ -733,7 +733,10 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   const int lx = threadIdx.x, ly = threadIdx.y;
   const int w = c.w, h = c.h, pitch = c.pitch;
   const int64_t ks = c.kstride;
-  const int wv = min(TXC, w - tile.tx0), hv = min(TY, h - tile.ty0);
+  // FULL: the tile lies inside the chunk, every thread owns two cells (the
+  // common case); the compiler drops all partial-tile predicates
+  const int wv = FULL ? TXC : min(TXC, w - tile.tx0);
+  const int hv = FULL ? TY : min(TY, h - tile.ty0);
   const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
   const int pair = max(0, min(2, wv - 2 * lx));  // cells of this thread's pair inside the chunk
   const int ncell = ly < hv ? pair : 0;
@@ -806,9 +809,10 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     if (fast > 0) {
       double y0 = s0.y, y1 = s1.y;
       const double e0 = s0.eb, e1 = s1.eb;
-      for (int j = 0; j < b0; j += 8) {
+      // b0 is a multiple of 16 (quota rounded to 8, two levels per call)
+      for (int j = 0; j < b0; j += 16) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const double u0 = __fma_rn(-y0, y0, y0);
           const double u1 = __fma_rn(-y1, y1, y1);
           y0 = __fma_rn(kR, u0, e0);
@@ -906,6 +910,19 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                           chunk_ns);
 }
 
+// Partial tiles (chunk edges narrower than 64 x TY) take an out-of-line path so
+// their predicates do not cost registers in the common full-tile code.
+template <int TY, int S, bool TIMED>
+__device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const TileDev tile,
+                                               const ChunkDev* __restrict__ chunks, int32_t nz,
+                                               int32_t F, const double* __restrict__ cfield,
+                                               int32_t nx, int32_t ny, int32_t shift,
+                                               int32_t n_inner,
+                                               unsigned long long* __restrict__ chunk_ns) {
+  tile_step<TY, S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                 chunk_ns);
+}
+
 // Persistent variant: a fixed grid (one wave) pulls tiles, heaviest first,
 // from a counter, so the per-GPU time follows the work even when the GPU holds
 // few tiles (strong scaling) and heavy tiles do not end up in a ragged tail.
@@ -925,8 +942,14 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     const int ti = s_next;
     __syncthreads();  // everyone has read s_next and left the previous tile's ring
     if (ti >= ntiles) break;
-    tile_step<TY, S, TIMED>(ring, tiles[ti], chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                            chunk_ns);
+    const TileDev t = tiles[ti];
+    const ChunkDev& c = chunks[t.slot];
+    if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
+      tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                    chunk_ns);
+    else
+      tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                      chunk_ns);
   }
 }
 

@@ -23,6 +23,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -53,6 +54,14 @@ namespace odb {
                          #expr);                                                         \
   } while (0)
 
+static bool trace_on() {
+  static const bool on = std::getenv("OD_TRACE") != nullptr;
+  return on;
+}
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 constexpr int kTX = 32, kTY = 8, kPrefetch = 4, kFusedPrefetch = 6;
 
 static int opposite(int d) { return d ^ 1; }
@@ -75,6 +84,7 @@ struct StepRec {
   double host_launch_s = 0;
   int ns_row = -1;                  // TIMER: row of the per-chunk ns counters
   int chunk_ev0 = -1;               // EVENTS: first event of the per-chunk pairs
+  int kev0 = -1, kev1 = -1;         // TIMER: events around the step's compute kernels
   std::vector<int32_t> slot_vps;    // resident vps at launch time (slot order)
 };
 
@@ -234,7 +244,8 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
   if (cfg.overlap < 0 || cfg.overlap > 6) throw ValidationError("unknown kernel mode (overlap)");
-  if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER)
+  if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER &&
+      cfg.measure != OD_MEASURE_TIMER_RAW)
     throw ValidationError("unknown measurement mode");
   if (world != cfg.nodes)
     throw ValidationError("one rank per node GPU: world size must equal cluster.nodes");
@@ -519,6 +530,7 @@ static void upload(T*& dptr, size_t& cap, const std::vector<T>& h) {
 }
 
 void Runtime::rebuild_tables() {
+  const double r0 = now_s();
   resident_.clear();
   for (int32_t v = 0; v < K(); ++v)
     if (rank_of_vp(v) == rank_) resident_.push_back(v);
@@ -584,6 +596,7 @@ void Runtime::rebuild_tables() {
                      cudaMemcpyHostToDevice));
   order_dirty_ = true;
 
+  const double r1 = now_s();
   // exchange schedule: per peer, faces in (sender vp, side) order
   jobs_.clear();
   send_off_.assign(world_, 0);
@@ -615,6 +628,16 @@ void Runtime::rebuild_tables() {
     so += send_cnt_[q];
     ro += recv_cnt_[q];
   }
+  if (world_ > 1 && send_cap_ == 0) {
+    // worst case for this rank: every face of every chunk slot remote
+    size_t per = 0;
+    for (const Sub& sb : subs_)
+      per = std::max<size_t>(per, size_t(2 * (((sb.w() + 1) & ~1) + ((sb.h() + 1) & ~1))));
+    const size_t slots = std::max<size_t>(slab_slots_, resident_.size());
+    send_cap_ = recv_cap_ = per * size_t(per_cell) * slots;
+    OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
+    OD_CU(cudaMalloc(&d_recv_, recv_cap_ * sizeof(double)));
+  }
   if (size_t(soff) > send_cap_) {
     cudaFree(d_send_);
     d_send_ = nullptr;
@@ -628,6 +651,7 @@ void Runtime::rebuild_tables() {
     OD_CU(cudaMalloc(&d_recv_, recv_cap_ * sizeof(double)));
   }
   upload(d_jobs_, d_jobs_cap_, jobs_);
+  const double r2 = now_s();
 
   // chunk descriptors for both parities
   for (int par = 0; par < 2; ++par) {
@@ -666,7 +690,7 @@ void Runtime::rebuild_tables() {
     upload(d_chunks_[par], d_chunks_cap_[par], tab);
   }
   if (!d_trips_ || ns_cols_ < nres) {
-    ns_cols_ = std::max(nres, 1);
+    ns_cols_ = std::max(std::max(nres, 1), int(slab_slots_));
     cudaFree(d_trips_);
     OD_CU(cudaMalloc(&d_trips_, size_t(ns_cols_) * sizeof(unsigned long long)));
     cudaFree(d_ns_);
@@ -674,6 +698,9 @@ void Runtime::rebuild_tables() {
     ns_rows_ = 0;
   }
   st_.resident_chunks = nres;
+  if (trace_on())
+    fprintf(stderr, "[od rank %d] rebuild: tiles %.2f ms, exchange %.2f ms, chunk tables %.2f ms\n",
+            rank_, (r1 - r0) * 1e3, (r2 - r1) * 1e3, (now_s() - r2) * 1e3);
 }
 
 // ------------------------------------------------------------------- steps --
@@ -706,7 +733,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   r.slot_vps = resident_;
   const int par = parity_;
   const int32_t nres = int32_t(resident_.size());
-  const bool timer = host_io || (mode == kSync && cfg_.measure == OD_MEASURE_TIMER);
+  const bool timer = host_io || (mode == kSync && (cfg_.measure == OD_MEASURE_TIMER ||
+                                                    cfg_.measure == OD_MEASURE_TIMER_RAW));
   r.ev_begin = new_event();
   OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
 
@@ -778,6 +806,10 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   const dim3 blk(kTX, kTY);
+  if (timer) {
+    r.kev0 = new_event();
+    OD_CU(cudaEventRecord(events_[r.kev0], s0_));
+  }
   if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 3) {
     int e0 = -1, e1 = -1;
     if (profiling_) {
@@ -1035,6 +1067,10 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       st_.physics_launches += 1;
     }
   }
+  if (timer) {
+    r.kev1 = new_event();
+    OD_CU(cudaEventRecord(events_[r.kev1], s0_));
+  }
   if (host_io && nres > 0) {
     // the step's per-chunk device times back to the host
     OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(nres) * sizeof(unsigned long long),
@@ -1072,8 +1108,18 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
     local[size_t(S) * Kv + s] = elapsed_s(events_[r.ev_begin], events_[r.ev_end]);
     for (size_t i = 0; i < r.slot_vps.size(); ++i) {
       double v;
-      if (r.ns_row >= 0 && r.mode == kSync)
+      if (r.ns_row >= 0 && r.mode == kSync) {
         v = double(ns[size_t(r.ns_row) * ns_cols_ + i]) * 1e-9;
+        if (cfg_.measure == OD_MEASURE_TIMER && r.kev0 >= 0) {
+          // the chunk's SM-time share of this GPU's measured kernel time, so the
+          // per-GPU sums are the GPUs' real busy times
+          double sum = 0;
+          for (size_t j = 0; j < r.slot_vps.size(); ++j)
+            sum += double(ns[size_t(r.ns_row) * ns_cols_ + j]);
+          const double kt = elapsed_s(events_[r.kev0], events_[r.kev1]);
+          v = sum > 0 ? double(ns[size_t(r.ns_row) * ns_cols_ + i]) / sum * kt : 0.0;
+        }
+      }
       else if (r.mode == kSync && r.chunk_ev0 >= 0)
         v = elapsed_s(events_[r.chunk_ev0 + 2 * i], events_[r.chunk_ev0 + 2 * i + 1]);
       else
@@ -1264,7 +1310,9 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
 // ---------------------------------------------------------------- migrate --
 
 void Runtime::migrate(const std::vector<MoveRec>& plan) {
+  const double t0 = now_s();
   std::vector<int32_t> next = apply_moves(map_, P(), plan);  // throws before any data moves
+  double t1 = t0, t2 = t0, t3 = t0;
   if (world_ > 1) {
     std::vector<int32_t> moved;
     for (int32_t v = 0; v < K(); ++v)
@@ -1273,6 +1321,7 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
     for (int32_t v : moved)
       if (rank_of_proc(next[v]) == rank_) incoming[v] = alloc_chunk(v);
     OD_CU(cudaStreamSynchronize(s0_));
+    t1 = now_s();
     OD_NC(odb::nccl().GroupStart());
     for (int32_t v : moved) {
       const int src = rank_of_proc(map_[v]), dst = rank_of_proc(next[v]);
@@ -1290,13 +1339,19 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
     }
     OD_NC(odb::nccl().GroupEnd());
     OD_CU(cudaStreamSynchronize(s0_));
+    t2 = now_s();
     for (int32_t v : moved) {
       if (rank_of_proc(map_[v]) == rank_) release_chunk(chunks_[v]);
       if (rank_of_proc(next[v]) == rank_) chunks_[v] = incoming[v];
     }
   }
   map_ = std::move(next);
+  t3 = now_s();
   rebuild_tables();
+  if (trace_on())
+    fprintf(stderr, "[od rank %d] migrate: alloc+sync %.2f ms, transfer %.2f ms, release %.2f ms, "
+            "rebuild %.2f ms, moves %zu\n", rank_, (t1 - t0) * 1e3, (t2 - t1) * 1e3,
+            (t3 - t2) * 1e3, (now_s() - t3) * 1e3, plan.size());
 }
 
 bool Runtime::read_chunk(int32_t vp, double* u, double* a) {
