@@ -124,6 +124,7 @@ def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=64, side=256, warmup=0):
     n_inner and load pattern."""
     import numpy as np
     from oracle import fields as of
+    threads = of.set_threads(os.cpu_count() or 1)
     d = cfg.domain
     nx, ny = min(side, d.nx), min(side, d.ny)
     U, A = of.init_state(nx, ny, d.nz, d.fields, cfg.seed)
@@ -142,7 +143,7 @@ def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=64, side=256, warmup=0):
             break
     dt = time.perf_counter() - t0
     return nx * ny * steps / dt, {"grid": [nx, ny, d.nz], "fields": d.fields, "steps": steps,
-                                  "seconds": dt}
+                                  "seconds": dt, "threads": threads}
 
 
 def reference_arm(args, cfg):
@@ -151,7 +152,7 @@ def reference_arm(args, cfg):
     bounded sample of the same workload."""
     import numpy as np
     from oracle import fields as of
-    cores = os.cpu_count() or 1
+    cores = of.set_threads(os.cpu_count() or 1)
     d = cfg.domain
     side = 128
     nx, ny = min(side, d.nx), min(side, d.ny)
@@ -384,7 +385,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         rate, info = cpu_sample_rate(cfg)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": rate, "unit": UNIT, "cores": info["threads"], "kind": "port",
                "sample": f"oracle/field_oracle.c (OpenMP) on {info['grid'][0]}x{info['grid'][1]}"
                          f" columns x {info['grid'][2]} levels x {info['fields']} fields, "
                          f"{info['steps']} steps, {info['seconds']:.1f} s"}

@@ -211,3 +211,17 @@ int64_t oracle_trips(int nx, int ny, int nz, const double* cbase, int shift, int
     }
   return s;
 }
+
+/* thread count of the OpenMP loops (torchrun exports OMP_NUM_THREADS=1) */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+int oracle_set_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
+}

@@ -29,6 +29,8 @@ def lib():
         l.oracle_run.argtypes = [I, I, I, I, I, D, C.POINTER(C.c_int), I, D, D, D]
         l.oracle_trips.argtypes = [I, I, I, D, I, I, I, I, I]
         l.oracle_trips.restype = C.c_int64
+        l.oracle_set_threads.argtypes = [I]
+        l.oracle_set_threads.restype = I
         for f in (l.oracle_init, l.oracle_jacobi, l.oracle_physics, l.oracle_step, l.oracle_run):
             f.restype = None
         _lib = l
@@ -65,3 +67,9 @@ def trips(cbase, nz, shift, x0, x1, y0, y1):
     ny, nx = cbase.shape
     cb = np.ascontiguousarray(cbase, dtype=np.float64)
     return int(lib().oracle_trips(nx, ny, nz, _d(cb), int(shift), x0, x1, y0, y1))
+
+
+def set_threads(n: int) -> int:
+    """Use n OpenMP threads (all host cores for the CPU baseline); returns the
+    effective count."""
+    return int(lib().oracle_set_threads(int(n)))
