@@ -141,6 +141,9 @@ def timelines():
         eps = []
         for i, e in enumerate(doc["epochs"]):
             eps.append({"epoch": e["epoch"], "vp_loads": [float(x).hex() for x in e["vp_loads"]],
+                        "step_times": [float(x).hex() for x in e["step_times"]],
+                        "step_time_sum": float(e["step_time_sum"]).hex(),
+                        "migration_cost": float(e["migration_cost"]).hex(),
                         "proc_loads": [float(x).hex() for x in e["proc_loads"]],
                         "strategy": e["plan"]["strategy"], "moves": doc["moves"][i],
                         "mapping": doc["mappings"][i],
