@@ -738,8 +738,10 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   const int wv = FULL ? TXC : min(TXC, w - tile.tx0);
   const int hv = FULL ? TY : min(TY, h - tile.ty0);
   const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
-  const int pair = max(0, min(2, wv - 2 * lx));  // cells of this thread's pair inside the chunk
-  const int ncell = ly < hv ? pair : 0;
+  // cells of this thread's pair inside the chunk (compile-time 2 for full tiles:
+  // the compiler cannot know threadIdx < blockDim)
+  const int pair = FULL ? 2 : max(0, min(2, wv - 2 * lx));
+  const int ncell = FULL ? 2 : (ly < hv ? pair : 0);
   const int64_t own = int64_t(y) * pitch + x;
 
   const double* pc = c.in + own;
