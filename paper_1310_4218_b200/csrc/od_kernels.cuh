@@ -49,6 +49,8 @@ struct TileDev {
 struct PackJob {
   int32_t slot, side, len, lenp;  // side: which edge of the source chunk; lenp: row stride
   int64_t dst;                   // element offset into the send buffer
+  int32_t peer, pad;             // destination rank
+  int64_t rdst;                  // element offset in the peer's receive buffer half
 };
 
 __device__ __forceinline__ uint64_t dmix64(uint64_t x) {
@@ -1328,6 +1330,73 @@ __global__ void pack_faces(const ChunkDev* __restrict__ chunks, const PackJob* _
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const int64_t k = i / j.len, e = i - k * j.len;
     out[k * j.lenp + e] = base[off + k * c.kstride + e * es];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Halo exchange over NVLink peer memory: the pack kernel stores the boundary
+// strips straight into the receive buffers of the neighbouring GPUs (CUDA IPC
+// mappings), then the last CTA publishes the step number in each receiver's
+// flag array (release, system scope).  The receiver's wait_halo acquires the
+// flags before its step kernel reads the strips.  Receive buffers are double
+// buffered by step parity; faces are symmetric between ranks, so a rank can
+// only reach step t+2 after its neighbours finished reading step t.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
+                               const PackJob* __restrict__ jobs, double* const* __restrict__ peer_base,
+                               int64_t half_elems, int32_t par, int32_t nz,
+                               unsigned int* __restrict__ counter,
+                               unsigned long long* const* __restrict__ peer_flags,
+                               const int32_t* __restrict__ notify, int32_t n_notify,
+                               int32_t my_rank, unsigned long long value) {
+  const PackJob j = jobs[blockIdx.x];
+  const ChunkDev& c = chunks[j.slot];
+  const int f = blockIdx.y;
+  const double* base = c.in + f * c.fstride;
+  int64_t off = 0, es = 1;
+  switch (j.side) {
+    case kLeft: off = 0; es = c.pitch; break;
+    case kRight: off = c.w - 1; es = c.pitch; break;
+    case kTop: off = 0; es = 1; break;
+    default: off = int64_t(c.h - 1) * c.pitch; es = 1; break;
+  }
+  double* out = peer_base[j.peer] + int64_t(par) * half_elems + j.rdst + int64_t(f) * nz * j.lenp;
+  const int64_t n = int64_t(nz) * j.len;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const int64_t k = i / j.len, e = i - k * j.len;
+    out[k * j.lenp + e] = base[off + k * c.kstride + e * es];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(counter, 1u) == total - 1) {
+      __threadfence_system();
+      for (int i = 0; i < n_notify; ++i) st_release_sys(peer_flags[notify[i]] + my_rank, value);
+      *counter = 0u;  // next step's count (stream ordered)
+    }
+  }
+}
+
+__global__ void wait_halo(const unsigned long long* __restrict__ flags,
+                          const int32_t* __restrict__ senders, int32_t n,
+                          unsigned long long value, unsigned long long timeout_ns) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const unsigned long long* f = flags + senders[i];
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(f) < value) {
+      if (globaltimer_ns() - t0 > timeout_ns) __trap();  // a peer died: fail loudly
+      __nanosleep(64);
+    }
   }
 }
 

@@ -195,6 +195,20 @@ class Runtime {
   std::vector<int64_t> send_off_, send_cnt_, recv_off_, recv_cnt_;  // per peer, elements
   double* d_send_ = nullptr;
   double* d_recv_ = nullptr;
+  // NVLink peer-memory halo exchange (CUDA IPC), default for world > 1
+  bool p2p_ = false;
+  int64_t recv_half_ = 0;  // elements per parity half of d_recv_ (p2p)
+  unsigned long long* d_flags_ = nullptr;  // [world] step published by each sender
+  std::vector<double*> peer_recv_;
+  std::vector<unsigned long long*> peer_flags_;
+  double** d_peer_base_ = nullptr;
+  unsigned long long** d_peer_flags_ = nullptr;
+  unsigned int* d_pack_counter_ = nullptr;
+  int32_t* d_notify_ = nullptr;   // ranks this rank sends to
+  int32_t* d_senders_ = nullptr;  // ranks that send to this rank
+  int32_t n_notify_ = 0, n_senders_ = 0;
+  void alloc_comm_buffers();
+  void setup_p2p();
   size_t send_cap_ = 0, recv_cap_ = 0;
   std::vector<std::array<int64_t, 4>> recv_face_off_;  // per slot
   // measurement
@@ -326,6 +340,12 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   set_shift(0);
 
   init_slab();
+  if (world_ > 1) {
+    const char* hm = std::getenv("OD_HALO");
+    p2p_ = !(hm && std::string(hm) == "nccl");
+    alloc_comm_buffers();
+    if (p2p_) setup_p2p();
+  }
   chunks_.resize(K());
   for (int32_t v = 0; v < K(); ++v) {
     if (rank_of_vp(v) != rank_) continue;
@@ -371,6 +391,17 @@ Runtime::~Runtime() {
   cudaFree(d_ns_);
   cudaFree(d_trips_);
   cudaFree(d_gather_);
+  for (int q = 0; q < int(peer_recv_.size()); ++q) {
+    if (q == rank_) continue;
+    if (peer_recv_[q]) cudaIpcCloseMemHandle(peer_recv_[q]);
+    if (peer_flags_[q]) cudaIpcCloseMemHandle(peer_flags_[q]);
+  }
+  cudaFree(d_flags_);
+  cudaFree(d_peer_base_);
+  cudaFree(d_peer_flags_);
+  cudaFree(d_pack_counter_);
+  cudaFree(d_notify_);
+  cudaFree(d_senders_);
   if (comm_) odb::nccl().CommDestroy(comm_);
   cudaFree(d_counter_);
   if (s1_) cudaStreamDestroy(s1_);
@@ -611,8 +642,26 @@ void Runtime::rebuild_tables() {
   exchange_schedule(subs_, cfg_.decomposition_kind, cfg_.kx, cfg_.ky, rank_of, world_, rank_,
                     per_cell, sends, recvs);
   int64_t soff = 0, roff = 0;
+  // receive-side offsets of this rank's strips on each peer (the peer's own
+  // schedule, computed here from the same global mapping)
+  std::vector<std::vector<int64_t>> remote_off(world_);
+  if (p2p_) {
+    std::vector<bool> need(world_, false);
+    for (const FaceXfer& f : sends) need[f.peer] = true;
+    for (int q = 0; q < world_; ++q) {
+      if (!need[q]) continue;
+      std::vector<FaceXfer> qs, qr;
+      exchange_schedule(subs_, cfg_.decomposition_kind, cfg_.kx, cfg_.ky, rank_of, world_, q,
+                        per_cell, qs, qr);
+      for (const FaceXfer& f : qr)
+        if (f.peer == rank_) remote_off[q].push_back(f.offset);
+    }
+  }
+  std::vector<size_t> taken(world_, 0);
   for (const FaceXfer& f : sends) {
-    jobs_.push_back(PackJob{slot_of[f.vp], f.side, f.len, f.lenp, f.offset});
+    PackJob pj{slot_of[f.vp], f.side, f.len, f.lenp, f.offset, f.peer, 0, 0};
+    if (p2p_) pj.rdst = remote_off[f.peer].at(taken[f.peer]++);
+    jobs_.push_back(pj);
     send_cnt_[f.peer] += per_cell * f.lenp;
     soff = f.offset + per_cell * f.lenp;
   }
@@ -628,15 +677,16 @@ void Runtime::rebuild_tables() {
     so += send_cnt_[q];
     ro += recv_cnt_[q];
   }
-  if (world_ > 1 && send_cap_ == 0) {
-    // worst case for this rank: every face of every chunk slot remote
-    size_t per = 0;
-    for (const Sub& sb : subs_)
-      per = std::max<size_t>(per, size_t(2 * (((sb.w() + 1) & ~1) + ((sb.h() + 1) & ~1))));
-    const size_t slots = std::max<size_t>(slab_slots_, resident_.size());
-    send_cap_ = recv_cap_ = per * size_t(per_cell) * slots;
-    OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
-    OD_CU(cudaMalloc(&d_recv_, recv_cap_ * sizeof(double)));
+  if (p2p_) {
+    std::vector<int32_t> notify, senders;
+    for (int q = 0; q < world_; ++q) {
+      if (send_cnt_[q] > 0) notify.push_back(q);
+      if (recv_cnt_[q] > 0) senders.push_back(q);
+    }
+    n_notify_ = int32_t(notify.size());
+    n_senders_ = int32_t(senders.size());
+    if (n_notify_) OD_CU(cudaMemcpy(d_notify_, notify.data(), notify.size() * 4, cudaMemcpyHostToDevice));
+    if (n_senders_) OD_CU(cudaMemcpy(d_senders_, senders.data(), senders.size() * 4, cudaMemcpyHostToDevice));
   }
   if (size_t(soff) > send_cap_) {
     cudaFree(d_send_);
@@ -645,6 +695,7 @@ void Runtime::rebuild_tables() {
     OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
   }
   if (size_t(roff) > recv_cap_) {
+    if (p2p_) throw RuntimeFault("halo receive buffer exceeded its preallocated capacity");
     cudaFree(d_recv_);
     d_recv_ = nullptr;
     recv_cap_ = std::max(size_t(roff) * 3 / 2, recv_cap_ * 2);
@@ -679,7 +730,7 @@ void Runtime::rebuild_tables() {
           c.face[d] = edge_of(chunks_[n], opposite(d), par);
         } else {
           const int32_t len = (d == kLeft || d == kRight) ? c.h : c.w;
-          c.face[d].p = d_recv_ + recv_face_off_[i][d];
+          c.face[d].p = d_recv_ + par * recv_half_ + recv_face_off_[i][d];
           const int32_t lenp = (len + 1) & ~1;
           c.face[d].fs = int64_t(cfg_.nz) * lenp;
           c.face[d].ks = lenp;
@@ -701,6 +752,64 @@ void Runtime::rebuild_tables() {
   if (trace_on())
     fprintf(stderr, "[od rank %d] rebuild: tiles %.2f ms, exchange %.2f ms, chunk tables %.2f ms\n",
             rank_, (r1 - r0) * 1e3, (r2 - r1) * 1e3, (now_s() - r2) * 1e3);
+}
+
+// Worst case for this rank: every face of every chunk slot borders another GPU.
+void Runtime::alloc_comm_buffers() {
+  size_t per = 0;
+  for (const Sub& sb : subs_)
+    per = std::max<size_t>(per, size_t(2 * (((sb.w() + 1) & ~1) + ((sb.h() + 1) & ~1))));
+  size_t resident = 0;
+  for (int32_t v = 0; v < K(); ++v) resident += rank_of_vp(v) == rank_;
+  const size_t slots = std::max<size_t>(slab_slots_, resident);
+  send_cap_ = recv_cap_ = per * size_t(cfg_.nz) * cfg_.fields * slots;
+  OD_CU(cudaMalloc(&d_send_, send_cap_ * sizeof(double)));
+  recv_half_ = p2p_ ? int64_t(recv_cap_) : 0;
+  OD_CU(cudaMalloc(&d_recv_, (p2p_ ? 2 : 1) * recv_cap_ * sizeof(double)));
+}
+
+// Map every peer's receive buffer and flag array into this process (CUDA IPC;
+// handles all-gathered over the NCCL communicator).
+void Runtime::setup_p2p() {
+  OD_CU(cudaMalloc(&d_flags_, sizeof(unsigned long long) * world_));
+  OD_CU(cudaMemset(d_flags_, 0, sizeof(unsigned long long) * world_));
+  OD_CU(cudaMalloc(&d_pack_counter_, sizeof(unsigned int)));
+  OD_CU(cudaMemset(d_pack_counter_, 0, sizeof(unsigned int)));
+  cudaIpcMemHandle_t mine[2];
+  OD_CU(cudaIpcGetMemHandle(&mine[0], d_recv_));
+  OD_CU(cudaIpcGetMemHandle(&mine[1], d_flags_));
+  const size_t hb = sizeof(mine);
+  uint8_t* d_h = nullptr;
+  OD_CU(cudaMalloc(&d_h, hb * (world_ + 1)));
+  OD_CU(cudaMemcpy(d_h, mine, hb, cudaMemcpyHostToDevice));
+  OD_CU(cudaDeviceSynchronize());
+  OD_NC(odb::nccl().AllGather(d_h, d_h + hb, hb, ncclUint8, comm_, s0_));
+  std::vector<cudaIpcMemHandle_t> all(2 * world_);
+  OD_CU(cudaMemcpyAsync(all.data(), d_h + hb, hb * world_, cudaMemcpyDeviceToHost, s0_));
+  OD_CU(cudaStreamSynchronize(s0_));
+  cudaFree(d_h);
+  peer_recv_.assign(world_, nullptr);
+  peer_flags_.assign(world_, nullptr);
+  for (int q = 0; q < world_; ++q) {
+    if (q == rank_) {
+      peer_recv_[q] = d_recv_;
+      peer_flags_[q] = d_flags_;
+      continue;
+    }
+    void* p = nullptr;
+    OD_CU(cudaIpcOpenMemHandle(&p, all[2 * q], cudaIpcMemLazyEnablePeerAccess));
+    peer_recv_[q] = static_cast<double*>(p);
+    OD_CU(cudaIpcOpenMemHandle(&p, all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    peer_flags_[q] = static_cast<unsigned long long*>(p);
+  }
+  OD_CU(cudaMalloc(&d_peer_base_, sizeof(double*) * world_));
+  OD_CU(cudaMemcpy(d_peer_base_, peer_recv_.data(), sizeof(double*) * world_,
+                   cudaMemcpyHostToDevice));
+  OD_CU(cudaMalloc(&d_peer_flags_, sizeof(unsigned long long*) * world_));
+  OD_CU(cudaMemcpy(d_peer_flags_, peer_flags_.data(), sizeof(unsigned long long*) * world_,
+                   cudaMemcpyHostToDevice));
+  OD_CU(cudaMalloc(&d_notify_, sizeof(int32_t) * world_));
+  OD_CU(cudaMalloc(&d_senders_, sizeof(int32_t) * world_));
 }
 
 // ------------------------------------------------------------------- steps --
@@ -769,9 +878,42 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     OD_CU(cudaMemsetAsync(ns, 0, size_t(ns_cols_) * sizeof(unsigned long long), s0_));
   }
 
-  // boundaries of chunks that border another GPU: pack, then exchange
-  if (!jobs_.empty() || (world_ > 1 && std::any_of(recv_cnt_.begin(), recv_cnt_.end(),
-                                                   [](int64_t c) { return c > 0; }))) {
+  // boundaries of chunks that border another GPU
+  if (p2p_ && (!jobs_.empty() || n_senders_ > 0)) {
+    // pack straight into the neighbours' receive buffers over NVLink, publish
+    // the step, then wait for the neighbours' strips of this step
+    int e0 = -1, e1 = -1, e2 = -1;
+    if (profiling_) {
+      e0 = new_event();
+      OD_CU(cudaEventRecord(events_[e0], s0_));
+    }
+    const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
+    if (!jobs_.empty()) {
+      pack_faces_p2p<<<dim3(unsigned(jobs_.size()), unsigned(cfg_.fields)), 256, 0, s0_>>>(
+          d_chunks_[par], d_jobs_, d_peer_base_, recv_half_, par, cfg_.nz, d_pack_counter_,
+          d_peer_flags_, d_notify_, n_notify_, rank_, stamp);
+      OD_CU(cudaGetLastError());
+      ++st_.kernel_launches;
+      for (int q = 0; q < world_; ++q) st_.halo_bytes_sent += send_cnt_[q] * int64_t(sizeof(double));
+    }
+    if (profiling_) {
+      e1 = new_event();
+      OD_CU(cudaEventRecord(events_[e1], s0_));
+    }
+    if (n_senders_ > 0) {
+      wait_halo<<<1, 32, 0, s0_>>>(d_flags_, d_senders_, n_senders_, stamp,
+                                   20ull * 1000 * 1000 * 1000);
+      OD_CU(cudaGetLastError());
+      ++st_.kernel_launches;
+    }
+    if (profiling_) {
+      e2 = new_event();
+      OD_CU(cudaEventRecord(events_[e2], s0_));
+      prof_pack_.push_back({e0, e1});
+      prof_x_.push_back({e1, e2});
+    }
+  } else if (!jobs_.empty() || (world_ > 1 && std::any_of(recv_cnt_.begin(), recv_cnt_.end(),
+                                                          [](int64_t c) { return c > 0; }))) {
     int e0 = -1, e1 = -1, e2 = -1;
     if (profiling_) {
       e0 = new_event();
