@@ -187,8 +187,9 @@ typedef struct od_config {
   /* B200 path parameters (no reference counterpart) */
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
   int32_t measure;      /* OD_MEASURE_EVENTS | OD_MEASURE_TIMER */
-  int32_t overlap;      /* kernel mode: 0 Jacobi then physics (two launches),
-                           1 the two kernels on two streams, 2 fused column_step */
+  int32_t overlap;      /* kernel mode: 0 jacobi_step + physics_step, 4 fused
+                           column_step3, 5 persistent fused (default), 6 persistent
+                           fused, four columns per thread */
   int32_t reserved_[5];
 } od_config;
 

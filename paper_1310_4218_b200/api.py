@@ -574,8 +574,9 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     seed: int = 1
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
-    # kernel mode: 0 Jacobi then physics, 1 two streams, 2 fused (1 column/thread),
-    # 3 fused pair kernel, 4 fused pair kernel v2, 5 persistent fused (default)
+    # kernel mode: 0 jacobi_step then physics_step (two launches), 4 fused
+    # column_step3 (one CTA per 64x8 tile), 5 persistent fused, heaviest tiles
+    # first (default), 6 persistent fused with four columns per thread
     overlap: int = 5
 
     def vp_count(self) -> int:

@@ -264,34 +264,6 @@ __global__ void __launch_bounds__(TX* TY)
   }
 }
 
-// Persistent physics: a few CTAs per SM pull tiles from a counter so the
-// kernel co-resides with jacobi_step (launched on another stream) instead of
-// occupying every SM slot: the FP64 pipe runs the recurrences while the
-// Jacobi streams HBM.
-template <int TX, int TY, bool TIMED>
-__global__ void __launch_bounds__(TX* TY)
-    physics_persistent(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                       int32_t ntiles, unsigned int* __restrict__ counter,
-                       const double* __restrict__ cfield, int32_t nx, int32_t ny, int32_t shift,
-                       int32_t nz, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
-  __shared__ int s_tile;
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-  for (;;) {
-    if (lead) s_tile = int(atomicAdd(counter, 1u));
-    __syncthreads();
-    const int ti = s_tile;
-    if (ti >= ntiles) break;
-    uint64_t t_start = 0;
-    if (TIMED && lead) t_start = globaltimer_ns();
-    const TileDev tile = tiles[ti];
-    physics_column(chunks[tile.slot], tile, threadIdx.x, threadIdx.y, cfield, nx, ny, shift, nz,
-                   n_inner);
-    __syncthreads();  // tile done (and s_tile consumed) before the next claim
-    if (TIMED && lead)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Fused step.  On B200 a kernel that saturates the FP64 pipe starves every
 // co-resident warp that needs that pipe (tools/overlap_probe.cu: a copy with 7
@@ -382,326 +354,6 @@ __device__ __forceinline__ void physics_advance(ColumnState& s, int budget) {
       ++s.t;
       s.i = 0;
     }
-  }
-}
-
-// Running pointer over the (field, level) planes of one column: +ks inside a
-// field, +(fs - (nz-1) ks) from the last level of a field to the next field.
-struct PlaneWalker {
-  const double* p;
-  int64_t step, wrap;
-  __device__ __forceinline__ void next(bool last_level) { p += last_level ? wrap : step; }
-};
-
-template <int TX, int TY, int S, bool TIMED>
-__global__ void __launch_bounds__(TX* TY, 4)
-    column_step(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
-  constexpr int R = 8;  // ring slots (power of two); S + 2 <= R
-  constexpr int PW = TX + 2;
-  constexpr int PLANE = (TY + 2) * PW;
-  static_assert(S + 2 <= R, "prefetch depth too large for the ring");
-  __shared__ __align__(16) double ring[R * PLANE];
-
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
-
-  const TileDev tile = tiles[blockIdx.x];
-  const ChunkDev& c = chunks[tile.slot];
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int w = c.w, h = c.h, pitch = c.pitch;
-  const int64_t ks = c.kstride, fs = c.fstride;
-  const int wv = min(TX, w - tile.tx0), hv = min(TY, h - tile.ty0);
-  const int x = tile.tx0 + lx, y = tile.ty0 + ly;
-  const bool act = lx < wv && ly < hv;
-  const int64_t own = int64_t(y) * pitch + x;
-  const int64_t wrap = fs - int64_t(nz - 1) * ks;
-
-  // global sources (running pointers) and smem destinations of this thread
-  const double* pc = c.in + own;
-  const double* px = nullptr;
-  const double* py = nullptr;
-  int64_t xstep = 0, xwrap = 0, ystep = 0, ywrap = 0;
-  int ox = 0, oy = 0;
-  if (ly < hv && (lx == 0 || lx == TX - 1)) {
-    const bool left = lx == 0;
-    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
-    ox = (ly + 1) * PW + (left ? 0 : wv + 1);
-    if (xs >= 0 && xs < w) {
-      px = c.in + int64_t(y) * pitch + xs;
-      xstep = ks;
-      xwrap = wrap;
-    } else {
-      const FaceDev& fd = c.face[left ? kLeft : kRight];
-      px = fd.p + int64_t(y) * fd.es;
-      xstep = fd.ks;
-      xwrap = fd.fs - int64_t(nz - 1) * fd.ks;
-    }
-  }
-  if (lx < wv && (ly == 0 || ly == TY - 1)) {
-    const bool top = ly == 0;
-    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
-    oy = (top ? 0 : hv + 1) * PW + lx + 1;
-    if (ys >= 0 && ys < h) {
-      py = c.in + int64_t(ys) * pitch + x;
-      ystep = ks;
-      ywrap = wrap;
-    } else {
-      const FaceDev& fd = c.face[top ? kTop : kBottom];
-      py = fd.p + int64_t(x) * fd.es;
-      ystep = fd.ks;
-      ywrap = fd.fs - int64_t(nz - 1) * fd.ks;
-    }
-  }
-  const int oc = (ly + 1) * PW + lx + 1;
-
-  const int levels = F * nz;
-  int ki = 0;  // level (within its field) of the next plane to issue
-  auto issue = [&](int L) {
-    if (L < levels) {
-      double* slot = ring + (L & (R - 1)) * PLANE;
-      if (act) cp_async8(slot + oc, pc);
-      if (px) cp_async8(slot + ox, px);
-      if (py) cp_async8(slot + oy, py);
-      const bool last = ki == nz - 1;
-      pc += last ? wrap : ks;
-      px += last ? xwrap : xstep;
-      py += last ? ywrap : ystep;
-      ki = last ? 0 : ki + 1;
-    }
-    cp_async_commit();
-  };
-
-  ColumnState st;
-  int quota = 0;
-  if (act) {
-    physics_init(st, c, x, y, cfield, nx, ny, shift, nz, n_inner);
-    const int64_t units = int64_t(st.T) * (n_inner + 1);
-    quota = int((units + levels - 1) / levels);
-    quota = (quota + 7) & ~7;
-  }
-
-#pragma unroll
-  for (int L = 0; L < S; ++L) issue(L);
-
-  double* pout = c.out + own;
-  const double* rc = ring + oc;
-  double zm = 0.0;
-  int k = 0;
-  for (int L = 0; L < levels; ++L) {
-    cp_async_wait<S - 2>();
-    __syncthreads();
-    issue(L + S);
-    const bool last = k == nz - 1;
-    if (act) {
-      const double* pl = rc + (L & (R - 1)) * PLANE;
-      const double uc = pl[0];
-      const double xm = pl[-1];
-      const double xp = pl[1];
-      const double ym = pl[-PW];
-      const double yp = pl[PW];
-      const double zd = k > 0 ? zm : uc;
-      const double zu = last ? uc : rc[((L + 1) & (R - 1)) * PLANE];
-      const double sum =
-          __dadd_rn(__dadd_rn(__dadd_rn(xm, xp), __dadd_rn(ym, yp)), __dadd_rn(zd, zu));
-      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
-      zm = uc;
-      physics_advance(st, quota);
-    }
-    pout += last ? wrap : ks;
-    k = last ? 0 : k + 1;
-  }
-  cp_async_wait<0>();
-  if (act) physics_advance(st, 0x7fffffff);
-
-  if (TIMED) {
-    __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
-  }
-}
-
-// Two chains side by side in the common case (both inside a trip with the
-// same budget): independent DFMA chains give the FP64 pipe ILP 2 per thread.
-__device__ __forceinline__ void physics_advance2(ColumnState& s0, int b0, ColumnState& s1,
-                                                 int b1) {
-  if (b0 == b1 && s0.i > 0 && s1.i > 0 && s0.i + b0 <= s0.n_inner && s1.i + b1 <= s1.n_inner) {
-    double y0 = s0.y, y1 = s1.y;
-    const double e0 = s0.eb, e1 = s1.eb;
-    for (int j = 0; j < b0; j += 8) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double u0 = __fma_rn(-y0, y0, y0);
-        const double u1 = __fma_rn(-y1, y1, y1);
-        y0 = __fma_rn(kR, u0, e0);
-        y1 = __fma_rn(kR, u1, e1);
-      }
-    }
-    s0.y = y0;
-    s1.y = y1;
-    s0.i += b0;
-    s1.i += b1;
-    return;
-  }
-  physics_advance(s0, b0);
-  physics_advance(s1, b1);
-}
-
-// Fused step with two adjacent columns per thread: tile 64 x TY columns, 16-byte
-// plane loads and stores, two physics chains per thread.  Same arithmetic as
-// column_step / jacobi_step + physics_step.
-template <int TY, int S, bool TIMED, int MINB = 3>
-__global__ void __launch_bounds__(32 * TY, MINB)
-    column_step2(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
-  constexpr int R = 8;
-  constexpr int TXC = 64;
-  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
-  constexpr int PLANE = (TY + 2) * PW;
-  static_assert(S + 2 <= R, "prefetch depth too large for the ring");
-  __shared__ __align__(16) double ring[R * PLANE];
-
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
-
-  const TileDev tile = tiles[blockIdx.x];
-  const ChunkDev& c = chunks[tile.slot];
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int w = c.w, h = c.h, pitch = c.pitch;
-  const int64_t ks = c.kstride, fs = c.fstride;
-  const int wv = min(TXC, w - tile.tx0), hv = min(TY, h - tile.ty0);
-  const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
-  const int ncell = ly < hv ? max(0, min(2, wv - 2 * lx)) : 0;  // active cells of the pair
-  const int64_t own = int64_t(y) * pitch + x;
-  const int64_t wrap = fs - int64_t(nz - 1) * ks;
-
-  const double* pc = c.in + own;
-  const double* px = nullptr;
-  const double* py = nullptr;
-  int64_t xstep = 0, xwrap = 0, ystep = 0, ywrap = 0;
-  int ox = 0, oy = 0, ny_cells = 0;
-  if (ly < hv && (lx == 0 || lx == 31)) {
-    const bool left = lx == 0;
-    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
-    ox = (ly + 1) * PW + (left ? 1 : wv + 2);
-    if (xs >= 0 && xs < w) {
-      px = c.in + int64_t(y) * pitch + xs;
-      xstep = ks;
-      xwrap = wrap;
-    } else {
-      const FaceDev& fd = c.face[left ? kLeft : kRight];
-      px = fd.p + int64_t(y) * fd.es;
-      xstep = fd.ks;
-      xwrap = fd.fs - int64_t(nz - 1) * fd.ks;
-    }
-  }
-  const int ycells = max(0, min(2, wv - 2 * lx));
-  if (ycells > 0 && (ly == 0 || ly == TY - 1)) {
-    const bool top = ly == 0;
-    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
-    oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
-    ny_cells = ycells;
-    if (ys >= 0 && ys < h) {
-      py = c.in + int64_t(ys) * pitch + x;
-      ystep = ks;
-      ywrap = wrap;
-    } else {
-      const FaceDev& fd = c.face[top ? kTop : kBottom];
-      py = fd.p + int64_t(x) * fd.es;
-      ystep = fd.ks;
-      ywrap = fd.fs - int64_t(nz - 1) * fd.ks;
-    }
-  }
-  const int oc = (ly + 1) * PW + 2 + 2 * lx;
-
-  const int levels = F * nz;
-  int ki = 0;
-  auto issue = [&](int L) {
-    if (L < levels) {
-      double* slot = ring + (L & (R - 1)) * PLANE;
-      if (ncell == 2) cp_async16(slot + oc, pc);
-      else if (ncell == 1) cp_async8(slot + oc, pc);
-      if (px) cp_async8(slot + ox, px);
-      if (ny_cells == 2) cp_async16(slot + oy, py);
-      else if (ny_cells == 1) cp_async8(slot + oy, py);
-      const bool last = ki == nz - 1;
-      pc += last ? wrap : ks;
-      px += last ? xwrap : xstep;
-      py += last ? ywrap : ystep;
-      ki = last ? 0 : ki + 1;
-    }
-    cp_async_commit();
-  };
-
-  ColumnState s0, s1;
-  int q0 = 0, q1 = 0;
-  if (ncell >= 1) {
-    physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
-    q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
-    q0 = (q0 + 7) & ~7;
-  }
-  if (ncell == 2) {
-    physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
-    q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
-    q1 = (q1 + 7) & ~7;
-  }
-
-#pragma unroll
-  for (int L = 0; L < S; ++L) issue(L);
-
-  double* pout = c.out + own;
-  const double* rc = ring + oc;
-  double zm0 = 0.0, zm1 = 0.0;
-  int k = 0;
-  for (int L = 0; L < levels; ++L) {
-    cp_async_wait<S - 2>();
-    __syncthreads();
-    issue(L + S);
-    const bool last = k == nz - 1;
-    if (ncell == 2) {
-      const double* pl = rc + (L & (R - 1)) * PLANE;
-      const double2 uc = *reinterpret_cast<const double2*>(pl);
-      const double xl = pl[-1], xr = pl[2];
-      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
-      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
-      double2 zu = uc;
-      if (!last) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
-      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
-      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
-                                  __dadd_rn(zd0, zu.x));
-      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
-                                  __dadd_rn(zd1, zu.y));
-      double2 o;
-      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
-      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
-      __stcs(reinterpret_cast<double2*>(pout), o);
-      zm0 = uc.x;
-      zm1 = uc.y;
-      physics_advance2(s0, q0, s1, q1);
-    } else if (ncell == 1) {
-      const double* pl = rc + (L & (R - 1)) * PLANE;
-      const double uc = pl[0];
-      const double zu = last ? uc : rc[((L + 1) & (R - 1)) * PLANE];
-      const double zd = k > 0 ? zm0 : uc;
-      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
-                                   __dadd_rn(zd, zu));
-      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
-      zm0 = uc;
-      physics_advance(s0, q0);
-    }
-    pout += last ? wrap : ks;
-    k = last ? 0 : k + 1;
-  }
-  cp_async_wait<0>();
-  if (ncell >= 1) physics_advance(s0, 0x7fffffff);
-  if (ncell == 2) physics_advance(s1, 0x7fffffff);
-
-  if (TIMED) {
-    __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
   }
 }
 

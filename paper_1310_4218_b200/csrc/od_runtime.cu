@@ -147,7 +147,6 @@ class Runtime {
   int32_t cur_epoch_ = 1, cur_step_ = 0;
 
   cudaStream_t s0_ = nullptr;
-  cudaStream_t s1_ = nullptr;       // physics stream (overlap), higher priority
   unsigned int* d_counter_ = nullptr;
   int phys_ctas_ = 0;               // persistent physics grid
   ncclComm_t comm_ = nullptr;
@@ -165,7 +164,7 @@ class Runtime {
   std::vector<int32_t> resident_;  // slot -> vp
   std::vector<int32_t> tile_begin_, tile_count_;
   int32_t ntiles_ = 0;
-  // 64-column tiles of the pair kernel (column_step2)
+  // 64 x 8 tiles of the one-CTA-per-tile fused kernel (column_step3, mode 4)
   std::vector<int32_t> tile2_begin_, tile2_count_;
   int32_t ntiles2_ = 0;
   TileDev* d_tiles2_ = nullptr;
@@ -257,7 +256,8 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       cfg.later_call_strategy < 0 || cfg.later_call_strategy > 1)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
-  if (cfg.overlap < 0 || cfg.overlap > 6) throw ValidationError("unknown kernel mode (overlap)");
+  if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 6))
+    throw ValidationError("unknown kernel mode (overlap): 0, 4, 5 or 6");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER &&
       cfg.measure != OD_MEASURE_TIMER_RAW)
     throw ValidationError("unknown measurement mode");
@@ -278,9 +278,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
   {
-    int lo = 0, hi = 0, sms = 0;
-    OD_CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    OD_CU(cudaStreamCreateWithPriority(&s1_, cudaStreamNonBlocking, hi));
+    int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
     phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
@@ -295,8 +293,6 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     };
     set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, true>));
     set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, false>));
-    set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, true>));
-    set_carve(reinterpret_cast<const void*>(&physics_persistent<kTX, kTY, false>));
     int per_sm = 0;
     const char* pm = std::getenv("OD_PERSIST_MINB");
     persist_minb_ = pm ? std::atoi(pm) : 5;
@@ -363,7 +359,6 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
 Runtime::~Runtime() {
   cudaSetDevice(device_);
   if (s0_) cudaStreamSynchronize(s0_);
-  if (s1_) cudaStreamSynchronize(s1_);
   for (auto& m : chunks_)
     if (m.base && !(slab_ && m.base >= slab_ &&
                     m.base < slab_ + slab_slots_ * (slot_bytes_ / sizeof(double))))
@@ -404,7 +399,6 @@ Runtime::~Runtime() {
   cudaFree(d_senders_);
   if (comm_) odb::nccl().CommDestroy(comm_);
   cudaFree(d_counter_);
-  if (s1_) cudaStreamDestroy(s1_);
   if (s0_) cudaStreamDestroy(s0_);
 }
 
@@ -952,33 +946,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     r.kev0 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev0], s0_));
   }
-  if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 3) {
-    int e0 = -1, e1 = -1;
-    if (profiling_) {
-      e0 = new_event();
-      OD_CU(cudaEventRecord(events_[e0], s0_));
-    }
-    static const int variant = std::getenv("OD_FUSED_MINB") ? std::atoi(std::getenv("OD_FUSED_MINB")) : 3;
-#define OD_LAUNCH_CS2(MB)                                                                  \
-  if (timer)                                                                              \
-    column_step2<kTY, kFusedPrefetch, true, MB><<<ntiles2_, blk, 0, s0_>>>(               \
-        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
-        cfg_.n_inner, ns);                                                                \
-  else                                                                                    \
-    column_step2<kTY, kFusedPrefetch, false, MB><<<ntiles2_, blk, 0, s0_>>>(              \
-        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
-        cfg_.n_inner, nullptr);
-    if (variant == 2) { OD_LAUNCH_CS2(2) } else if (variant == 4) { OD_LAUNCH_CS2(4) } else { OD_LAUNCH_CS2(3) }
-#undef OD_LAUNCH_CS2
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
-      e1 = new_event();
-      OD_CU(cudaEventRecord(events_[e1], s0_));
-      prof_f_.push_back({e0, e1});
-    }
-    st_.kernel_launches += 1;
-    st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6) {
+  if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
     if (profiling_) {
@@ -1061,75 +1029,6 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
     st_.kernel_launches += 1;
     st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap == 2) {
-    // fused: Jacobi level steps and the column recurrence in the same warps
-    int e0 = -1, e1 = -1;
-    if (profiling_) {
-      e0 = new_event();
-      OD_CU(cudaEventRecord(events_[e0], s0_));
-    }
-    if (timer)
-      column_step<kTX, kTY, kFusedPrefetch, true><<<ntiles_, blk, 0, s0_>>>(
-          d_chunks_[par], d_tiles_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-          cfg_.n_inner, ns);
-    else
-      column_step<kTX, kTY, kFusedPrefetch, false><<<ntiles_, blk, 0, s0_>>>(
-          d_chunks_[par], d_tiles_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-          cfg_.n_inner, nullptr);
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
-      e1 = new_event();
-      OD_CU(cudaEventRecord(events_[e1], s0_));
-      prof_f_.push_back({e0, e1});
-    }
-    st_.kernel_launches += 1;
-    st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && ntiles_ > 0 && cfg_.overlap == 1) {
-    // physics (FP64 pipe) on s1 concurrently with the Jacobi (HBM) on s0;
-    // both read U^t only, so the fork/join per step is the only ordering
-    const int ef = new_event(), ej = new_event();
-    OD_CU(cudaEventRecord(events_[ef], s0_));
-    OD_CU(cudaStreamWaitEvent(s1_, events_[ef], 0));
-    int p0 = -1, p1 = -1, j0 = -1, j1 = -1;
-    if (profiling_) {
-      p0 = new_event();
-      OD_CU(cudaEventRecord(events_[p0], s1_));
-    }
-    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s1_));
-    const int grid = std::min(phys_ctas_, ntiles_);
-    if (timer)
-      physics_persistent<kTX, kTY, true><<<grid, blk, 0, s1_>>>(
-          d_chunks_[par], d_tiles_, ntiles_, d_counter_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
-          cfg_.n_inner, ns);
-    else
-      physics_persistent<kTX, kTY, false><<<grid, blk, 0, s1_>>>(
-          d_chunks_[par], d_tiles_, ntiles_, d_counter_, cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
-          cfg_.n_inner, nullptr);
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
-      p1 = new_event();
-      OD_CU(cudaEventRecord(events_[p1], s1_));
-      prof_p_.push_back({p0, p1});
-      j0 = new_event();
-      OD_CU(cudaEventRecord(events_[j0], s0_));
-    }
-    if (timer)
-      jacobi_step<kTX, kTY, kPrefetch, true><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
-          d_chunks_[par], d_tiles_, cfg_.nz, ns);
-    else
-      jacobi_step<kTX, kTY, kPrefetch, false><<<dim3(ntiles_, cfg_.fields), blk, 0, s0_>>>(
-          d_chunks_[par], d_tiles_, cfg_.nz, nullptr);
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
-      j1 = new_event();
-      OD_CU(cudaEventRecord(events_[j1], s0_));
-      prof_j_.push_back({j0, j1});
-    }
-    OD_CU(cudaEventRecord(events_[ej], s1_));
-    OD_CU(cudaStreamWaitEvent(s0_, events_[ej], 0));
-    st_.kernel_launches += 2;
-    st_.jacobi_launches += 1;
-    st_.physics_launches += 1;
   } else if (mode == kAsync || timer) {
     int e0 = -1, e1 = -1, e2 = -1;
     if (profiling_) {
@@ -1185,14 +1084,6 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       } else if (cfg_.overlap == 4) {
         column_step3<kTY, kFusedPrefetch, false, 3><<<tile2_count_[i], blk, 0, s0_>>>(
             d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr);
-      } else if (cfg_.overlap == 3) {
-        column_step2<kTY, kFusedPrefetch, false><<<tile2_count_[i], blk, 0, s0_>>>(
-            d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr);
-      } else if (cfg_.overlap == 2) {
-        column_step<kTX, kTY, kFusedPrefetch, false><<<tile_count_[i], blk, 0, s0_>>>(
-            d_chunks_[par], d_tiles_ + tile_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
             cfg_.ny, shift, cfg_.n_inner, nullptr);
       } else {
         jacobi_step<kTX, kTY, kPrefetch, false>

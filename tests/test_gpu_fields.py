@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 
 def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps_window=(2, 1),
           pattern=od.LoadPattern.UpperHalfHeavy, n_inner=5, adv=(0, 0, 1), threshold=1e30,
-          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0, overlap=2):
+          measure=od.MeasureMode.Timer, seed=1234, heavy=2.0, overlap=5):
     return od.ExperimentConfig(
         cluster=od.ClusterSpec(nodes, ppn), domain=od.Domain(nx, ny, nz, F),
         decomposition=od.Decomposition(kind, kx, ky), window=od.MeasurementWindow(*steps_window),
@@ -23,10 +23,8 @@ def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps
         seed=seed, n_inner=n_inner, measure=measure, overlap=overlap)
 
 
-@pytest.mark.parametrize("kx,ky,overlap", [(1, 1, 0), (4, 3, 0), (2, 5, 0), (4, 3, 1), (1, 1, 1),
-                                           (1, 1, 2), (4, 3, 2), (2, 5, 2), (1, 1, 3), (4, 3, 3),
-                                           (2, 5, 3), (1, 1, 4), (4, 3, 4), (2, 5, 4),
-                                           (1, 1, 5), (4, 3, 5), (2, 5, 5),
+@pytest.mark.parametrize("kx,ky,overlap", [(1, 1, 0), (4, 3, 0), (2, 5, 0), (1, 1, 4), (4, 3, 4),
+                                           (2, 5, 4), (1, 1, 5), (4, 3, 5), (2, 5, 5),
                                            (1, 1, 6), (4, 3, 6), (2, 5, 6)])
 def test_fields_bitwise_2d(kx, ky, overlap):
     cfg = small(kx=kx, ky=ky, overlap=overlap)
@@ -36,7 +34,7 @@ def test_fields_bitwise_2d(kx, ky, overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("overlap", [0, 4, 5, 6])
 def test_fields_bitwise_1d_strips(overlap):
     cfg = small(nx=45, ny=30, kind=ONE_D, kx=1, ky=7, overlap=overlap)
     U, A, _ = device_fields(cfg, 4)
@@ -54,8 +52,8 @@ def test_fields_multi_tile_chunks_and_advection():
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap,n_inner", [(0, 5), (2, 5), (2, 0), (2, 40), (3, 5), (3, 0),
-                                             (3, 40), (4, 5), (4, 0), (4, 40), (5, 5), (5, 0), (5, 40), (6, 5), (6, 0), (6, 40)])
+@pytest.mark.parametrize("overlap,n_inner", [(0, 5), (4, 5), (4, 0), (4, 40), (5, 5), (5, 0),
+                                             (5, 40), (6, 5), (6, 0), (6, 40)])
 def test_fields_edge_shapes(overlap, n_inner):
     # nz = 1 (no vertical neighbours, physics trips 0 or 1), single field
     cfg = small(nx=33, ny=9, nz=1, F=1, kx=3, ky=2, heavy=3.0, overlap=overlap, n_inner=n_inner)
@@ -77,7 +75,7 @@ def test_fields_invariant_under_balancing_and_procs():
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("overlap", [0, 4, 5, 6])
 def test_events_measurement_mode(overlap):
     cfg = small(nx=64, ny=32, kx=4, ky=2, measure=od.MeasureMode.Events, overlap=overlap)
     with od.Engine(cfg) as eng:
@@ -92,7 +90,7 @@ def test_events_measurement_mode(overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("mode", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("mode", [4, 5, 6])
 @pytest.mark.parametrize("n_inner,F,nz", [(0, 2, 5), (1, 3, 7), (13, 1, 4), (200, 2, 3)])
 def test_fused_quota_edge_cases(n_inner, F, nz, mode):
     # quota rounding: recurrences longer/shorter than the Jacobi level count;
