@@ -70,6 +70,30 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Spin (one thread) until every sender has published `stamp`; trap after
+// timeout_ns so a dead peer fails the step loudly instead of hanging it.
+__device__ __forceinline__ void wait_stamps(const unsigned long long* __restrict__ flags,
+                                            const int32_t* __restrict__ senders, int32_t n,
+                                            unsigned long long stamp, uint64_t timeout_ns) {
+  for (int i = 0; i < n; ++i) {
+    const unsigned long long* f = flags + senders[i];
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys(f) < stamp) {
+      if (globaltimer_ns() - t0 > timeout_ns) __trap();
+      __nanosleep(64);
+    }
+  }
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -588,10 +612,14 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                            int32_t ntiles, unsigned int* __restrict__ counter, int32_t nz,
                            int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
                            int32_t shift, int32_t n_inner,
-                           unsigned long long* __restrict__ chunk_ns) {
+                           unsigned long long* __restrict__ chunk_ns,
+                           const unsigned long long* __restrict__ halo_flags,
+                           const int32_t* __restrict__ senders, int32_t n_senders,
+                           unsigned long long stamp, unsigned long long* __restrict__ wait_ns) {
   __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
   __shared__ int s_next;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  bool halo_ready = n_senders == 0;  // meaningful in the lead thread only
   for (;;) {
     if (lead) s_next = int(atomicAdd(counter, 1u));
     __syncthreads();
@@ -600,6 +628,18 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     if (ti >= ntiles) break;
     const TileDev t = tiles[ti];
     const ChunkDev& c = chunks[t.slot];
+    if (t.pad & 1) {
+      // tile reads a strip from another GPU: those tiles come last in the
+      // queue, so the exchange has normally landed while interior tiles ran
+      if (lead && !halo_ready) {
+        const uint64_t w0 = globaltimer_ns();
+        wait_stamps(halo_flags, senders, n_senders, stamp, 20ull * 1000 * 1000 * 1000);
+        // time this SM idled for the neighbours (kept out of the load measurement)
+        if (wait_ns) atomicMax(wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+        halo_ready = true;
+      }
+      __syncthreads();
+    }
     if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
       tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
                                     chunk_ns);
@@ -945,16 +985,30 @@ __global__ void __launch_bounds__(128, MINB)
                             unsigned int* __restrict__ counter, int32_t nz, int32_t F,
                             const double* __restrict__ cfield, int32_t nx, int32_t ny,
                             int32_t shift, int32_t n_inner,
-                            unsigned long long* __restrict__ chunk_ns) {
+                            unsigned long long* __restrict__ chunk_ns,
+                            const unsigned long long* __restrict__ halo_flags,
+                            const int32_t* __restrict__ senders, int32_t n_senders,
+                            unsigned long long stamp, unsigned long long* __restrict__ wait_ns) {
   __shared__ __align__(16) double ring[8 * 10 * 68];
   __shared__ int s_next;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  bool halo_ready = n_senders == 0;
   for (;;) {
     if (lead) s_next = int(atomicAdd(counter, 1u));
     __syncthreads();
     const int ti = s_next;
     __syncthreads();
     if (ti >= ntiles) break;
+    if (tiles[ti].pad & 1) {
+      if (lead && !halo_ready) {
+        const uint64_t w0 = globaltimer_ns();
+        wait_stamps(halo_flags, senders, n_senders, stamp, 20ull * 1000 * 1000 * 1000);
+        // time this SM idled for the neighbours (kept out of the load measurement)
+        if (wait_ns) atomicMax(wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+        halo_ready = true;
+      }
+      __syncthreads();
+    }
     tile_step4<S, TIMED>(ring, tiles[ti], chunks, nz, F, cfield, nx, ny, shift, n_inner,
                          chunk_ns);
   }
@@ -994,14 +1048,6 @@ __global__ void pack_faces(const ChunkDev* __restrict__ chunks, const PackJob* _
 // buffered by step parity; faces are symmetric between ranks, so a rank can
 // only reach step t+2 after its neighbours finished reading step t.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
                                const PackJob* __restrict__ jobs, double* const* __restrict__ peer_base,
@@ -1042,14 +1088,7 @@ __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
 __global__ void wait_halo(const unsigned long long* __restrict__ flags,
                           const int32_t* __restrict__ senders, int32_t n,
                           unsigned long long value, unsigned long long timeout_ns) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const unsigned long long* f = flags + senders[i];
-    const uint64_t t0 = globaltimer_ns();
-    while (ld_acquire_sys(f) < value) {
-      if (globaltimer_ns() - t0 > timeout_ns) __trap();  // a peer died: fail loudly
-      __nanosleep(64);
-    }
-  }
+  if (threadIdx.x == 0) wait_stamps(flags, senders, n, value, timeout_ns);
 }
 
 // ---------------------------------------------------------------------------

@@ -432,7 +432,9 @@ void Runtime::refresh_tile_order() {
         const int32_t T = int32_t(std::floor(double(cfg_.nz) * field_.at(x, y))) - 1;
         w += double(T > 0 ? T : 0) * (cfg_.n_inner + 1) + jac;
       }
-    key[t] = {-w, int32_t(t)};
+    // tiles that read strips from other GPUs go last (their data arrives while
+    // the interior runs); heaviest first within each group
+    key[t] = {(td.pad & 1 ? 1e300 : 0.0) - w, int32_t(t)};
   }
   std::stable_sort(key.begin(), key.end());
   const int b = tiles4s_cur_ ^ 1;
@@ -594,8 +596,18 @@ void Runtime::rebuild_tables() {
   for (int32_t i = 0; i < nres; ++i) {
     const Sub& s = subs_[resident_[i]];
     tile4_begin_[i] = int32_t(tiles4_.size());
+    const int32_t v = resident_[i];
+    bool remote[4];
+    for (int d = 0; d < 4; ++d) {
+      const int32_t n = nbr(v, d);
+      remote[d] = n >= 0 && rank_of_vp(n) != rank_;
+    }
     for (int32_t ty = 0; ty < s.h(); ty += kTY4)
-      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) tiles4_.push_back(TileDev{i, tx, ty, 0});
+      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) {
+        const bool needs = (remote[kLeft] && tx == 0) || (remote[kRight] && tx + 2 * kTX >= s.w()) ||
+                           (remote[kTop] && ty == 0) || (remote[kBottom] && ty + kTY4 >= s.h());
+        tiles4_.push_back(TileDev{i, tx, ty, needs ? 1 : 0});
+      }
     tile4_count_[i] = int32_t(tiles4_.size()) - tile4_begin_[i];
   }
   if (tiles4_.size() > tiles4_cap_) {
@@ -735,7 +747,8 @@ void Runtime::rebuild_tables() {
     upload(d_chunks_[par], d_chunks_cap_[par], tab);
   }
   if (!d_trips_ || ns_cols_ < nres) {
-    ns_cols_ = std::max(std::max(nres, 1), int(slab_slots_));
+    // last column: the longest in-kernel wait for remote halos (per step)
+    ns_cols_ = std::max(std::max(nres, 1), int(slab_slots_)) + 1;
     cudaFree(d_trips_);
     OD_CU(cudaMalloc(&d_trips_, size_t(ns_cols_) * sizeof(unsigned long long)));
     cudaFree(d_ns_);
@@ -894,7 +907,11 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       e1 = new_event();
       OD_CU(cudaEventRecord(events_[e1], s0_));
     }
-    if (n_senders_ > 0) {
+    // the persistent kernels wait inside, before the first tile that needs a
+    // remote strip; the other kernels wait here
+    const bool in_kernel = (cfg_.overlap == 5 || cfg_.overlap == 6) &&
+                           (mode == kAsync || timer);
+    if (n_senders_ > 0 && !in_kernel) {
       wait_halo<<<1, 32, 0, s0_>>>(d_flags_, d_senders_, n_senders_, stamp,
                                    20ull * 1000 * 1000 * 1000);
       OD_CU(cudaGetLastError());
@@ -956,14 +973,18 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
+    const int32_t nsend = p2p_ ? n_senders_ : 0;
+    const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
     if (timer)
       column_step4_persistent<kFusedPrefetch, true, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
           d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
-          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns);
+          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend, stamp,
+          ns + (ns_cols_ - 1));
     else
       column_step4_persistent<kFusedPrefetch, false, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
           d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
-          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr);
+          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend,
+          stamp, nullptr);
     OD_CU(cudaGetLastError());
     if (profiling_) {
       e1 = new_event();
@@ -983,15 +1004,19 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
     const dim3 blk4(kTX, 4);
+    const int32_t nsend = p2p_ ? n_senders_ : 0;
+    const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
 #define OD_LAUNCH_PS(MB)                                                                    \
   if (timer)                                                                                \
     column_step_persistent<4, kFusedPrefetch, true, MB><<<grid, blk4, 0, s0_>>>(         \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
-        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns);                                 \
+        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend,     \
+        stamp, ns + (ns_cols_ - 1));                                                        \
   else                                                                                      \
     column_step_persistent<4, kFusedPrefetch, false, MB><<<grid, blk4, 0, s0_>>>(        \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
-        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr);
+        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, \
+        stamp, nullptr);
     if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
@@ -1149,7 +1174,8 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
           double sum = 0;
           for (size_t j = 0; j < r.slot_vps.size(); ++j)
             sum += double(ns[size_t(r.ns_row) * ns_cols_ + j]);
-          const double kt = elapsed_s(events_[r.kev0], events_[r.kev1]);
+          const double wait = double(ns[size_t(r.ns_row) * ns_cols_ + (ns_cols_ - 1)]) * 1e-9;
+          const double kt = std::max(0.0, elapsed_s(events_[r.kev0], events_[r.kev1]) - wait);
           v = sum > 0 ? double(ns[size_t(r.ns_row) * ns_cols_ + i]) / sum * kt : 0.0;
         }
       }
