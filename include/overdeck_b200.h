@@ -109,6 +109,26 @@ int od_proc_loads(const double* loads, int32_t n_loads, const int32_t* map,
 /* imbalance_ratio                                     cluster.hpp:151-157 */
 int od_imbalance_ratio(const double* totals, int32_t n, double* out);
 
+/* ---------------------------------------------------------- modelled costs */
+/* The reference's analytic GPU model (gpu_cost.hpp:21-47).  The B200 path
+ * measures instead; these keep the simulator's arithmetic for comparisons. */
+typedef struct od_gpu_model {
+  double launch_overhead, per_item_time, saturation_floor;
+  double h2d_bandwidth, d2h_bandwidth, async_overlap_gain;
+} od_gpu_model;
+/* kernel_time_sync                                     gpu_cost.hpp:50-54 */
+int od_kernel_time_sync(const od_kernel_work* work, const od_gpu_model* gpu, double* out);
+/* transfer_time (host_to_device: 1 = H2D, 0 = D2H)      gpu_cost.hpp:60-66 */
+int od_transfer_time(double bytes, int32_t host_to_device, const od_gpu_model* gpu, double* out);
+/* node_gpu_schedule (mode OD_SYNC / OD_ASYNC)           gpu_cost.hpp:70-80 */
+int od_node_gpu_schedule(const double* jobs, int32_t n, int32_t mode, const od_gpu_model* gpu,
+                         double* out);
+/* plan_cost over per-VP data bytes                     balancer.hpp:157-175 */
+int od_plan_cost(const od_move* moves, int32_t n_moves, const int64_t* data_bytes,
+                 int32_t vp_count, int32_t procs_per_node, int32_t nodes,
+                 double network_bandwidth, double network_latency, const od_gpu_model* gpu,
+                 double* out);
+
 /* ---------------------------------------------------------------- balancer */
 /* should_balance                                       balancer.hpp:29-32 */
 int od_should_balance(const double* totals, int32_t n, double trigger_threshold,

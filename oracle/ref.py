@@ -53,6 +53,10 @@ def lib():
         l.ref_jacobi_work.argtypes = [I, I, I, I, I, I, DP, DP]
         l.ref_epoch_loads.argtypes = [I, I, I, IP, DP, I, DP]
         l.ref_run_json.argtypes = [C.c_char_p, C.c_char_p, C.c_long]
+        l.ref_kernel_time_sync.argtypes = [D, D, DP, DP]
+        l.ref_transfer_time.argtypes = [D, I, DP, DP]
+        l.ref_node_gpu_schedule.argtypes = [DP, I, I, DP, DP]
+        l.ref_plan_cost.argtypes = [IP, I, C.POINTER(C.c_longlong), I, I, I, D, D, DP, DP]
         l.ref_preset_json.argtypes = [C.c_char_p, C.c_char_p, C.c_long]
         _lib = l
     return _lib
@@ -203,3 +207,36 @@ def base_field(cfg) -> np.ndarray:
         rects = node0_rects(d.nx, d.ny, kind, cfg.decomposition.kx, cfg.decomposition.ky,
                             cfg.cluster.nodes, cfg.cluster.procs_per_node)
     return init_load_field(d.nx, d.ny, int(cfg.pattern), cfg.heavy_value, cfg.light_value, rects)
+
+
+def _gm(g):
+    return np.array([g.launch_overhead, g.per_item_time, g.saturation_floor, g.h2d_bandwidth,
+                     g.d2h_bandwidth, g.async_overlap_gain], dtype=np.float64)
+
+
+def kernel_time_sync(items, depth, g):
+    out = C.c_double()
+    _chk(lib().ref_kernel_time_sync(items, depth, _dp(_gm(g)), C.byref(out)))
+    return out.value
+
+
+def transfer_time(nbytes, h2d, g):
+    out = C.c_double()
+    _chk(lib().ref_transfer_time(float(nbytes), int(h2d), _dp(_gm(g)), C.byref(out)))
+    return out.value
+
+
+def node_gpu_schedule(jobs, mode, g):
+    j = np.ascontiguousarray(jobs, dtype=np.float64)
+    out = C.c_double()
+    _chk(lib().ref_node_gpu_schedule(_dp(j), len(j), int(mode), _dp(_gm(g)), C.byref(out)))
+    return out.value
+
+
+def plan_cost(moves, data_bytes, nodes, ppn, bw, lat, g):
+    mv = np.ascontiguousarray(np.array(moves, dtype=np.int32).reshape(-1))
+    b = np.ascontiguousarray(data_bytes, dtype=np.int64)
+    out = C.c_double()
+    _chk(lib().ref_plan_cost(_ip(mv), len(moves), b.ctypes.data_as(C.POINTER(C.c_longlong)),
+                             len(b), nodes, ppn, bw, lat, _dp(_gm(g)), C.byref(out)))
+    return out.value

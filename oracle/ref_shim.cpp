@@ -12,6 +12,8 @@
 //   proc_loads / imbalance_ratio         cluster.hpp:142-157
 //   LoadDB / epoch_loads                 measurement.hpp:40-91
 //   run_experiment + render_report       engine.hpp:357, report.hpp:69
+//   kernel_time_sync / transfer_time / node_gpu_schedule / plan_cost
+//                                        gpu_cost.hpp:50-80, balancer.hpp:157-175
 #include <cstring>
 #include <exception>
 #include <string>
@@ -195,6 +197,47 @@ int ref_epoch_loads(int K, int async_steps, int sync_steps, const int* rows, con
                  rows[3 * i + 2] == 0 ? LaunchMode::Sync : LaunchMode::Async, vals[i]});
     auto l = epoch_loads(db);
     std::copy(l.begin(), l.end(), out);
+  });
+}
+
+static GpuModel gm(const double* g) {
+  GpuModel m;
+  m.launch_overhead = g[0];
+  m.per_item_time = g[1];
+  m.saturation_floor = g[2];
+  m.h2d_bandwidth = g[3];
+  m.d2h_bandwidth = g[4];
+  m.async_overlap_gain = g[5];
+  return m;
+}
+
+int ref_kernel_time_sync(double items, double depth, const double* g, double* out) {
+  return wrap([&] { *out = kernel_time_sync(KernelWork{items, depth}, gm(g)); });
+}
+
+int ref_transfer_time(double bytes, int h2d, const double* g, double* out) {
+  return wrap([&] {
+    *out = transfer_time(bytes, h2d ? TransferDirection::HostToDevice
+                                    : TransferDirection::DeviceToHost, gm(g));
+  });
+}
+
+int ref_node_gpu_schedule(const double* jobs, int n, int mode, const double* g, double* out) {
+  return wrap([&] {
+    *out = node_gpu_schedule(std::vector<double>(jobs, jobs + n),
+                             mode == 0 ? LaunchMode::Sync : LaunchMode::Async, gm(g));
+  });
+}
+
+int ref_plan_cost(const int* moves, int n, const long long* bytes, int K, int nodes, int ppn,
+                  double bw, double lat, const double* g, double* out) {
+  return wrap([&] {
+    MigrationPlan plan;
+    for (int i = 0; i < n; ++i) plan.moves.push_back({moves[3 * i], moves[3 * i + 1], moves[3 * i + 2]});
+    std::vector<VirtualProcess> vps(K);
+    for (int v = 0; v < K; ++v) vps[v].data_bytes = bytes[v];
+    ClusterState cl = build_cluster(ClusterSpec{nodes, ppn, 1, bw, lat});
+    *out = plan_cost(plan, vps, cl, gm(g));
   });
 }
 

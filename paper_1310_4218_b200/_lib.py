@@ -97,6 +97,12 @@ class od_epoch_summary(C.Structure):
                 ("imbalance_after", C.c_double), ("boundary_seconds", C.c_double)]
 
 
+class od_gpu_model(C.Structure):
+    _fields_ = [("launch_overhead", C.c_double), ("per_item_time", C.c_double),
+                ("saturation_floor", C.c_double), ("h2d_bandwidth", C.c_double),
+                ("d2h_bandwidth", C.c_double), ("async_overlap_gain", C.c_double)]
+
+
 class od_face_xfer(C.Structure):
     _fields_ = [("peer", C.c_int32), ("vp", C.c_int32), ("side", C.c_int32),
                 ("nbr", C.c_int32), ("len", C.c_int32), ("lenp", C.c_int32),
@@ -127,6 +133,11 @@ PROTOTYPES = {
     "od_should_balance": [_P(_D), _I32, _D, _P(_I32)],
     "od_greedy_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _P(od_move), _I32, _P(_I32)],
     "od_refine_swap_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _P(od_move), _I32, _P(_I32)],
+    "od_kernel_time_sync": [_P(od_kernel_work), _P(od_gpu_model), _P(_D)],
+    "od_transfer_time": [_D, _I32, _P(od_gpu_model), _P(_D)],
+    "od_node_gpu_schedule": [_P(_D), _I32, _I32, _P(od_gpu_model), _P(_D)],
+    "od_plan_cost": [_P(od_move), _I32, _P(_I64), _I32, _I32, _I32, _D, _D, _P(od_gpu_model),
+                     _P(_D)],
     "od_epoch_decision": [_P(_D), _I32, _P(_I32), _I32, _I32, _I32, _I32, _P(_I32), _I32, _I32,
                           _D, _D, _P(_I32), _P(od_move), _I32, _P(_I32), _P(_D), _P(_D),
                           _P(_D)],

@@ -26,7 +26,7 @@ from typing import List, Optional, Sequence, Tuple
 import numpy as np
 
 from ._lib import (RuntimeFault, ValidationError, check, lib, od_config, od_epoch_record,
-                   od_epoch_summary, od_face_xfer,
+                   od_epoch_summary, od_face_xfer, od_gpu_model,
                    od_kernel_work, od_move, od_rt_stats, od_sample, od_subdomain)
 
 __all__ = [
@@ -39,7 +39,8 @@ __all__ = [
     "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
     "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
-    "FaceXfer", "exchange_schedule",
+    "FaceXfer", "exchange_schedule", "GpuModel", "TransferDirection", "kernel_time_sync",
+    "transfer_time", "node_gpu_schedule", "plan_cost",
 ]
 
 
@@ -454,6 +455,64 @@ def exchange_schedule(subs: Sequence[SubDomain], kind: DecompositionKind, kx: in
                                    C.byref(nr)))
     cv = lambda f: FaceXfer(f.peer, f.vp, f.side, f.nbr, f.len, f.lenp, f.offset)  # noqa: E731
     return [cv(so[i]) for i in range(ns.value)], [cv(ro[i]) for i in range(nr.value)]
+
+
+# ------------------------------------------------------------- modelled costs --
+
+class TransferDirection(enum.IntEnum):  # gpu_cost.hpp:17
+    HostToDevice = 0
+    DeviceToHost = 1
+
+
+@dataclass
+class GpuModel:  # gpu_cost.hpp:21-39 (analytic; the B200 path measures instead)
+    launch_overhead: float = 1.0e-4
+    per_item_time: float = 1.0e-9
+    saturation_floor: float = 0.0
+    h2d_bandwidth: float = 6.0e9
+    d2h_bandwidth: float = 6.0e9
+    async_overlap_gain: float = 0.06
+
+    def _c(self) -> od_gpu_model:
+        return od_gpu_model(self.launch_overhead, self.per_item_time, self.saturation_floor,
+                            self.h2d_bandwidth, self.d2h_bandwidth, self.async_overlap_gain)
+
+
+def kernel_time_sync(work: KernelWork, gpu: GpuModel) -> float:  # gpu_cost.hpp:50-54
+    out = C.c_double()
+    w = od_kernel_work(work.work_items, work.serial_depth)
+    g = gpu._c()
+    check(lib.od_kernel_time_sync(C.byref(w), C.byref(g), C.byref(out)))
+    return out.value
+
+
+def transfer_time(bytes_: float, direction: TransferDirection, gpu: GpuModel) -> float:
+    out = C.c_double()  # gpu_cost.hpp:60-66
+    g = gpu._c()
+    check(lib.od_transfer_time(float(bytes_), 1 if direction == TransferDirection.HostToDevice
+                               else 0, C.byref(g), C.byref(out)))
+    return out.value
+
+
+def node_gpu_schedule(jobs: Sequence[float], mode: LaunchMode, gpu: GpuModel) -> float:
+    j = np.ascontiguousarray(jobs, dtype=np.float64)  # gpu_cost.hpp:70-80
+    out = C.c_double()
+    g = gpu._c()
+    check(lib.od_node_gpu_schedule(_dptr(j), int(j.size), int(mode), C.byref(g), C.byref(out)))
+    return out.value
+
+
+def plan_cost(plan: MigrationPlan, data_bytes: Sequence[int], procs_per_node: int, nodes: int,
+              gpu: GpuModel, network_bandwidth: float = 5.0e9,
+              network_latency: float = 1.0e-5) -> float:  # balancer.hpp:157-175
+    db = np.ascontiguousarray(data_bytes, dtype=np.int64)
+    out = C.c_double()
+    g = gpu._c()
+    check(lib.od_plan_cost(_moves_c(plan.moves), len(plan.moves),
+                           db.ctypes.data_as(C.POINTER(C.c_int64)), int(db.size),
+                           int(procs_per_node), int(nodes), float(network_bandwidth),
+                           float(network_latency), C.byref(g), C.byref(out)))
+    return out.value
 
 
 # --------------------------------------------------------------- measurement --

@@ -247,6 +247,62 @@ int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
   });
 }
 
+static GpuCostModel gpu_of(const od_gpu_model* g) {
+  need(g, "gpu model");
+  GpuCostModel m;
+  m.launch_overhead = g->launch_overhead;
+  m.per_item_time = g->per_item_time;
+  m.saturation_floor = g->saturation_floor;
+  m.h2d_bandwidth = g->h2d_bandwidth;
+  m.d2h_bandwidth = g->d2h_bandwidth;
+  m.async_overlap_gain = g->async_overlap_gain;
+  m.validate();
+  return m;
+}
+
+int od_kernel_time_sync(const od_kernel_work* work, const od_gpu_model* gpu, double* out) {
+  return guarded([&] {
+    need(work, "work");
+    need(out, "out");
+    *out = kernel_time_sync_model(Work{work->work_items, work->serial_depth}, gpu_of(gpu));
+  });
+}
+
+int od_transfer_time(double bytes, int32_t host_to_device, const od_gpu_model* gpu, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    *out = transfer_time_model(bytes, host_to_device != 0, gpu_of(gpu));
+  });
+}
+
+int od_node_gpu_schedule(const double* jobs, int32_t n, int32_t mode, const od_gpu_model* gpu,
+                         double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (mode != OD_SYNC && mode != OD_ASYNC) throw ValidationError("unknown launch mode");
+    *out = node_gpu_schedule_model(vec_view(jobs, n, "jobs"), mode, gpu_of(gpu));
+  });
+}
+
+int od_plan_cost(const od_move* moves, int32_t n_moves, const int64_t* data_bytes,
+                 int32_t vp_count, int32_t procs_per_node, int32_t nodes,
+                 double network_bandwidth, double network_latency, const od_gpu_model* gpu,
+                 double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_moves < 0 || vp_count < 0) throw ValidationError("negative count");
+    if (n_moves > 0) need(moves, "moves");
+    if (vp_count > 0) need(data_bytes, "data_bytes");
+    if (network_bandwidth <= 0) throw ValidationError("cluster.network_bandwidth must be > 0");
+    if (network_latency < 0) throw ValidationError("cluster.network_latency must be >= 0");
+    std::vector<MoveRec> mv(n_moves);
+    for (int32_t i = 0; i < n_moves; ++i) mv[i] = {moves[i].vp, moves[i].from, moves[i].to};
+    std::vector<int64_t> db(data_bytes, data_bytes + vp_count);
+    *out = plan_cost_model(mv, db, procs_per_node, nodes, network_bandwidth, network_latency,
+                           gpu_of(gpu));
+  });
+}
+
 int od_epoch_decision(const double* loads, int32_t n_loads, const int32_t* map,
                       int32_t vp_count, int32_t proc_count, int32_t epoch_index, int32_t epochs,
                       int32_t* balance_calls, int32_t first_strategy, int32_t later_strategy,

@@ -302,6 +302,66 @@ std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
   return plan;
 }
 
+// ------------------------------------------------------------ modelled costs --
+
+void GpuCostModel::validate() const {
+  if (launch_overhead < 0 || per_item_time < 0 || saturation_floor < 0)
+    throw ValidationError("gpu model times must be >= 0");
+  if (h2d_bandwidth <= 0 || d2h_bandwidth <= 0)
+    throw ValidationError("gpu model bandwidths must be > 0");
+  if (async_overlap_gain < 0 || async_overlap_gain >= 1)
+    throw ValidationError("gpu model async_overlap_gain must be in [0, 1)");
+}
+
+double kernel_time_sync_model(const Work& w, const GpuCostModel& g) {
+  if (w.total() <= 0) return 0.0;
+  const double t = g.launch_overhead + g.per_item_time * w.total();
+  return g.saturation_floor < t ? t : g.saturation_floor;
+}
+
+double transfer_time_model(double bytes, bool host_to_device, const GpuCostModel& g) {
+  if (bytes < 0) throw ValidationError("transfer bytes must be >= 0");
+  if (bytes == 0) return 0.0;
+  return bytes / (host_to_device ? g.h2d_bandwidth : g.d2h_bandwidth);
+}
+
+double node_gpu_schedule_model(const std::vector<double>& jobs, int32_t mode,
+                               const GpuCostModel& g) {
+  double sum = 0.0, mx = 0.0;
+  for (double j : jobs) {
+    if (j < 0) throw ValidationError("kernel durations must be >= 0");
+    sum += j;
+    mx = mx < j ? j : mx;
+  }
+  if (mode == kSync || jobs.size() <= 1) return sum;
+  const double overlapped = sum * (1.0 - g.async_overlap_gain);
+  return overlapped < mx ? mx : overlapped;
+}
+
+double plan_cost_model(const std::vector<MoveRec>& plan, const std::vector<int64_t>& data_bytes,
+                       int32_t procs_per_node, int32_t nodes, double net_bandwidth,
+                       double net_latency, const GpuCostModel& g) {
+  if (procs_per_node < 1 || nodes < 1) throw ValidationError("cluster counts must be >= 1");
+  std::vector<double> per_node(nodes, 0.0);
+  for (const MoveRec& m : plan) {
+    if (m.vp < 0 || m.vp >= int32_t(data_bytes.size()))
+      throw ValidationError("move names an unknown vp");
+    const double bytes = double(data_bytes[m.vp]);
+    const int32_t a = m.from / procs_per_node, b = m.to / procs_per_node;
+    if (a < 0 || a >= nodes || b < 0 || b >= nodes) throw ValidationError("processor id out of range");
+    per_node[a] += transfer_time_model(bytes, false, g);
+    per_node[b] += transfer_time_model(bytes, true, g);
+    if (a != b) {
+      const double hop = bytes / net_bandwidth + net_latency;
+      per_node[a] += hop;
+      per_node[b] += hop;
+    }
+  }
+  double mx = 0.0;
+  for (double c : per_node) mx = mx < c ? c : mx;
+  return per_node.empty() ? 0.0 : mx;
+}
+
 // ------------------------------------------------------------ epoch policy --
 
 Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,

@@ -89,6 +89,25 @@ std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
                                       const std::vector<int32_t>& map, int32_t P,
                                       double tol);                            // :68-152
 
+// ---- modelled costs (gpu_cost.hpp:21-80, balancer.hpp:157-175) ---------------
+// The B200 path measures these quantities; the model functions stay available
+// with the reference's arithmetic for users who compare against the simulator.
+struct GpuCostModel {
+  double launch_overhead = 1.0e-4, per_item_time = 1.0e-9, saturation_floor = 0.0;
+  double h2d_bandwidth = 6.0e9, d2h_bandwidth = 6.0e9, async_overlap_gain = 0.06;
+  void validate() const;
+};
+double kernel_time_sync_model(const Work& w, const GpuCostModel& g);                // :50-54
+double transfer_time_model(double bytes, bool host_to_device, const GpuCostModel& g);  // :60-66
+double node_gpu_schedule_model(const std::vector<double>& jobs, int32_t mode,
+                               const GpuCostModel& g);                                // :70-80
+// plan_cost: per moved VP a D2H stage on the source node, an H2D stage on the
+// destination node, plus the network hop on both when the nodes differ; nodes
+// in parallel, each node's transfers serialised (balancer.hpp:157-175)
+double plan_cost_model(const std::vector<MoveRec>& plan, const std::vector<int64_t>& data_bytes,
+                       int32_t procs_per_node, int32_t nodes, double net_bandwidth,
+                       double net_latency, const GpuCostModel& g);
+
 // ---- epoch policy (Engine::run_epoch, engine.hpp:257-268) --------------------
 struct Decision {
   int32_t strategy = -1;  // -1: no strategy called
