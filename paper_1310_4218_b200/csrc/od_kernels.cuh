@@ -45,6 +45,9 @@ struct ChunkDev {
 struct TileDev {
   int32_t slot, tx0, ty0, pad;
 };
+__device__ __forceinline__ int share_tag(const TileDev& t) {
+  return (t.slot << 20) | (t.ty0 << 8) | (t.tx0 >> 5);
+}
 
 struct PackJob {
   int32_t slot, side, len, lenp;  // side: which edge of the source chunk; lenp: row stride
@@ -68,6 +71,53 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Per-SM processor-sharing clock for the per-chunk load measurement.  The
+// CTAs resident on one SM share its FP64 pipe, so a tile's wall duration
+// depends on how many neighbours it had (heavy tiles early in the heaviest-
+// first queue run under full contention, the tail runs nearly alone).  Each
+// SM keeps V(t) = integral dt / n_active(t); a tile is charged V(end) -
+// V(start), its fair share of the SM.  The shares of all tiles on an SM sum to
+// the SM's busy time, independent of the queue position of the tile.
+// Updated by one thread per CTA at tile begin/end under a per-SM spin lock.
+struct SmShare {
+  int lock, n;
+  unsigned long long t_last;
+  double v, pad;
+};
+__device__ SmShare g_sm_share[1024];
+// diagnostic event log of the share clock (OD_TILELOG): {time, V, n, tag, sm, delta}
+struct ShareEvent {
+  unsigned long long t;
+  double v;
+  int n, tag, sm, delta;
+};
+__device__ ShareEvent* g_share_log = nullptr;
+__device__ unsigned int g_share_log_n = 0;
+__device__ unsigned int g_share_log_cap = 0;
+
+__device__ __noinline__ double sm_share_update(int delta, int tag) {
+  unsigned sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  SmShare* s = &g_sm_share[sm & 1023];
+  while (atomicCAS(&s->lock, 0, 1) != 0) __nanosleep(20);
+  __threadfence();
+  volatile SmShare* vs = s;
+  const unsigned long long now = globaltimer_ns();
+  double v = vs->v;
+  const int n = vs->n;
+  if (n > 0 && now > vs->t_last) v += double(now - vs->t_last) / double(n);
+  vs->v = v;
+  vs->t_last = now;
+  vs->n = n + delta;
+  if (g_share_log) {
+    const unsigned i = atomicAdd(&g_share_log_n, 1u);
+    if (i < g_share_log_cap) g_share_log[i] = ShareEvent{now, v, n, tag, int(sm), delta};
+  }
+  __threadfence();
+  atomicExch(&s->lock, 0);
+  return v;
 }
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -136,8 +186,8 @@ __global__ void __launch_bounds__(TX* TY)
   constexpr int R = S + 2;
   __shared__ __align__(16) double ring[R][TY + 2][TX + 2];
 
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+  double t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tiles[blockIdx.x]));
 
   const TileDev tile = tiles[blockIdx.x];
   const ChunkDev& c = chunks[tile.slot];
@@ -225,7 +275,7 @@ __global__ void __launch_bounds__(TX* TY)
   if (TIMED) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -271,8 +321,8 @@ __global__ void __launch_bounds__(TX* TY)
                  const double* __restrict__ cfield, int32_t nx, int32_t ny, int32_t shift,
                  int32_t nz, int32_t n_inner, unsigned long long* __restrict__ chunk_ns,
                  unsigned long long* __restrict__ trips) {
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+  double t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tiles[blockIdx.x]));
   const TileDev tile = tiles[blockIdx.x];
   const int T = physics_column(chunks[tile.slot], tile, threadIdx.x, threadIdx.y, cfield, nx, ny,
                                shift, nz, n_inner);
@@ -284,7 +334,7 @@ __global__ void __launch_bounds__(TX* TY)
   if (TIMED) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -404,8 +454,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
   constexpr int PLANE = (TY + 2) * PW;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+  double t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
 
   const ChunkDev& c = chunks[tile.slot];
   const int lx = threadIdx.x, ly = threadIdx.y;
@@ -576,7 +626,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   if (TIMED) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -720,8 +770,8 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
   constexpr int PW = 68;
   constexpr int PLANE = (TY + 2) * PW;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  uint64_t t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = globaltimer_ns();
+  double t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
 
   const ChunkDev& c = chunks[tile.slot];
   const int lx = threadIdx.x, ly = threadIdx.y;  // ly in [0, 4)
@@ -964,7 +1014,7 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
   if (TIMED) {
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)(globaltimer_ns() - t_start));
+      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -1084,6 +1134,11 @@ __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
     }
   }
 }
+
+// Diagnostic device timeline (OD_TIMELINE): one globaltimer stamp in stream order.
+__global__ void stamp_time(unsigned long long* __restrict__ slot) { *slot = globaltimer_ns(); }
+__global__ void copy_u64(unsigned long long* __restrict__ dst,
+                         const unsigned long long* __restrict__ src) { *dst = *src; }
 
 __global__ void wait_halo(const unsigned long long* __restrict__ flags,
                           const int32_t* __restrict__ senders, int32_t n,

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <array>
+#include <tuple>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -219,6 +220,25 @@ class Runtime {
   unsigned long long* d_trips_ = nullptr;
   double* d_gather_ = nullptr;
   size_t gather_cap_ = 0;
+  // diagnostic device timeline (env OD_TIMELINE=<path prefix>): per step,
+  // globaltimer stamps at step begin, after the halo pack, before and after
+  // the step kernel; written to <prefix>.rank<r>.txt at destruction
+  unsigned long long* d_tl_ = nullptr;
+  int tl_cap_ = 0, tl_n_ = 0;
+  void tl_mark(int k) {
+    if (d_tl_ && tl_n_ < tl_cap_) stamp_time<<<1, 1, 0, s0_>>>(d_tl_ + size_t(tl_n_) * 5 + k);
+  }
+  void tl_dump();
+  double tr_drained_ = 0;  // OD_TRACE: host time the stream last drained
+  // diagnostic share-clock event log of one step (env OD_TILELOG=<path>, OD_TILELOG_STEP=<n>)
+  ShareEvent* d_slog_ = nullptr;
+  unsigned slog_cap_ = 0;
+  long slog_step_ = -1;
+  void slog_arm(bool on);
+  void slog_dump();
+  unsigned long long* tl_wait() {
+    return d_tl_ && tl_n_ < tl_cap_ ? d_tl_ + size_t(tl_n_) * 5 + 4 : nullptr;
+  }
   // stats
   bool profiling_ = false;
   std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_, prof_f_;
@@ -277,6 +297,16 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
 
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
+  if (std::getenv("OD_TILELOG")) {
+    slog_cap_ = 1u << 20;
+    slog_step_ = std::getenv("OD_TILELOG_STEP") ? std::atol(std::getenv("OD_TILELOG_STEP")) : 19;
+    OD_CU(cudaMalloc(&d_slog_, size_t(slog_cap_) * sizeof(ShareEvent)));
+  }
+  if (std::getenv("OD_TIMELINE")) {
+    tl_cap_ = 8192;
+    OD_CU(cudaMalloc(&d_tl_, size_t(tl_cap_) * 5 * sizeof(unsigned long long)));
+    OD_CU(cudaMemset(d_tl_, 0, size_t(tl_cap_) * 5 * sizeof(unsigned long long)));
+  }
   {
     int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
@@ -356,9 +386,57 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   OD_CU(cudaStreamSynchronize(s0_));
 }
 
+void Runtime::slog_arm(bool on) {
+  ShareEvent* p = on ? d_slog_ : nullptr;
+  unsigned zero = 0;
+  OD_CU(cudaMemcpyToSymbolAsync(g_share_log, &p, sizeof(p), 0, cudaMemcpyHostToDevice, s0_));
+  if (on) {
+    OD_CU(cudaMemcpyToSymbolAsync(g_share_log_n, &zero, sizeof(zero), 0, cudaMemcpyHostToDevice, s0_));
+    OD_CU(cudaMemcpyToSymbolAsync(g_share_log_cap, &slog_cap_, sizeof(slog_cap_), 0,
+                                  cudaMemcpyHostToDevice, s0_));
+  }
+}
+
+void Runtime::slog_dump() {
+  const char* path = std::getenv("OD_TILELOG");
+  if (!d_slog_ || !path) return;
+  unsigned n = 0;
+  if (cudaMemcpyFromSymbol(&n, g_share_log_n, sizeof(n)) != cudaSuccess) return;
+  n = std::min(n, slog_cap_);
+  std::vector<ShareEvent> h(n);
+  if (n && cudaMemcpy(h.data(), d_slog_, n * sizeof(ShareEvent), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  const std::string p = std::string(path) + ".rank" + std::to_string(rank_) + ".txt";
+  if (FILE* f = std::fopen(p.c_str(), "w")) {
+    for (const auto& e : h)
+      std::fprintf(f, "%llu %.3f %d %d %d %d\n", e.t, e.v, e.n, e.tag, e.sm, e.delta);
+    std::fclose(f);
+  }
+}
+
+void Runtime::tl_dump() {
+  const char* pre = std::getenv("OD_TIMELINE");
+  if (!d_tl_ || !pre || tl_n_ == 0) return;
+  std::vector<unsigned long long> h(size_t(tl_n_) * 5);
+  if (cudaMemcpy(h.data(), d_tl_, h.size() * sizeof(unsigned long long),
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
+    return;
+  const std::string path = std::string(pre) + ".rank" + std::to_string(rank_) + ".txt";
+  if (FILE* f = std::fopen(path.c_str(), "w")) {
+    for (int i = 0; i < tl_n_; ++i)
+      std::fprintf(f, "%d %llu %llu %llu %llu %llu\n", i, h[5 * i], h[5 * i + 1], h[5 * i + 2],
+                   h[5 * i + 3], h[5 * i + 4]);
+    std::fclose(f);
+  }
+}
+
 Runtime::~Runtime() {
   cudaSetDevice(device_);
   if (s0_) cudaStreamSynchronize(s0_);
+  tl_dump();
+  cudaFree(d_tl_);
+  slog_dump();
+  cudaFree(d_slog_);
   for (auto& m : chunks_)
     if (m.base && !(slab_ && m.base >= slab_ &&
                     m.base < slab_ + slab_slots_ * (slot_bytes_ / sizeof(double))))
@@ -419,7 +497,13 @@ void Runtime::set_shift(int32_t rows) {
 void Runtime::refresh_tile_order() {
   const size_t n = tiles4_.size();
   if (n == 0) return;
-  std::vector<std::pair<double, int32_t>> key(n);
+  // (group, -work, tile index within its chunk, tile): equal-work tiles are
+  // dealt round-robin over the chunks, so each chunk's tiles meet every queue
+  // position (and with it every issue priority on the SM: the warp scheduler
+  // favours older CTAs) and the per-chunk measurements average over them
+  std::vector<std::tuple<double, int32_t, int32_t>> key(n);
+  static const bool chunk_major = std::getenv("OD_TILE_ORDER") &&
+                                  std::string(std::getenv("OD_TILE_ORDER")) == "chunk";
   const double jac = 2.0 * cfg_.nz * cfg_.fields;  // a Jacobi cell ~ 2 micro-steps
   for (size_t t = 0; t < n; ++t) {
     const TileDev& td = tiles4_[t];
@@ -434,12 +518,13 @@ void Runtime::refresh_tile_order() {
       }
     // tiles that read strips from other GPUs go last (their data arrives while
     // the interior runs); heaviest first within each group
-    key[t] = {(td.pad & 1 ? 1e300 : 0.0) - w, int32_t(t)};
+    key[t] = {(td.pad & 1 ? 1e300 : 0.0) - w,
+              chunk_major ? 0 : int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
   }
-  std::stable_sort(key.begin(), key.end());
+  std::sort(key.begin(), key.end());
   const int b = tiles4s_cur_ ^ 1;
   OD_CU(cudaEventSynchronize(tiles4s_ev_[b]));  // previous upload from this buffer done
-  for (size_t t = 0; t < n; ++t) h_tiles4s_[b][t] = tiles4_[key[t].second];
+  for (size_t t = 0; t < n; ++t) h_tiles4s_[b][t] = tiles4_[std::get<2>(key[t])];
   OD_CU(cudaMemcpyAsync(d_tiles4s_[b], h_tiles4s_[b], n * sizeof(TileDev),
                         cudaMemcpyHostToDevice, s0_));
   OD_CU(cudaEventRecord(tiles4s_ev_[b], s0_));
@@ -853,6 +938,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
                                                     cfg_.measure == OD_MEASURE_TIMER_RAW));
   r.ev_begin = new_event();
   OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
+  tl_mark(0);
 
   const double* cfield = d_cbase_;
   int32_t shift = shift_ % cfg_.ny;
@@ -958,6 +1044,9 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
   }
 
+  tl_mark(1);
+  const bool slog = d_slog_ && timer && long(st_.steps) == slog_step_;
+  if (slog) slog_arm(true);
   const dim3 blk(kTX, kTY);
   if (timer) {
     r.kev0 = new_event();
@@ -971,6 +1060,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
     OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
+    tl_mark(2);
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
     const int32_t nsend = p2p_ ? n_senders_ : 0;
@@ -984,7 +1074,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       column_step4_persistent<kFusedPrefetch, false, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
           d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
           cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend,
-          stamp, nullptr);
+          stamp, tl_wait());
     OD_CU(cudaGetLastError());
     if (profiling_) {
       e1 = new_event();
@@ -1001,6 +1091,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
     OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
+    tl_mark(2);
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
     const dim3 blk4(kTX, 4);
@@ -1011,12 +1102,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     column_step_persistent<4, kFusedPrefetch, true, MB><<<grid, blk4, 0, s0_>>>(         \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
         cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend,     \
-        stamp, ns + (ns_cols_ - 1));                                                        \
+        stamp, ns + (ns_cols_ - 1));                               \
   else                                                                                      \
     column_step_persistent<4, kFusedPrefetch, false, MB><<<grid, blk4, 0, s0_>>>(        \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
         cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, \
-        stamp, nullptr);
+        stamp, tl_wait());
     if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
@@ -1129,6 +1220,10 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     r.kev1 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev1], s0_));
   }
+  tl_mark(3);
+  if (slog) slog_arm(false);
+  if (timer && ns && tl_wait()) copy_u64<<<1, 1, 0, s0_>>>(tl_wait(), ns + (ns_cols_ - 1));
+  if (d_tl_ && tl_n_ < tl_cap_) ++tl_n_;
   if (host_io && nres > 0) {
     // the step's per-chunk device times back to the host
     OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(nres) * sizeof(unsigned long long),
@@ -1150,6 +1245,7 @@ static double elapsed_s(cudaEvent_t a, cudaEvent_t b) {
 
 void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) {
   OD_CU(cudaStreamSynchronize(s0_));
+  if (trace_on()) tr_drained_ = now_s();
   const int32_t S = int32_t(window_.size());
   const int32_t Kv = K();
   std::vector<unsigned long long> ns;
@@ -1242,7 +1338,9 @@ void Runtime::step_api(int32_t mode, int32_t epoch_step, double* wall, od_sample
 void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
   const auto tb = std::chrono::steady_clock::now();
   std::vector<double> samples;
+  const double tr0 = trace_on() ? now_s() : 0;
   collect(o.walls, samples);
+  const double tr1 = trace_on() ? now_s() : 0;
   SampleStore db(K(), cfg_.async_steps, cfg_.sync_steps);
   for (int32_t s = 0; s < steps; ++s) {
     const int32_t mode = s < cfg_.async_steps ? kAsync : kSync;
@@ -1257,11 +1355,16 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
   o.imb_after = d.imbalance_after;
   o.strategy = d.strategy;
   o.plan = d.plan;
+  const double tr2 = trace_on() ? now_s() : 0;
   if (!o.plan.empty()) {
     const auto t0 = std::chrono::steady_clock::now();
     migrate(o.plan);
     o.mig_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
+  if (trace_on())
+    std::fprintf(stderr, "[od rank %d] epoch %d boundary: collect %.3f ms, decide %.3f ms, "
+                 "migrate %.3f ms (%zu moves)\n", rank_, e, (tr1 - tr0) * 1e3, (tr2 - tr1) * 1e3,
+                 (now_s() - tr2) * 1e3, o.plan.size());
   od_epoch_summary h{};
   h.epoch = e;
   h.strategy = o.strategy;
@@ -1279,13 +1382,24 @@ void Runtime::run_epoch(int32_t e, od_epoch_record* rec) {
   const int32_t S = cfg_.async_steps + cfg_.sync_steps;
   EpochOut o;
   o.map_before = map_;
+  const double tr0 = trace_on() ? now_s() : 0;
   o.classes = classify();
   begin_window();
+  double tr1 = 0;
   for (int32_t s = 0; s < S; ++s) {
     advance_advection(e, s);
     launch_step(s < cfg_.async_steps ? kAsync : kSync, s, false);
+    if (s == 0 && trace_on()) {
+      tr1 = now_s();
+      if (tr_drained_ > 0)
+        std::fprintf(stderr, "[od rank %d] epoch %d: GPU idle between epochs (host) %.3f ms\n",
+                     rank_, e, (tr1 - tr_drained_) * 1e3);
+    }
     ++global_step_;
   }
+  if (trace_on())
+    std::fprintf(stderr, "[od rank %d] epoch %d start: classify+first launch %.3f ms\n", rank_, e,
+                 (tr1 - tr0) * 1e3);
   finish_epoch(e, S, o);
   if (!rec) return;
   rec->epoch = e;
