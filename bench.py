@@ -307,7 +307,10 @@ def main():
         pass
     step_ms = ms / args.steps
     if n_fus > 0:
-        kname, kms, kflops = "column_step3 (fused Jacobi + physics)", fus_ms, phys_flops + jac_flops
+        kname = {5: "column_step_persistent (fused Jacobi + physics)",
+                 6: "column_step4_persistent (fused Jacobi + physics)"}.get(
+                     cfg.overlap, "column_step3 (fused Jacobi + physics)")
+        kms, kflops = fus_ms, phys_flops + jac_flops
     else:
         kname, kms, kflops = "physics_step", phys_ms, phys_flops
     k_tf = kflops / (kms * 1e-3) / 1e12 if kms > 0 else None

@@ -41,9 +41,12 @@ enum { OD_ONE_D = 0, OD_TWO_D = 1 };
 /* per-chunk load measurement in Sync steps */
 enum {
   OD_MEASURE_EVENTS = 0,   /* paper protocol: one launch per chunk, cudaEvent pair */
-  OD_MEASURE_TIMER = 1,    /* batched launch; in-kernel per-chunk SM time apportions the
-                              GPU's event-timed kernel time (per-GPU sums = busy time) */
-  OD_MEASURE_TIMER_RAW = 2 /* batched launch, raw per-chunk SM-time sums */
+  OD_MEASURE_TIMER = 1,    /* batched launch; per-chunk processor-sharing SM time (in-kernel
+                              per-SM clock) apportions the GPU's event-timed kernel time
+                              (per-GPU sums = busy time) */
+  OD_MEASURE_TIMER_RAW = 2, /* batched launch, raw per-chunk SM-time shares */
+  OD_MEASURE_OPS = 3       /* batched launch; in-kernel counted FP64 instructions per chunk
+                              apportion the GPU's kernel time (ignores HBM time) */
 };
 
 /* Move{vp, from, to}                                   cluster.hpp:62-67 */
@@ -206,7 +209,7 @@ typedef struct od_config {
   uint64_t seed;
   /* B200 path parameters (no reference counterpart) */
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
-  int32_t measure;      /* OD_MEASURE_EVENTS | OD_MEASURE_TIMER */
+  int32_t measure;      /* OD_MEASURE_EVENTS | _TIMER | _TIMER_RAW | _OPS */
   int32_t overlap;      /* kernel mode: 0 jacobi_step + physics_step, 4 fused
                            column_step3, 5 persistent fused (default), 6 persistent
                            fused, four columns per thread */

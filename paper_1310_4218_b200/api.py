@@ -73,7 +73,8 @@ class DecompositionKind(enum.IntEnum):  # engine.hpp:18
 class MeasureMode(enum.IntEnum):
     Events = 0    # paper protocol: serialised per-chunk launches, cudaEvent pairs
     Timer = 1     # batched launch, chunk SM-time shares of the GPU's measured kernel time
-    TimerRaw = 2  # batched launch, raw per-chunk SM-time sums
+    TimerRaw = 2  # batched launch, raw per-chunk processor-sharing SM-time shares
+    Ops = 3       # batched launch, kernel time apportioned by counted FP64 instructions
 
 
 def _dptr(a: np.ndarray):

@@ -87,6 +87,7 @@ struct SmShare {
   double v, pad;
 };
 __device__ SmShare g_sm_share[1024];
+__device__ int g_share_min_n = 1;  // OD_SHARE_MIN_N: floor of the divisor (diagnostic)
 // diagnostic event log of the share clock (OD_TILELOG): {time, V, n, tag, sm, delta}
 struct ShareEvent {
   unsigned long long t;
@@ -107,7 +108,7 @@ __device__ __noinline__ double sm_share_update(int delta, int tag) {
   const unsigned long long now = globaltimer_ns();
   double v = vs->v;
   const int n = vs->n;
-  if (n > 0 && now > vs->t_last) v += double(now - vs->t_last) / double(n);
+  if (n > 0 && now > vs->t_last) v += double(now - vs->t_last) / double(n < g_share_min_n ? g_share_min_n : n);
   vs->v = v;
   vs->t_last = now;
   vs->n = n + delta;
@@ -118,6 +119,22 @@ __device__ __noinline__ double sm_share_update(int delta, int tag) {
   __threadfence();
   atomicExch(&s->lock, 0);
   return v;
+}
+
+// Executed FP64 pipe instructions, the work measure that apportions a GPU's
+// measured busy time among its chunks (TIMER): one physics trip is 2*n_inner+3
+// (two FMAs per unit, the trip's y and eb), one Jacobi cell 8 (6 add, mul, fma).
+__device__ __forceinline__ unsigned long long trip_ops(int n_inner) {
+  return 2ull * (unsigned long long)n_inner + 3ull;
+}
+constexpr unsigned long long kJacobiOps = 8;
+
+// chunk_ns rows hold (share ns, executed ops) per slot: add this thread's ops,
+// one atomic per warp.  Every lane of the warp must call it.
+__device__ __forceinline__ void charge_ops(unsigned long long* __restrict__ chunk_ns, int slot,
+                                           unsigned long long ops) {
+  for (int o = 16; o > 0; o >>= 1) ops += __shfl_down_sync(0xffffffffu, ops, o);
+  if ((threadIdx.x & 31) == 0 && ops) atomicAdd(&chunk_ns[2 * slot + 1], ops);
 }
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
@@ -273,9 +290,10 @@ __global__ void __launch_bounds__(TX* TY)
   cp_async_wait<0>();
 
   if (TIMED) {
+    charge_ops(chunk_ns, tile.slot, act ? kJacobiOps * (unsigned long long)nz : 0ull);
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -332,9 +350,10 @@ __global__ void __launch_bounds__(TX* TY)
     if ((threadIdx.x & 31) == 0 && v) atomicAdd(&trips[tile.slot], v);
   }
   if (TIMED) {
+    charge_ops(chunk_ns, tile.slot, (unsigned long long)(T > 0 ? T : 0) * trip_ops(n_inner));
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -624,9 +643,13 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   if (ncell == 2) physics_advance(s1, 0x7fffffff);
 
   if (TIMED) {
+    unsigned long long ops = (unsigned long long)ncell * nz * F * kJacobiOps;
+    if (ncell >= 1) ops += (unsigned long long)s0.T * trip_ops(n_inner);
+    if (ncell == 2) ops += (unsigned long long)s1.T * trip_ops(n_inner);
+    charge_ops(chunk_ns, tile.slot, ops);
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 
@@ -679,8 +702,8 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     const TileDev t = tiles[ti];
     const ChunkDev& c = chunks[t.slot];
     if (t.pad & 1) {
-      // tile reads a strip from another GPU: those tiles come last in the
-      // queue, so the exchange has normally landed while interior tiles ran
+      // tile reads a strip from another GPU: none of those is in the first
+      // wave, so the exchange has normally landed by the time one is taken
       if (lead && !halo_ready) {
         const uint64_t w0 = globaltimer_ns();
         wait_stamps(halo_flags, senders, n_senders, stamp, 20ull * 1000 * 1000 * 1000);
@@ -879,6 +902,7 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
   int quota[4] = {0, 0, 0, 0};
   int64_t off[4];
   const int ncells[4] = {na >= 1, na == 2, nb >= 1, nb == 2};
+  unsigned long long my_ops = 0;  // TIMED: executed FP64 ops of this thread's cells
   off[0] = own_a;
   off[1] = own_a + 1;
   off[2] = own_b;
@@ -894,6 +918,8 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
       T = int(floor(__dmul_rn(double(nz), cm))) - 1;
       if (T < 0) T = 0;
       chain_init(ch[j], Bb + off[j], Ab + off[j], T, nz, ks);
+      if (TIMED) my_ops += (unsigned long long)T * trip_ops(n_inner) +
+                           (unsigned long long)nz * F * kJacobiOps;
       quota[j] = int((int64_t(T) * (n_inner + 1) + levels - 1) / levels);
       quota[j] = (quota[j] + 7) & ~7;
     } else {
@@ -1012,9 +1038,10 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
     if (ncells[j]) chain_advance(ch[j], 0x7fffffff, Bb + off[j], Ab + off[j], nz, ks, n_inner);
 
   if (TIMED) {
+    charge_ops(chunk_ns, tile.slot, my_ops);
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
   }
 }
 

@@ -183,7 +183,14 @@ class Runtime {
   bool order_dirty_ = true;
   int persist_grid_ = 0;
   int persist_minb_ = 5;
+  int sms_ = 1;
   void refresh_tile_order();
+  // host caches keyed on the load-field generation (set_shift bumps it)
+  uint64_t field_gen_ = 0;
+  std::vector<std::vector<double>> tile_work_;  // per vp, per tile of the chunk
+  std::vector<uint64_t> tile_work_gen_;
+  mutable std::vector<int32_t> classes_;
+  mutable uint64_t classes_gen_ = ~0ull;
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
   size_t d_chunks_cap_[2] = {0, 0};
   TileDev* d_tiles_ = nullptr;
@@ -279,7 +286,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 6))
     throw ValidationError("unknown kernel mode (overlap): 0, 4, 5 or 6");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER &&
-      cfg.measure != OD_MEASURE_TIMER_RAW)
+      cfg.measure != OD_MEASURE_TIMER_RAW && cfg.measure != OD_MEASURE_OPS)
     throw ValidationError("unknown measurement mode");
   if (world != cfg.nodes)
     throw ValidationError("one rank per node GPU: world size must equal cluster.nodes");
@@ -297,6 +304,10 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
 
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
+  if (const char* mn = std::getenv("OD_SHARE_MIN_N")) {
+    const int v = std::max(1, std::atoi(mn));
+    OD_CU(cudaMemcpyToSymbol(g_share_min_n, &v, sizeof(v)));
+  }
   if (std::getenv("OD_TILELOG")) {
     slog_cap_ = 1u << 20;
     slog_step_ = std::getenv("OD_TILELOG_STEP") ? std::atol(std::getenv("OD_TILELOG_STEP")) : 19;
@@ -310,6 +321,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
   {
     int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
+    sms_ = sms;
     const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
     phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
     OD_CU(cudaMalloc(&d_counter_, sizeof(unsigned int)));
@@ -337,6 +349,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &per_sm, column_step4_persistent<kFusedPrefetch, false, 4>, kTX * 4, 0));
     }
+    if (const char* pc = std::getenv("OD_PERSIST_CTAS")) per_sm = std::min(per_sm, std::atoi(pc));
     persist_grid_ = sms * std::max(per_sm, 1);
   }
   if (world_ > 1) {
@@ -489,6 +502,7 @@ int32_t Runtime::nbr(int32_t v, int d) const {
 void Runtime::set_shift(int32_t rows) {
   shift_ = rows;
   field_ = shift_rows_down(base_, rows % cfg_.ny);
+  ++field_gen_;
   order_dirty_ = true;
 }
 
@@ -505,23 +519,59 @@ void Runtime::refresh_tile_order() {
   static const bool chunk_major = std::getenv("OD_TILE_ORDER") &&
                                   std::string(std::getenv("OD_TILE_ORDER")) == "chunk";
   const double jac = 2.0 * cfg_.nz * cfg_.fields;  // a Jacobi cell ~ 2 micro-steps
+  if (tile_work_.size() != size_t(K())) {
+    tile_work_.assign(K(), {});
+    tile_work_gen_.assign(K(), ~0ull);
+  }
   for (size_t t = 0; t < n; ++t) {
     const TileDev& td = tiles4_[t];
-    const Sub& s = subs_[resident_[td.slot]];
-    const int32_t x0 = s.x0 + td.tx0, x1 = std::min(s.x1, x0 + 2 * kTX);
-    const int32_t y0 = s.y0 + td.ty0, y1 = std::min(s.y1, y0 + kTY4);
-    double w = 0;
-    for (int32_t y = y0; y < y1; ++y)
-      for (int32_t x = x0; x < x1; ++x) {
-        const int32_t T = int32_t(std::floor(double(cfg_.nz) * field_.at(x, y))) - 1;
-        w += double(T > 0 ? T : 0) * (cfg_.n_inner + 1) + jac;
+    const int32_t vp = resident_[td.slot];
+    const size_t local = t - size_t(tile4_begin_[td.slot]);
+    if (tile_work_gen_[vp] != field_gen_) {
+      // the work of every tile of this chunk under the current load field
+      tile_work_gen_[vp] = field_gen_;
+      auto& tw = tile_work_[vp];
+      tw.assign(size_t(tile4_count_[td.slot]), 0.0);
+      const Sub& s = subs_[vp];
+      for (int32_t j = 0; j < tile4_count_[td.slot]; ++j) {
+        const TileDev& tj = tiles4_[tile4_begin_[td.slot] + j];
+        const int32_t x0 = s.x0 + tj.tx0, x1 = std::min(s.x1, x0 + 2 * kTX);
+        const int32_t y0 = s.y0 + tj.ty0, y1 = std::min(s.y1, y0 + kTY4);
+        double w = 0;
+        for (int32_t y = y0; y < y1; ++y)
+          for (int32_t x = x0; x < x1; ++x) {
+            const int32_t T = int32_t(std::floor(double(cfg_.nz) * field_.at(x, y))) - 1;
+            w += double(T > 0 ? T : 0) * (cfg_.n_inner + 1) + jac;
+          }
+        tw[j] = w;
       }
-    // tiles that read strips from other GPUs go last (their data arrives while
-    // the interior runs); heaviest first within each group
-    key[t] = {(td.pad & 1 ? 1e300 : 0.0) - w,
-              chunk_major ? 0 : int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
+    }
+    const double w = tile_work_[vp][local];
+    key[t] = {-w, chunk_major ? 0 : int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
   }
   std::sort(key.begin(), key.end());
+  static const bool boundary_last = std::getenv("OD_BOUNDARY_LAST") != nullptr;
+  static const bool first_wave_interior =
+      !(std::getenv("OD_FIRSTWAVE") && std::string(std::getenv("OD_FIRSTWAVE")) == "0");
+  if (p2p_ && n_senders_ > 0 && boundary_last) {
+    std::stable_sort(key.begin(), key.end(), [&](const auto& a, const auto& b) {
+      return (tiles4_[std::get<2>(a)].pad & 1) < (tiles4_[std::get<2>(b)].pad & 1);
+    });
+  } else if (p2p_ && n_senders_ > 0 && first_wave_interior) {
+    // with peer-memory halos the neighbours' strips of this step land while the
+    // kernel runs: the first wave (one tile per CTA) takes the heaviest tiles
+    // that read no remote strip; everything after it stays in heaviest-first
+    // order (deferring all boundary tiles to the end would put heavy migrated
+    // chunks -- typically boundary after a rebalance -- into the tail)
+    std::vector<std::tuple<double, int32_t, int32_t>> front, rest;
+    front.reserve(n);
+    rest.reserve(n);
+    for (const auto& k : key)
+      (front.size() < size_t(persist_grid_) && !(tiles4_[std::get<2>(k)].pad & 1) ? front : rest)
+          .push_back(k);
+    front.insert(front.end(), rest.begin(), rest.end());
+    key.swap(front);
+  }
   const int b = tiles4s_cur_ ^ 1;
   OD_CU(cudaEventSynchronize(tiles4s_ev_[b]));  // previous upload from this buffer done
   for (size_t t = 0; t < n; ++t) h_tiles4s_[b][t] = tiles4_[std::get<2>(key[t])];
@@ -547,9 +597,12 @@ void Runtime::advance_advection(int32_t epoch, int32_t step) {
 
 // engine.hpp:281-287
 std::vector<int32_t> Runtime::classify() const {
+  if (classes_gen_ == field_gen_) return classes_;
   const double mid = 0.5 * (cfg_.heavy_value + cfg_.light_value);
   std::vector<int32_t> out(K());
   for (int32_t v = 0; v < K(); ++v) out[v] = field_.mean_over(subs_[v]) > mid ? kHeavy : kLight;
+  classes_ = out;
+  classes_gen_ = field_gen_;
   return out;
 }
 
@@ -831,9 +884,10 @@ void Runtime::rebuild_tables() {
     }
     upload(d_chunks_[par], d_chunks_cap_[par], tab);
   }
-  if (!d_trips_ || ns_cols_ < nres) {
-    // last column: the longest in-kernel wait for remote halos (per step)
-    ns_cols_ = std::max(std::max(nres, 1), int(slab_slots_)) + 1;
+  if (!d_trips_ || ns_cols_ < 2 * nres + 1) {
+    // per slot (SM-time share ns, executed FP64 ops); last column: the longest
+    // in-kernel wait for remote halos (per step)
+    ns_cols_ = 2 * std::max(std::max(nres, 1), int(slab_slots_)) + 1;
     cudaFree(d_trips_);
     OD_CU(cudaMalloc(&d_trips_, size_t(ns_cols_) * sizeof(unsigned long long)));
     cudaFree(d_ns_);
@@ -935,7 +989,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   const int par = parity_;
   const int32_t nres = int32_t(resident_.size());
   const bool timer = host_io || (mode == kSync && (cfg_.measure == OD_MEASURE_TIMER ||
-                                                    cfg_.measure == OD_MEASURE_TIMER_RAW));
+                                                    cfg_.measure == OD_MEASURE_TIMER_RAW ||
+                                                    cfg_.measure == OD_MEASURE_OPS));
   r.ev_begin = new_event();
   OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
   tl_mark(0);
@@ -1226,7 +1281,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   if (d_tl_ && tl_n_ < tl_cap_) ++tl_n_;
   if (host_io && nres > 0) {
     // the step's per-chunk device times back to the host
-    OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(nres) * sizeof(unsigned long long),
+    OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(2 * nres) * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s0_));
   }
   r.ev_end = new_event();
@@ -1260,20 +1315,29 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
   for (int32_t s = 0; s < S; ++s) {
     const StepRec& r = window_[s];
     local[size_t(S) * Kv + s] = elapsed_s(events_[r.ev_begin], events_[r.ev_end]);
+    // TIMER: the chunk's processor-sharing SM time (sum over its tiles of
+    // integral dt / resident CTAs on the tile's SM) divided by the SM count, in
+    // seconds of the whole GPU.  A GPU's samples sum to its mean SM busy time;
+    // CTAs spinning on a peer's halo are not resident in a tile, so time a GPU
+    // idles for its neighbours is charged to nobody.  TIMER_RAW: the same shares
+    // in SM-seconds.  OPS: the event-timed kernel time minus the longest
+    // in-kernel halo wait, apportioned by the FP64 instructions each chunk
+    // executed (ignores the Jacobi's HBM time).
+    const bool by_ops = cfg_.measure == OD_MEASURE_OPS && r.kev0 >= 0;
+    double sum = 0, kt = 0;
+    if (r.ns_row >= 0 && r.mode == kSync && by_ops) {
+      for (size_t j = 0; j < r.slot_vps.size(); ++j)
+        sum += double(ns[size_t(r.ns_row) * ns_cols_ + 2 * j + 1]);
+      const double wait = double(ns[size_t(r.ns_row) * ns_cols_ + (ns_cols_ - 1)]) * 1e-9;
+      kt = std::max(0.0, elapsed_s(events_[r.kev0], events_[r.kev1]) - wait);
+    }
     for (size_t i = 0; i < r.slot_vps.size(); ++i) {
       double v;
       if (r.ns_row >= 0 && r.mode == kSync) {
-        v = double(ns[size_t(r.ns_row) * ns_cols_ + i]) * 1e-9;
-        if (cfg_.measure == OD_MEASURE_TIMER && r.kev0 >= 0) {
-          // the chunk's SM-time share of this GPU's measured kernel time, so the
-          // per-GPU sums are the GPUs' real busy times
-          double sum = 0;
-          for (size_t j = 0; j < r.slot_vps.size(); ++j)
-            sum += double(ns[size_t(r.ns_row) * ns_cols_ + j]);
-          const double wait = double(ns[size_t(r.ns_row) * ns_cols_ + (ns_cols_ - 1)]) * 1e-9;
-          const double kt = std::max(0.0, elapsed_s(events_[r.kev0], events_[r.kev1]) - wait);
-          v = sum > 0 ? double(ns[size_t(r.ns_row) * ns_cols_ + i]) / sum * kt : 0.0;
-        }
+        v = double(ns[size_t(r.ns_row) * ns_cols_ + 2 * i]) * 1e-9;
+        if (cfg_.measure == OD_MEASURE_TIMER) v /= double(sms_);
+        if (by_ops)
+          v = sum > 0 ? double(ns[size_t(r.ns_row) * ns_cols_ + 2 * i + 1]) / sum * kt : 0.0;
       }
       else if (r.mode == kSync && r.chunk_ev0 >= 0)
         v = elapsed_s(events_[r.chunk_ev0 + 2 * i], events_[r.chunk_ev0 + 2 * i + 1]);
@@ -1450,7 +1514,7 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
   if (!h_cstage_) {
     OD_CU(cudaMallocHost(&h_cstage_, cells * sizeof(double)));
     OD_CU(cudaMalloc(&d_cstage_, cells * sizeof(double)));
-    OD_CU(cudaMallocHost(&h_loads_, std::max<size_t>(K(), 1) * sizeof(unsigned long long)));
+    OD_CU(cudaMallocHost(&h_loads_, 2 * std::max<size_t>(K(), 1) * sizeof(unsigned long long)));
   }
   if (host_c && n_fields > 0) {
     // the caller's load multiplier field replaces the base field
@@ -1468,7 +1532,7 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
       double* row = host_loads + size_t(i) * K();
       std::fill(row, row + K(), 0.0);
       const auto& vps = window_.back().slot_vps;
-      for (size_t j = 0; j < vps.size(); ++j) row[vps[j]] = double(h_loads_[j]) * 1e-9;
+      for (size_t j = 0; j < vps.size(); ++j) row[vps[j]] = double(h_loads_[2 * j]) * 1e-9;
     }
     ++global_step_;
     if (++cur_step_ == S) {

@@ -33,6 +33,8 @@ obj = [od.nccl_unique_id() if rank == 0 else None]
 if world > 1:
     dist.broadcast_object_list(obj, src=0)
 cfg = configs.cfg4(world, overlap=mode)
+if len(sys.argv) > 3:
+    cfg = cfg.replace(measure=od.MeasureMode(int(sys.argv[3])))
 if not lb:
     import dataclasses
     cfg = cfg.replace(policy=dataclasses.replace(cfg.policy, trigger_threshold=1e9))
