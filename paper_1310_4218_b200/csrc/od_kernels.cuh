@@ -161,6 +161,25 @@ __device__ __forceinline__ void wait_stamps(const unsigned long long* __restrict
   }
 }
 
+// Peer-halo dependency of one tile (persistent kernels, P2P halos): the
+// senders' step flags to poll; n == 0 when the tile needs nothing remote or the
+// strips are known to have landed.
+constexpr int kPreroll = 256;  // physics units per pre-roll round (multiple of 16)
+
+struct HaloWait {
+  const unsigned long long* flags;
+  const int32_t* senders;
+  int32_t n;
+  unsigned long long stamp;
+  unsigned long long* wait_ns;  // longest pre-roll (diagnostic), may be null
+};
+
+__device__ __forceinline__ bool stamps_ready(const HaloWait& hw) {
+  for (int i = 0; i < hw.n; ++i)
+    if (ld_acquire_sys(hw.flags + hw.senders[i]) < hw.stamp) return false;
+  return true;
+}
+
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
@@ -467,7 +486,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
                                           const ChunkDev* __restrict__ chunks, int32_t nz,
                                           int32_t F, const double* __restrict__ cfield,
                                           int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
-                                          unsigned long long* __restrict__ chunk_ns) {
+                                          unsigned long long* __restrict__ chunk_ns,
+                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr}) {
   constexpr int R = 8;
   constexpr int TXC = 64;
   constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
@@ -618,6 +638,35 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     pout += ks;
   };
 
+  if (hw.n > 0) {
+    // The tile reads strips a peer GPU stores into this GPU's receive buffer
+    // during this step.  Until they have landed, run the tile's physics (which
+    // reads only this GPU's U^t): the wait costs the SM nothing while the
+    // physics lasts, so such tiles can sit anywhere in the heaviest-first queue.
+    const uint64_t w0 = globaltimer_ns();
+    const int64_t need = int64_t(max(ncell >= 1 ? s0.T : 0, ncell == 2 ? s1.T : 0)) * (n_inner + 1);
+    int64_t done = 0;
+    bool lead_ready = false;
+    for (;;) {
+      const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+      if (lead) {
+        if (done >= need) {
+          // physics exhausted before the strips came: block (traps on a dead peer)
+          wait_stamps(hw.flags, hw.senders, hw.n, hw.stamp, 20ull * 1000 * 1000 * 1000);
+          lead_ready = true;
+        } else {
+          lead_ready = stamps_ready(hw);
+        }
+      }
+      if (__syncthreads_or(lead && lead_ready)) break;
+      physics(kPreroll, kPreroll);
+      done += kPreroll;
+    }
+    fast = 0;  // the level loop's budgets differ from the pre-roll's
+    if (hw.wait_ns && threadIdx.x == 0 && threadIdx.y == 0)
+      atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+  }
+
 #pragma unroll
   for (int L = 0; L < S; ++L) issue(L);
 
@@ -671,9 +720,10 @@ __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const 
                                                int32_t F, const double* __restrict__ cfield,
                                                int32_t nx, int32_t ny, int32_t shift,
                                                int32_t n_inner,
-                                               unsigned long long* __restrict__ chunk_ns) {
+                                               unsigned long long* __restrict__ chunk_ns,
+                                               const HaloWait hw) {
   tile_step<TY, S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                 chunk_ns);
+                                 chunk_ns, hw);
 }
 
 // Persistent variant: a fixed grid (one wave) pulls tiles, heaviest first,
@@ -701,24 +751,17 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     if (ti >= ntiles) break;
     const TileDev t = tiles[ti];
     const ChunkDev& c = chunks[t.slot];
-    if (t.pad & 1) {
-      // tile reads a strip from another GPU: none of those is in the first
-      // wave, so the exchange has normally landed by the time one is taken
-      if (lead && !halo_ready) {
-        const uint64_t w0 = globaltimer_ns();
-        wait_stamps(halo_flags, senders, n_senders, stamp, 20ull * 1000 * 1000 * 1000);
-        // time this SM idled for the neighbours (kept out of the load measurement)
-        if (wait_ns) atomicMax(wait_ns, (unsigned long long)(globaltimer_ns() - w0));
-        halo_ready = true;
-      }
-      __syncthreads();
-    }
+    // a tile reading a strip from another GPU before this CTA has seen the
+    // strips land pre-rolls its physics while polling (tile_step)
+    const bool poll = __syncthreads_or(lead && (t.pad & 1) && !halo_ready);
+    const HaloWait hw{halo_flags, senders, poll ? n_senders : 0, stamp, wait_ns};
     if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
       tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                    chunk_ns);
+                                    chunk_ns, hw);
     else
       tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                      chunk_ns);
+                                      chunk_ns, hw);
+    if (poll) halo_ready = true;
   }
 }
 

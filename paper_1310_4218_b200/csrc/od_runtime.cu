@@ -550,7 +550,29 @@ void Runtime::refresh_tile_order() {
     key[t] = {-w, chunk_major ? 0 : int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
   }
   std::sort(key.begin(), key.end());
+  // diagnostic order variants (OD_ORDER): spt = lightest first; lightwave =
+  // the lightest tiles form the first wave, then heaviest first; shuffle
+  if (const char* ov = std::getenv("OD_ORDER")) {
+    const std::string o(ov);
+    if (o == "spt") {
+      std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) {
+        return std::get<0>(a) > std::get<0>(b);
+      });
+    } else if (o == "lightwave") {
+      const size_t g = std::min(n, size_t(persist_grid_));
+      std::rotate(key.begin(), key.end() - g, key.end());
+    } else if (o == "shuffle") {
+      uint64_t st = 12345;
+      for (size_t i = n; i > 1; --i) {
+        st = mix64(st);
+        std::swap(key[i - 1], key[st % i]);
+      }
+    }
+  }
   static const bool boundary_last = std::getenv("OD_BOUNDARY_LAST") != nullptr;
+  // OD_FIRSTWAVE=0: plain heaviest-first (boundary tiles in the first wave
+  // pre-roll their physics until the strips land); measured 5-7 % slower at 4
+  // GPUs on cfg4 than keeping them out of the first wave
   static const bool first_wave_interior =
       !(std::getenv("OD_FIRSTWAVE") && std::string(std::getenv("OD_FIRSTWAVE")) == "0");
   if (p2p_ && n_senders_ > 0 && boundary_last) {
