@@ -726,6 +726,61 @@ __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const 
                                  chunk_ns, hw);
 }
 
+// Halo pack fused into the persistent kernel (P2P halos): the first `ctas`
+// CTAs store this step's boundary strips straight into the peers' receive
+// buffers over NVLink, one (face, field) unit at a time, before they join the
+// tile queue; the other CTAs start on tiles at once, so the NVLink transfer
+// overlaps the compute.  The CTA that completes the last unit publishes the
+// step to the peers (same protocol as pack_faces_p2p).
+struct PackArgs {
+  const PackJob* jobs;
+  int32_t njobs, ctas;
+  double* const* peer_base;
+  int64_t half_elems;
+  int32_t par, n_notify, my_rank, pad;
+  unsigned int* counters;  // [next unit, units done], zeroed before the launch
+  unsigned long long* const* peer_flags;
+  const int32_t* notify;
+};
+
+__device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __restrict__ chunks,
+                                        int32_t nz, int32_t F, unsigned long long stamp) {
+  __shared__ int s_unit;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
+  const int total = pk.njobs * F;
+  for (;;) {
+    if (lead) s_unit = int(atomicAdd(&pk.counters[0], 1u));
+    __syncthreads();
+    const int u = s_unit;
+    __syncthreads();
+    if (u >= total) break;
+    const PackJob j = pk.jobs[u / F];
+    const int f = u - (u / F) * F;
+    const ChunkDev& c = chunks[j.slot];
+    const double* base = c.in + f * c.fstride;
+    int64_t off = 0, es = 1;
+    switch (j.side) {
+      case kLeft: off = 0; es = c.pitch; break;
+      case kRight: off = c.w - 1; es = c.pitch; break;
+      case kTop: off = 0; es = 1; break;
+      default: off = int64_t(c.h - 1) * c.pitch; es = 1; break;
+    }
+    double* out = pk.peer_base[j.peer] + int64_t(pk.par) * pk.half_elems + j.rdst +
+                  int64_t(f) * nz * j.lenp;
+    for (int k = 0; k < nz; ++k)
+      for (int e = tid; e < j.len; e += nthr)
+        out[int64_t(k) * j.lenp + e] = base[off + k * c.kstride + e * es];
+    __threadfence_system();
+    __syncthreads();
+    if (lead && atomicAdd(&pk.counters[1], 1u) == unsigned(total - 1)) {
+      __threadfence_system();
+      for (int i = 0; i < pk.n_notify; ++i)
+        st_release_sys(pk.peer_flags[pk.notify[i]] + pk.my_rank, stamp);
+    }
+  }
+}
+
 // Persistent variant: a fixed grid (one wave) pulls tiles, heaviest first,
 // from a counter, so the per-GPU time follows the work even when the GPU holds
 // few tiles (strong scaling) and heavy tiles do not end up in a ragged tail.
@@ -738,11 +793,13 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                            unsigned long long* __restrict__ chunk_ns,
                            const unsigned long long* __restrict__ halo_flags,
                            const int32_t* __restrict__ senders, int32_t n_senders,
-                           unsigned long long stamp, unsigned long long* __restrict__ wait_ns) {
+                           unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
+                           const PackArgs pk) {
   __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
   __shared__ int s_next;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   bool halo_ready = n_senders == 0;  // meaningful in the lead thread only
+  if (pk.njobs > 0 && int(blockIdx.x) < pk.ctas) pack_units(pk, chunks, nz, F, stamp);
   for (;;) {
     if (lead) s_next = int(atomicAdd(counter, 1u));
     __syncthreads();

@@ -184,6 +184,7 @@ class Runtime {
   int persist_grid_ = 0;
   int persist_minb_ = 5;
   int sms_ = 1;
+  int pack_ctas_ = 0;  // CTAs of the persistent kernel that pack P2P halos (0: separate kernel)
   void refresh_tile_order();
   // host caches keyed on the load-field generation (set_shift bumps it)
   uint64_t field_gen_ = 0;
@@ -322,9 +323,10 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     sms_ = sms;
+    pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
     phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
-    OD_CU(cudaMalloc(&d_counter_, sizeof(unsigned int)));
+    OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
     // Concurrent kernels can share an SM only with the same L1/smem split:
     // give the co-scheduled kernels one carveout so the Jacobi CTAs fit next
     // to the persistent physics CTAs.
@@ -1049,6 +1051,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   // boundaries of chunks that border another GPU
+  const bool fused_pack = p2p_ && pack_ctas_ > 0 && cfg_.overlap == 5 && !tiles4_.empty() &&
+                          (mode == kAsync || timer);
   if (p2p_ && (!jobs_.empty() || n_senders_ > 0)) {
     // pack straight into the neighbours' receive buffers over NVLink, publish
     // the step, then wait for the neighbours' strips of this step
@@ -1058,7 +1062,10 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
     const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
-    if (!jobs_.empty()) {
+    if (!jobs_.empty() && fused_pack) {
+      // packed by the persistent kernel's first CTAs (pack_units)
+      for (int q = 0; q < world_; ++q) st_.halo_bytes_sent += send_cnt_[q] * int64_t(sizeof(double));
+    } else if (!jobs_.empty()) {
       pack_faces_p2p<<<dim3(unsigned(jobs_.size()), unsigned(cfg_.fields)), 256, 0, s0_>>>(
           d_chunks_[par], d_jobs_, d_peer_base_, recv_half_, par, cfg_.nz, d_pack_counter_,
           d_peer_flags_, d_notify_, n_notify_, rank_, stamp);
@@ -1167,11 +1174,25 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       e0 = new_event();
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
-    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
+    OD_CU(cudaMemsetAsync(d_counter_, 0, 3 * sizeof(unsigned int), s0_));
     tl_mark(2);
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
     const dim3 blk4(kTX, 4);
+    PackArgs pk{};
+    if (fused_pack && !jobs_.empty()) {
+      pk.jobs = d_jobs_;
+      pk.njobs = int32_t(jobs_.size());
+      pk.ctas = std::min(pack_ctas_, grid);
+      pk.peer_base = d_peer_base_;
+      pk.half_elems = recv_half_;
+      pk.par = par;
+      pk.n_notify = n_notify_;
+      pk.my_rank = rank_;
+      pk.counters = d_counter_ + 1;
+      pk.peer_flags = d_peer_flags_;
+      pk.notify = d_notify_;
+    }
     const int32_t nsend = p2p_ ? n_senders_ : 0;
     const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
 #define OD_LAUNCH_PS(MB)                                                                    \
@@ -1179,12 +1200,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     column_step_persistent<4, kFusedPrefetch, true, MB><<<grid, blk4, 0, s0_>>>(         \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
         cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend,     \
-        stamp, ns + (ns_cols_ - 1));                               \
+        stamp, ns + (ns_cols_ - 1), pk);                           \
   else                                                                                      \
     column_step_persistent<4, kFusedPrefetch, false, MB><<<grid, blk4, 0, s0_>>>(        \
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
         cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, \
-        stamp, tl_wait());
+        stamp, tl_wait(), pk);
     if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
