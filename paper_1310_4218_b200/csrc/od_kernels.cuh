@@ -643,7 +643,6 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     // during this step.  Until they have landed, run the tile's physics (which
     // reads only this GPU's U^t): the wait costs the SM nothing while the
     // physics lasts, so such tiles can sit anywhere in the heaviest-first queue.
-    const uint64_t w0 = globaltimer_ns();
     const int64_t need = int64_t(max(ncell >= 1 ? s0.T : 0, ncell == 2 ? s1.T : 0)) * (n_inner + 1);
     int64_t done = 0;
     bool lead_ready = false;
@@ -651,8 +650,11 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
       if (lead) {
         if (done >= need) {
-          // physics exhausted before the strips came: block (traps on a dead peer)
+          // physics exhausted before the strips came: block (traps on a dead
+          // peer); the longest such idle is kept out of the load measurement
+          const uint64_t w0 = globaltimer_ns();
           wait_stamps(hw.flags, hw.senders, hw.n, hw.stamp, 20ull * 1000 * 1000 * 1000);
+          if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
           lead_ready = true;
         } else {
           lead_ready = stamps_ready(hw);
@@ -663,8 +665,6 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       done += kPreroll;
     }
     fast = 0;  // the level loop's budgets differ from the pre-roll's
-    if (hw.wait_ns && threadIdx.x == 0 && threadIdx.y == 0)
-      atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
   }
 
 #pragma unroll
@@ -737,7 +737,7 @@ struct PackArgs {
   int32_t njobs, ctas;
   double* const* peer_base;
   int64_t half_elems;
-  int32_t par, n_notify, my_rank, pad;
+  int32_t par, n_notify, my_rank, first;  // first: lowest blockIdx that packs
   unsigned int* counters;  // [next unit, units done], zeroed before the launch
   unsigned long long* const* peer_flags;
   const int32_t* notify;
@@ -799,7 +799,8 @@ __global__ void __launch_bounds__(32 * TY, MINB)
   __shared__ int s_next;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   bool halo_ready = n_senders == 0;  // meaningful in the lead thread only
-  if (pk.njobs > 0 && int(blockIdx.x) < pk.ctas) pack_units(pk, chunks, nz, F, stamp);
+  if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
+    pack_units(pk, chunks, nz, F, stamp);
   for (;;) {
     if (lead) s_next = int(atomicAdd(counter, 1u));
     __syncthreads();
@@ -820,6 +821,36 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                                       chunk_ns, hw);
     if (poll) halo_ready = true;
   }
+}
+
+// One CTA per tile over the heaviest-first tile list.  The block scheduler
+// starts CTAs in index order as earlier ones retire, and the warp scheduler
+// favours older warps, so tiles are served roughly first-come-first-served: an
+// early (heavy) tile is never starved behind a stream of later tiles the way a
+// young CTA of the persistent kernel is (its oldest CTAs keep the pipe while
+// they pull tile after tile).  Same tile body, halo pre-roll and fused pack.
+template <int TY, int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(32 * TY, MINB)
+    column_step_grid(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                     int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
+                     int32_t ny, int32_t shift, int32_t n_inner,
+                     unsigned long long* __restrict__ chunk_ns,
+                     const unsigned long long* __restrict__ halo_flags,
+                     const int32_t* __restrict__ senders, int32_t n_senders,
+                     unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
+                     const PackArgs pk) {
+  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
+  if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
+    pack_units(pk, chunks, nz, F, stamp);
+  const TileDev t = tiles[blockIdx.x];
+  const ChunkDev& c = chunks[t.slot];
+  const HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns};
+  if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
+    tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                  chunk_ns, hw);
+  else
+    tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                    chunk_ns, hw);
 }
 
 // ---------------------------------------------------------------------------

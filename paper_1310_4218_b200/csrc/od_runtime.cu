@@ -184,7 +184,8 @@ class Runtime {
   int persist_grid_ = 0;
   int persist_minb_ = 5;
   int sms_ = 1;
-  int pack_ctas_ = 0;  // CTAs of the persistent kernel that pack P2P halos (0: separate kernel)
+  int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
+  bool grid_launch_ = true;  // mode 5 as one CTA per tile (column_step_grid)
   void refresh_tile_order();
   // host caches keyed on the load-field generation (set_shift bumps it)
   uint64_t field_gen_ = 0;
@@ -323,6 +324,9 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     sms_ = sms;
+    // mode 5 launches one CTA per tile (column_step_grid) unless OD_GRID=0
+    // selects the persistent tile-pulling kernel (column_step_persistent)
+    grid_launch_ = !(std::getenv("OD_GRID") && std::string(std::getenv("OD_GRID")) == "0");
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
     phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
@@ -1206,7 +1210,21 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
         d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
         cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, \
         stamp, tl_wait(), pk);
-    if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
+    if (grid_launch_) {
+      // one CTA per tile, heaviest first; the fused pack rides on the last
+      // CTAs of the first wave (the lightest tiles of it)
+      if (pk.njobs > 0) pk.first = std::max(0, std::min(nt, persist_grid_) - pk.ctas);
+      if (timer)
+        column_step_grid<4, kFusedPrefetch, true, 5><<<nt, blk4, 0, s0_>>>(
+            d_chunks_[par], d_tiles4s_[tiles4s_cur_], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend, stamp,
+            ns + (ns_cols_ - 1), pk);
+      else
+        column_step_grid<4, kFusedPrefetch, false, 5><<<nt, blk4, 0, s0_>>>(
+            d_chunks_[par], d_tiles4s_[tiles4s_cur_], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
+            cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, stamp,
+            tl_wait(), pk);
+    } else if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
     if (profiling_) {

@@ -54,8 +54,10 @@ if rank == 0:
             nb = [(ix - 1, iy), (ix + 1, iy), (ix, iy - 1), (ix, iy + 1)]
             remote = sum(1 for (a, b) in nb if 0 <= a < kx and 0 <= b < ky and m[b * kx + a] != m[v])
             out.setdefault((int(m[v]), "H" if heavy else "L", remote), []).append(L[v])
+        import hashlib
         print("epoch", r.epoch, "imb", round(r.imbalance_before, 4), "->", round(r.imbalance_after, 4),
-              "moves", len(r.plan.moves))
+              "moves", len(r.plan.moves), "map", hashlib.md5(bytes(m.astype(np.int8))).hexdigest()[:8],
+              "plan", [tuple(x) for x in r.plan.moves][:30])
         if world == 1 and r.epoch == 2:
             Lh = L[: len(L) // 2].reshape(ky // 2, kx)
             print("heavy chunk loads (ms), rows of the chunk grid:")
@@ -94,6 +96,9 @@ if rank == 0:
                           "gap_ms_max": round(float(gap.max()), 3),
                           "step_ms_median": round(float(np.median(step)), 4),
                           "total_ms": round(float((t[-1, 3] - t[0, 0]) / 1e6), 3)}))
+    # per-epoch median kernel ms per rank
+    for e in range(n // 10):
+        print("epoch-kernels", e + 1, " ".join("%.3f" % np.median((rows[r][10 * e:10 * e + 10, 3] - rows[r][10 * e:10 * e + 10, 2]) / 1e6) for r in range(world)))
     # per-step detail for the last epoch
     for s in range(n - 10, n):
         print("step", s, " ".join(f"{(rows[r][s, 3] - rows[r][s, 2]) / 1e6:.3f}/w{rows[r][s, 4] / 1e6:.3f}"
