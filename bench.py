@@ -307,7 +307,9 @@ def main():
         pass
     step_ms = ms / args.steps
     if n_fus > 0:
-        kname = {5: "column_step_persistent (fused Jacobi + physics)",
+        grid5 = os.environ.get("OD_GRID", "1") != "0"
+        kname = {5: ("column_step_grid (fused Jacobi + physics, one CTA per tile)" if grid5
+                     else "column_step_persistent (fused Jacobi + physics)"),
                  6: "column_step4_persistent (fused Jacobi + physics)"}.get(
                      cfg.overlap, "column_step3 (fused Jacobi + physics)")
         kms, kflops = fus_ms, phys_flops + jac_flops
@@ -357,7 +359,7 @@ def main():
         ms_e2e = timed(lambda: eng.advance_host(args.steps, None, loads))
         e2e = {"value": cols * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": cols * 8,
-               "d2h_bytes_per_step": int(st1["resident_chunks"]) * 8}
+               "d2h_bytes_per_step": int(st1["resident_chunks"]) * 16}
     eng.close()
     del eng
 

@@ -152,9 +152,16 @@ class Runtime {
   int phys_ctas_ = 0;               // persistent physics grid
   ncclComm_t comm_ = nullptr;
   double* d_cbase_ = nullptr;   // base load field (device copy)
-  double* d_cstage_ = nullptr;  // host-staged shifted field (host_io path)
-  double* h_cstage_ = nullptr;  // pinned
-  unsigned long long* h_loads_ = nullptr;  // pinned, per-step chunk ns (host_io path)
+  // host_io path: the shifted field staged from pinned host memory every step
+  // (double-buffered so the host fills one while the other is in flight) and
+  // each step's per-chunk shares read back into a pinned row of h_loads_
+  double* d_cstage_[2] = {nullptr, nullptr};
+  double* h_cstage_[2] = {nullptr, nullptr};
+  cudaEvent_t cstage_ev_[2] = {nullptr, nullptr};
+  int cstage_cur_ = 0;
+  unsigned long long* h_loads_ = nullptr;  // pinned [rows][2 * K]
+  size_t h_loads_rows_ = 0;
+  unsigned long long* h_loads_dst_ = nullptr;  // row for the step being launched
   std::vector<ChunkMem> chunks_;  // indexed by vp; base == nullptr if not local
   std::multimap<size_t, double*> pool_;  // individually allocated (fallback) buffers
   double* slab_ = nullptr;                // preallocated chunk slots
@@ -464,8 +471,11 @@ Runtime::~Runtime() {
   for (auto& kv : pool_) cudaFree(kv.second);
   for (auto e : events_) cudaEventDestroy(e);
   cudaFree(d_cbase_);
-  cudaFree(d_cstage_);
-  if (h_cstage_) cudaFreeHost(h_cstage_);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(d_cstage_[b]);
+    if (h_cstage_[b]) cudaFreeHost(h_cstage_[b]);
+    if (cstage_ev_[b]) cudaEventDestroy(cstage_ev_[b]);
+  }
   if (h_loads_) cudaFreeHost(h_loads_);
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
@@ -1027,10 +1037,13 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   int32_t shift = shift_ % cfg_.ny;
   if (host_io) {
     // the reference keeps the shifted load field on the host (engine.hpp:337-342)
-    std::memcpy(h_cstage_, field_.c.data(), field_.c.size() * sizeof(double));
-    OD_CU(cudaMemcpyAsync(d_cstage_, h_cstage_, field_.c.size() * sizeof(double),
+    const int b = cstage_cur_ ^= 1;
+    OD_CU(cudaEventSynchronize(cstage_ev_[b]));  // the copy two steps ago has left it
+    std::memcpy(h_cstage_[b], field_.c.data(), field_.c.size() * sizeof(double));
+    OD_CU(cudaMemcpyAsync(d_cstage_[b], h_cstage_[b], field_.c.size() * sizeof(double),
                           cudaMemcpyHostToDevice, s0_));
-    cfield = d_cstage_;
+    OD_CU(cudaEventRecord(cstage_ev_[b], s0_));
+    cfield = d_cstage_[b];
     shift = 0;
   }
   unsigned long long* ns = nullptr;
@@ -1342,7 +1355,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   if (d_tl_ && tl_n_ < tl_cap_) ++tl_n_;
   if (host_io && nres > 0) {
     // the step's per-chunk device times back to the host
-    OD_CU(cudaMemcpyAsync(h_loads_, ns, size_t(2 * nres) * sizeof(unsigned long long),
+    OD_CU(cudaMemcpyAsync(h_loads_dst_, ns, size_t(2 * nres) * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s0_));
   }
   r.ev_end = new_event();
@@ -1572,10 +1585,19 @@ void Runtime::advance(int32_t n, int32_t* epochs_done) {
 void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads) {
   if (n < 0) throw ValidationError("negative step count");
   const size_t cells = size_t(cfg_.nx) * cfg_.ny;
-  if (!h_cstage_) {
-    OD_CU(cudaMallocHost(&h_cstage_, cells * sizeof(double)));
-    OD_CU(cudaMalloc(&d_cstage_, cells * sizeof(double)));
-    OD_CU(cudaMallocHost(&h_loads_, 2 * std::max<size_t>(K(), 1) * sizeof(unsigned long long)));
+  if (!h_cstage_[0]) {
+    for (int b = 0; b < 2; ++b) {
+      OD_CU(cudaMallocHost(&h_cstage_[b], cells * sizeof(double)));
+      OD_CU(cudaMalloc(&d_cstage_[b], cells * sizeof(double)));
+      OD_CU(cudaEventCreateWithFlags(&cstage_ev_[b], cudaEventDisableTiming));
+    }
+  }
+  const size_t row_words = 2 * std::max<size_t>(K(), 1);
+  if (h_loads_rows_ < size_t(std::max(n, 1))) {
+    OD_CU(cudaStreamSynchronize(s0_));
+    if (h_loads_) cudaFreeHost(h_loads_);
+    h_loads_rows_ = size_t(std::max(n, 1));
+    OD_CU(cudaMallocHost(&h_loads_, h_loads_rows_ * row_words * sizeof(unsigned long long)));
   }
   if (host_c && n_fields > 0) {
     // the caller's load multiplier field replaces the base field
@@ -1584,17 +1606,15 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
     set_shift(shift_);
   }
   const int32_t S = cfg_.async_steps + cfg_.sync_steps;
+  // steps are launched back to back; the per-step loads land in pinned rows
+  // and are read once the stream has drained (epoch ends drain it anyway)
+  std::vector<std::vector<int32_t>> step_vps(host_loads ? n : 0);
   for (int32_t i = 0; i < n; ++i) {
     if (cur_step_ == 0) begin_window();
     advance_advection(cur_epoch_, cur_step_);
+    h_loads_dst_ = h_loads_ + size_t(i) * row_words;
     launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true);
-    OD_CU(cudaStreamSynchronize(s0_));
-    if (host_loads) {
-      double* row = host_loads + size_t(i) * K();
-      std::fill(row, row + K(), 0.0);
-      const auto& vps = window_.back().slot_vps;
-      for (size_t j = 0; j < vps.size(); ++j) row[vps[j]] = double(h_loads_[2 * j]) * 1e-9;
-    }
+    if (host_loads) step_vps[i] = window_.back().slot_vps;
     ++global_step_;
     if (++cur_step_ == S) {
       EpochOut o;
@@ -1602,6 +1622,13 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
       ++cur_epoch_;
       cur_step_ = 0;
     }
+  }
+  OD_CU(cudaStreamSynchronize(s0_));
+  for (int32_t i = 0; host_loads && i < n; ++i) {
+    double* row = host_loads + size_t(i) * K();
+    std::fill(row, row + K(), 0.0);
+    const unsigned long long* src = h_loads_ + size_t(i) * row_words;
+    for (size_t j = 0; j < step_vps[i].size(); ++j) row[step_vps[i][j]] = double(src[2 * j]) * 1e-9;
   }
 }
 
