@@ -132,6 +132,30 @@ int od_plan_cost(const od_move* moves, int32_t n_moves, const int64_t* data_byte
                  double network_bandwidth, double network_latency, const od_gpu_model* gpu,
                  double* out);
 
+/* B200 replacement of plan_cost (balancer.hpp:157-175; no host staging): chunk
+   moves are NVLink peer copies between the owning GPUs, GPUs copy concurrently,
+   a GPU's sends and receives share its port: max over GPUs of max(bytes out,
+   bytes in) / link_bandwidth + latency per transfer touching it.  Moves between
+   processors of one GPU are free. */
+int od_plan_cost_nvlink(const od_move* moves, int32_t n_moves, const int64_t* data_bytes,
+                        int32_t vp_count, int32_t procs_per_gpu, int32_t gpus,
+                        double link_bandwidth, double latency, double* out);
+/* calibrate_gpu: saturated rows (within 10 % of the fastest) set the floor, a
+   least-squares line the rest, then a Nelder-Mead refinement of the hinge model
+   when it leaves a residual; non-model fields come from `defaults`
+                                                        gpu_cost.hpp:187-246 */
+int od_calibrate_gpu(const od_kernel_work* work, const double* seconds, int32_t n,
+                     const od_gpu_model* defaults, od_gpu_model* out, double* max_rel_residual);
+/* calibrate_cpu: least squares through the origin      gpu_cost.hpp:249-261 */
+int od_calibrate_cpu(const od_kernel_work* work, const double* seconds, int32_t n,
+                     double* per_item_time);
+/* cpu_time                                             gpu_cost.hpp:56-58 */
+int od_cpu_time(const od_kernel_work* work, double per_item_time, double* out);
+/* scaling_probe: (n-2)*(m-2) items x `inner` per m     engine.hpp:363-373 */
+int od_scaling_probe(int32_t n, const int32_t* m_list, int32_t n_m, double inner,
+                     const od_gpu_model* gpu, double cpu_per_item, double* cpu_seconds,
+                     double* gpu_seconds);
+
 /* ---------------------------------------------------------------- balancer */
 /* should_balance                                       balancer.hpp:29-32 */
 int od_should_balance(const double* totals, int32_t n, double trigger_threshold,

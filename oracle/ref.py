@@ -58,6 +58,9 @@ def lib():
         l.ref_node_gpu_schedule.argtypes = [DP, I, I, DP, DP]
         l.ref_plan_cost.argtypes = [IP, I, C.POINTER(C.c_longlong), I, I, I, D, D, DP, DP]
         l.ref_preset_json.argtypes = [C.c_char_p, C.c_char_p, C.c_long]
+        l.ref_calibrate_gpu.argtypes = [DP, DP, DP, I, DP, DP, DP]
+        l.ref_calibrate_cpu.argtypes = [DP, DP, DP, I, DP]
+        l.ref_scaling_probe.argtypes = [I, IP, I, D, DP, D, DP, DP]
         _lib = l
     return _lib
 
@@ -240,3 +243,30 @@ def plan_cost(moves, data_bytes, nodes, ppn, bw, lat, g):
     _chk(lib().ref_plan_cost(_ip(mv), len(moves), b.ctypes.data_as(C.POINTER(C.c_longlong)),
                              len(b), nodes, ppn, bw, lat, _dp(_gm(g)), C.byref(out)))
     return out.value
+
+
+def calibrate_gpu(samples, defaults):
+    """samples: (items, depth, seconds) rows; returns (6 model values, residual)."""
+    a = np.ascontiguousarray(np.array(samples, dtype=np.float64).reshape(-1, 3))
+    it, dp, sc = (np.ascontiguousarray(a[:, i]) for i in range(3))
+    out = np.zeros(6)
+    res = C.c_double()
+    _chk(lib().ref_calibrate_gpu(_dp(it), _dp(dp), _dp(sc), len(a), _dp(_gm(defaults)), _dp(out),
+                                 C.byref(res)))
+    return out.tolist(), res.value
+
+
+def calibrate_cpu(samples):
+    a = np.ascontiguousarray(np.array(samples, dtype=np.float64).reshape(-1, 3))
+    it, dp, sc = (np.ascontiguousarray(a[:, i]) for i in range(3))
+    out = C.c_double()
+    _chk(lib().ref_calibrate_cpu(_dp(it), _dp(dp), _dp(sc), len(a), C.byref(out)))
+    return out.value
+
+
+def scaling_probe(n, m_list, inner, g, cpu_per_item):
+    m = np.ascontiguousarray(m_list, dtype=np.int32)
+    c, gg = np.zeros(len(m)), np.zeros(len(m))
+    _chk(lib().ref_scaling_probe(n, _ip(m), len(m), float(inner), _dp(_gm(g)), float(cpu_per_item),
+                                 _dp(c), _dp(gg)))
+    return c.tolist(), gg.tolist()

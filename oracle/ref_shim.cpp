@@ -14,6 +14,8 @@
 //   run_experiment + render_report       engine.hpp:357, report.hpp:69
 //   kernel_time_sync / transfer_time / node_gpu_schedule / plan_cost
 //                                        gpu_cost.hpp:50-80, balancer.hpp:157-175
+//   calibrate_gpu / calibrate_cpu / cpu_time / scaling_probe
+//                                        gpu_cost.hpp:56-58,187-261, engine.hpp:363-373
 #include <cstring>
 #include <exception>
 #include <string>
@@ -238,6 +240,43 @@ int ref_plan_cost(const int* moves, int n, const long long* bytes, int K, int no
     for (int v = 0; v < K; ++v) vps[v].data_bytes = bytes[v];
     ClusterState cl = build_cluster(ClusterSpec{nodes, ppn, 1, bw, lat});
     *out = plan_cost(plan, vps, cl, gm(g));
+  });
+}
+
+static std::vector<CalibrationSample> calib(const double* items, const double* depth,
+                                            const double* sec, int n) {
+  std::vector<CalibrationSample> v;
+  for (int i = 0; i < n; ++i) v.push_back({KernelWork{items[i], depth[i]}, sec[i]});
+  return v;
+}
+
+int ref_calibrate_gpu(const double* items, const double* depth, const double* sec, int n,
+                      const double* defaults, double* out, double* residual) {
+  return wrap([&] {
+    GpuCalibration c = calibrate_gpu(calib(items, depth, sec, n), gm(defaults));
+    out[0] = c.model.launch_overhead;
+    out[1] = c.model.per_item_time;
+    out[2] = c.model.saturation_floor;
+    out[3] = c.model.h2d_bandwidth;
+    out[4] = c.model.d2h_bandwidth;
+    out[5] = c.model.async_overlap_gain;
+    *residual = c.max_relative_residual;
+  });
+}
+
+int ref_calibrate_cpu(const double* items, const double* depth, const double* sec, int n,
+                      double* out) {
+  return wrap([&] { *out = calibrate_cpu(calib(items, depth, sec, n)).per_item_time; });
+}
+
+int ref_scaling_probe(int n, const int* m, int nm, double inner, const double* g, double cpu,
+                      double* cpu_out, double* gpu_out) {
+  return wrap([&] {
+    auto rows = scaling_probe(n, std::vector<int>(m, m + nm), inner, gm(g), CpuModel{cpu});
+    for (size_t i = 0; i < rows.size(); ++i) {
+      cpu_out[i] = rows[i].cpu_seconds;
+      gpu_out[i] = rows[i].gpu_seconds;
+    }
   });
 }
 

@@ -138,6 +138,12 @@ PROTOTYPES = {
     "od_node_gpu_schedule": [_P(_D), _I32, _I32, _P(od_gpu_model), _P(_D)],
     "od_plan_cost": [_P(od_move), _I32, _P(_I64), _I32, _I32, _I32, _D, _D, _P(od_gpu_model),
                      _P(_D)],
+    "od_plan_cost_nvlink": [_P(od_move), _I32, _P(_I64), _I32, _I32, _I32, _D, _D, _P(_D)],
+    "od_calibrate_gpu": [_P(od_kernel_work), _P(_D), _I32, _P(od_gpu_model), _P(od_gpu_model),
+                         _P(_D)],
+    "od_calibrate_cpu": [_P(od_kernel_work), _P(_D), _I32, _P(_D)],
+    "od_cpu_time": [_P(od_kernel_work), _D, _P(_D)],
+    "od_scaling_probe": [_I32, _P(_I32), _I32, _D, _P(od_gpu_model), _D, _P(_D), _P(_D)],
     "od_epoch_decision": [_P(_D), _I32, _P(_I32), _I32, _I32, _I32, _I32, _P(_I32), _I32, _I32,
                           _D, _D, _P(_I32), _P(od_move), _I32, _P(_I32), _P(_D), _P(_D),
                           _P(_D)],

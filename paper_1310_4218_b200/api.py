@@ -40,7 +40,9 @@ __all__ = [
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
     "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
     "FaceXfer", "exchange_schedule", "GpuModel", "TransferDirection", "kernel_time_sync",
-    "transfer_time", "node_gpu_schedule", "plan_cost",
+    "transfer_time", "node_gpu_schedule", "plan_cost", "CpuModel", "CalibrationSample",
+    "GpuCalibration", "calibrate_gpu", "calibrate_cpu", "cpu_time", "ProbeRow", "scaling_probe",
+    "reference_gpu_probe_samples", "reference_cpu_probe_samples", "plan_cost_nvlink",
 ]
 
 
@@ -514,6 +516,104 @@ def plan_cost(plan: MigrationPlan, data_bytes: Sequence[int], procs_per_node: in
                            int(procs_per_node), int(nodes), float(network_bandwidth),
                            float(network_latency), C.byref(g), C.byref(out)))
     return out.value
+
+
+def plan_cost_nvlink(plan: MigrationPlan, data_bytes: Sequence[int], procs_per_gpu: int,
+                     gpus: int, link_bandwidth: float = 450e9,
+                     latency: float = 2e-5) -> float:
+    """B200 migration cost (replaces plan_cost's host staging): NVLink peer copies,
+    GPUs in parallel, max(bytes out, bytes in) per GPU over its link."""
+    db = np.ascontiguousarray(data_bytes, dtype=np.int64)
+    out = C.c_double()
+    check(lib.od_plan_cost_nvlink(_moves_c(plan.moves), len(plan.moves),
+                                  db.ctypes.data_as(C.POINTER(C.c_int64)), int(db.size),
+                                  int(procs_per_gpu), int(gpus), float(link_bandwidth),
+                                  float(latency), C.byref(out)))
+    return out.value
+
+
+# --------------------------------------------------------------- calibration --
+@dataclass
+class CpuModel:  # gpu_cost.hpp:41-47
+    per_item_time: float = 1.0e-9
+
+
+@dataclass
+class CalibrationSample:  # gpu_cost.hpp:82-85
+    work: KernelWork
+    seconds: float
+
+
+@dataclass
+class GpuCalibration:  # gpu_cost.hpp:87-90
+    model: GpuModel
+    max_relative_residual: float = 0.0
+
+
+@dataclass
+class ProbeRow:  # engine.hpp:104-108
+    m: int
+    cpu_seconds: float
+    gpu_seconds: float
+
+
+def _calib_arrays(samples: Sequence[CalibrationSample]):
+    n = len(samples)
+    w = (od_kernel_work * max(n, 1))()
+    for i, s in enumerate(samples):
+        w[i] = od_kernel_work(float(s.work.work_items), float(s.work.serial_depth))
+    sec = np.ascontiguousarray([float(s.seconds) for s in samples] or [0.0], dtype=np.float64)
+    return w, sec, n
+
+
+def calibrate_gpu(samples: Sequence[CalibrationSample],
+                  defaults: Optional[GpuModel] = None) -> GpuCalibration:  # gpu_cost.hpp:187-246
+    w, sec, n = _calib_arrays(samples)
+    d = (defaults or GpuModel())._c()
+    out = od_gpu_model()
+    res = C.c_double()
+    check(lib.od_calibrate_gpu(w, _dptr(sec), n, C.byref(d), C.byref(out), C.byref(res)))
+    m = GpuModel(out.launch_overhead, out.per_item_time, out.saturation_floor, out.h2d_bandwidth,
+                 out.d2h_bandwidth, out.async_overlap_gain)
+    return GpuCalibration(m, res.value)
+
+
+def calibrate_cpu(samples: Sequence[CalibrationSample]) -> CpuModel:  # gpu_cost.hpp:249-261
+    w, sec, n = _calib_arrays(samples)
+    out = C.c_double()
+    check(lib.od_calibrate_cpu(w, _dptr(sec), n, C.byref(out)))
+    return CpuModel(out.value)
+
+
+def cpu_time(work: KernelWork, cpu: CpuModel) -> float:  # gpu_cost.hpp:56-58
+    out = C.c_double()
+    w = od_kernel_work(work.work_items, work.serial_depth)
+    check(lib.od_cpu_time(C.byref(w), float(cpu.per_item_time), C.byref(out)))
+    return out.value
+
+
+def scaling_probe(n: int, m_list: Sequence[int], inner: float, gpu: GpuModel,
+                  cpu: CpuModel) -> List[ProbeRow]:  # engine.hpp:363-373
+    m = np.ascontiguousarray(m_list, dtype=np.int32)
+    c = np.zeros(max(m.size, 1))
+    g = np.zeros(max(m.size, 1))
+    gm = gpu._c()
+    check(lib.od_scaling_probe(int(n), m.ctypes.data_as(C.POINTER(C.c_int32)), int(m.size),
+                               float(inner), C.byref(gm), float(cpu.per_item_time), _dptr(c),
+                               _dptr(g)))
+    return [ProbeRow(int(m[i]), float(c[i]), float(g[i])) for i in range(m.size)]
+
+
+def reference_gpu_probe_samples() -> List[CalibrationSample]:
+    """The K20 probe measurements the reference bundles (gpu_cost.hpp:264-274):
+    a 1024 x M grid with a 2e5-deep serial inner loop."""
+    return [CalibrationSample(KernelWork(1022.0 * m, 2.0e5), t)
+            for m, t in ((510, 0.82), (254, 0.49), (126, 0.33), (62, 0.17), (30, 0.18))]
+
+
+def reference_cpu_probe_samples() -> List[CalibrationSample]:  # gpu_cost.hpp:276-283
+    return [CalibrationSample(KernelWork(1022.0 * m, 2.0e5), t)
+            for m, t in ((510, 54.41), (254, 27.1), (126, 13.45))]
 
 
 # --------------------------------------------------------------- measurement --

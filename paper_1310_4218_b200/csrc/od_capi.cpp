@@ -303,6 +303,80 @@ int od_plan_cost(const od_move* moves, int32_t n_moves, const int64_t* data_byte
   });
 }
 
+static std::vector<CalibSample> samples_of(const od_kernel_work* work, const double* seconds,
+                                           int32_t n) {
+  if (n < 0) throw ValidationError("negative count");
+  if (n > 0) {
+    need(work, "work");
+    need(seconds, "seconds");
+  }
+  std::vector<CalibSample> ss(n);
+  for (int32_t i = 0; i < n; ++i) ss[i] = {Work{work[i].work_items, work[i].serial_depth}, seconds[i]};
+  return ss;
+}
+
+int od_calibrate_gpu(const od_kernel_work* work, const double* seconds, int32_t n,
+                     const od_gpu_model* defaults, od_gpu_model* out, double* max_rel_residual) {
+  return guarded([&] {
+    need(out, "out");
+    const GpuFit f = calibrate_gpu_model(samples_of(work, seconds, n), gpu_of(defaults));
+    *out = od_gpu_model{f.model.launch_overhead, f.model.per_item_time, f.model.saturation_floor,
+                        f.model.h2d_bandwidth, f.model.d2h_bandwidth, f.model.async_overlap_gain};
+    if (max_rel_residual) *max_rel_residual = f.max_rel_residual;
+  });
+}
+
+int od_calibrate_cpu(const od_kernel_work* work, const double* seconds, int32_t n,
+                     double* per_item_time) {
+  return guarded([&] {
+    need(per_item_time, "per_item_time");
+    *per_item_time = calibrate_cpu_model(samples_of(work, seconds, n));
+  });
+}
+
+int od_cpu_time(const od_kernel_work* work, double per_item_time, double* out) {
+  return guarded([&] {
+    need(work, "work");
+    need(out, "out");
+    if (per_item_time <= 0) throw ValidationError("cpu model per_item_time must be > 0");
+    *out = cpu_time_model(Work{work->work_items, work->serial_depth}, per_item_time);
+  });
+}
+
+int od_scaling_probe(int32_t n, const int32_t* m_list, int32_t n_m, double inner,
+                     const od_gpu_model* gpu, double cpu_per_item, double* cpu_seconds,
+                     double* gpu_seconds) {
+  return guarded([&] {
+    if (n_m < 0) throw ValidationError("negative count");
+    if (n_m > 0) {
+      need(m_list, "m_list");
+      need(cpu_seconds, "cpu_seconds");
+      need(gpu_seconds, "gpu_seconds");
+    }
+    if (cpu_per_item <= 0) throw ValidationError("cpu model per_item_time must be > 0");
+    std::vector<double> c, g;
+    scaling_probe_model(n, std::vector<int32_t>(m_list, m_list + n_m), inner, gpu_of(gpu),
+                        cpu_per_item, c, g);
+    std::copy(c.begin(), c.end(), cpu_seconds);
+    std::copy(g.begin(), g.end(), gpu_seconds);
+  });
+}
+
+int od_plan_cost_nvlink(const od_move* moves, int32_t n_moves, const int64_t* data_bytes,
+                        int32_t vp_count, int32_t procs_per_gpu, int32_t gpus,
+                        double link_bandwidth, double latency, double* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (n_moves < 0 || vp_count < 0) throw ValidationError("negative count");
+    if (n_moves > 0) need(moves, "moves");
+    if (vp_count > 0) need(data_bytes, "data_bytes");
+    std::vector<MoveRec> mv(n_moves);
+    for (int32_t i = 0; i < n_moves; ++i) mv[i] = {moves[i].vp, moves[i].from, moves[i].to};
+    *out = plan_cost_nvlink_model(mv, std::vector<int64_t>(data_bytes, data_bytes + vp_count),
+                                  procs_per_gpu, gpus, link_bandwidth, latency);
+  });
+}
+
 int od_epoch_decision(const double* loads, int32_t n_loads, const int32_t* map,
                       int32_t vp_count, int32_t proc_count, int32_t epoch_index, int32_t epochs,
                       int32_t* balance_calls, int32_t first_strategy, int32_t later_strategy,

@@ -3,6 +3,7 @@
 #include "od_model.hpp"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 
 namespace odb {
@@ -476,6 +477,212 @@ std::vector<double> SampleStore::sync_means() const {
     s[v] = s[v] / n[v];
   }
   return s;
+}
+
+double plan_cost_nvlink_model(const std::vector<MoveRec>& plan,
+                              const std::vector<int64_t>& data_bytes, int32_t procs_per_gpu,
+                              int32_t gpus, double link_bandwidth, double latency) {
+  if (procs_per_gpu < 1 || gpus < 1) throw ValidationError("cluster sizes must be >= 1");
+  if (link_bandwidth <= 0) throw ValidationError("link bandwidth must be > 0");
+  if (latency < 0) throw ValidationError("link latency must be >= 0");
+  std::vector<double> out_b(gpus, 0.0), in_b(gpus, 0.0);
+  std::vector<int32_t> count(gpus, 0);
+  for (const MoveRec& m : plan) {
+    if (m.vp < 0 || m.vp >= int32_t(data_bytes.size()))
+      throw ValidationError("move vp out of range");
+    const int32_t a = m.from / procs_per_gpu, b = m.to / procs_per_gpu;
+    if (m.from < 0 || m.to < 0 || a >= gpus || b >= gpus)
+      throw ValidationError("move processor out of range");
+    if (a == b) continue;
+    out_b[a] += double(data_bytes[m.vp]);
+    in_b[b] += double(data_bytes[m.vp]);
+    ++count[a];
+    ++count[b];
+  }
+  double worst = 0.0;
+  for (int32_t g = 0; g < gpus; ++g) {
+    const double t = (out_b[g] > in_b[g] ? out_b[g] : in_b[g]) / link_bandwidth +
+                     latency * count[g];
+    if (t > worst) worst = t;
+  }
+  return worst;
+}
+
+// ---- calibration --------------------------------------------------------------
+namespace {
+
+// squared relative error of max(floor, launch + rate * total) over the samples
+// (gpu_cost.hpp:94-104); out-of-domain parameters are rejected with a huge value
+double hinge_error(const std::vector<CalibSample>& ss, const std::array<double, 3>& p) {
+  const double launch = p[0], rate = p[1], floor = p[2];
+  if (launch < 0 || rate <= 0 || floor < 0) return 1e30;
+  double e = 0.0;
+  for (const CalibSample& s : ss) {
+    const double line = launch + rate * s.w.total();
+    const double pred = floor < line ? line : floor;
+    const double rel = (pred - s.seconds) / s.seconds;
+    e += rel * rel;
+  }
+  return e;
+}
+
+// Nelder-Mead on (launch, rate, floor) from `start` (gpu_cost.hpp:108-168):
+// initial simplex = start plus each coordinate scaled by 1.25 (1e-6 if zero);
+// reflect 1, expand 2, contract +-0.5, shrink 0.5 toward the best; at most
+// 2000 iterations, stop when the spread of values is below 1e-16 (1 + best)
+std::array<double, 3> nelder_mead(const std::vector<CalibSample>& ss, std::array<double, 3> start) {
+  using Pt = std::array<double, 3>;
+  std::array<Pt, 4> x;
+  std::array<double, 4> fx;
+  x[0] = start;
+  for (int i = 0; i < 3; ++i) {
+    x[i + 1] = start;
+    x[i + 1][i] = start[i] != 0.0 ? start[i] * 1.25 : 1e-6;
+  }
+  for (int i = 0; i < 4; ++i) fx[i] = hinge_error(ss, x[i]);
+  for (int it = 0; it < 2000; ++it) {
+    // exchange ordering by value (ties keep their relative order)
+    for (int i = 0; i < 4; ++i)
+      for (int j = i + 1; j < 4; ++j)
+        if (fx[j] < fx[i]) {
+          std::swap(fx[i], fx[j]);
+          std::swap(x[i], x[j]);
+        }
+    if (fx[3] - fx[0] < 1e-16 * (1.0 + fx[0])) break;
+    Pt c{0.0, 0.0, 0.0};
+    for (int i = 0; i < 3; ++i)
+      for (int d = 0; d < 3; ++d) c[d] += x[i][d] / 3.0;
+    auto along = [&](double t) {
+      Pt q;
+      for (int d = 0; d < 3; ++d) q[d] = c[d] + t * (c[d] - x[3][d]);
+      return q;
+    };
+    const Pt r = along(1.0);
+    const double fr = hinge_error(ss, r);
+    if (fr < fx[0]) {
+      const Pt e = along(2.0);
+      const double fe = hinge_error(ss, e);
+      if (fe < fr) {
+        x[3] = e;
+        fx[3] = fe;
+      } else {
+        x[3] = r;
+        fx[3] = fr;
+      }
+    } else if (fr < fx[2]) {
+      x[3] = r;
+      fx[3] = fr;
+    } else {
+      const Pt k = along(fr < fx[3] ? 0.5 : -0.5);
+      const double fk = hinge_error(ss, k);
+      if (fk < (fr < fx[3] ? fr : fx[3])) {
+        x[3] = k;
+        fx[3] = fk;
+      } else {
+        for (int i = 1; i < 4; ++i) {
+          for (int d = 0; d < 3; ++d) x[i][d] = 0.5 * (x[i][d] + x[0][d]);
+          fx[i] = hinge_error(ss, x[i]);
+        }
+      }
+    }
+  }
+  int best = 0;
+  for (int i = 1; i < 4; ++i)
+    if (fx[i] < fx[best]) best = i;
+  return x[best];
+}
+
+// ordinary least squares y = a + b x (gpu_cost.hpp:171-181)
+std::pair<double, double> line_fit(const std::vector<std::pair<double, double>>& xy) {
+  const double n = double(xy.size());
+  double sx = 0, sy = 0, sxx = 0, sxy = 0;
+  for (const auto& p : xy) {
+    sx += p.first;
+    sy += p.second;
+    sxx += p.first * p.first;
+    sxy += p.first * p.second;
+  }
+  const double den = n * sxx - sx * sx;
+  if (den == 0) throw ValidationError("degenerate calibration samples (identical work)");
+  const double b = (n * sxy - sx * sy) / den;
+  return {(sy - b * sx) / n, b};
+}
+
+}  // namespace
+
+GpuFit calibrate_gpu_model(const std::vector<CalibSample>& ss, const GpuCostModel& defaults) {
+  if (ss.size() < 3) throw ValidationError("gpu calibration needs >= 3 samples");
+  for (const CalibSample& s : ss)
+    if (s.seconds <= 0 || s.w.total() <= 0)
+      throw ValidationError("gpu calibration samples must have positive work and time");
+  double tmin = ss[0].seconds;
+  for (const CalibSample& s : ss)
+    if (s.seconds < tmin) tmin = s.seconds;
+  std::vector<std::pair<double, double>> above;
+  int floor_rows = 0;
+  for (const CalibSample& s : ss) {
+    if (s.seconds <= tmin * 1.10)
+      ++floor_rows;
+    else
+      above.emplace_back(s.w.total(), s.seconds);
+  }
+  std::array<double, 3> p{0.0, 0.0, 0.0};  // launch, rate, floor
+  if (above.size() >= 2) {
+    const auto ab = line_fit(above);
+    p = {ab.first > 0.0 ? ab.first : 0.0, ab.second, floor_rows >= 1 ? tmin : 0.0};
+  } else {
+    std::vector<std::pair<double, double>> all;
+    for (const CalibSample& s : ss) all.emplace_back(s.w.total(), s.seconds);
+    const auto ab = line_fit(all);
+    p = {ab.first > 0.0 ? ab.first : 0.0, ab.second, 0.0};
+  }
+  if (p[1] <= 0) throw ValidationError("gpu calibration produced a non-positive rate");
+  const double e0 = hinge_error(ss, p);
+  if (e0 > 1e-12) {
+    const double f0 = p[2] > tmin * 0.5 ? p[2] : tmin * 0.5;
+    const std::array<double, 3> q = nelder_mead(ss, {p[0], p[1], f0});
+    if (hinge_error(ss, q) < e0) p = q;
+  }
+  GpuFit out;
+  out.model = defaults;
+  out.model.launch_overhead = p[0];
+  out.model.per_item_time = p[1];
+  out.model.saturation_floor = p[2];
+  out.model.validate();
+  for (const CalibSample& s : ss) {
+    const double r = std::abs(kernel_time_sync_model(s.w, out.model) - s.seconds) / s.seconds;
+    if (r > out.max_rel_residual) out.max_rel_residual = r;
+  }
+  return out;
+}
+
+double calibrate_cpu_model(const std::vector<CalibSample>& ss) {
+  if (ss.empty()) throw ValidationError("cpu calibration needs samples");
+  double sxx = 0, sxy = 0;
+  for (const CalibSample& s : ss) {
+    const double x = s.w.total();
+    sxx += x * x;
+    sxy += x * s.seconds;
+  }
+  if (sxx == 0) throw ValidationError("degenerate cpu calibration samples");
+  const double r = sxy / sxx;
+  if (r <= 0) throw ValidationError("cpu model per_item_time must be > 0");
+  return r;
+}
+
+double cpu_time_model(const Work& w, double cpu_per_item) { return cpu_per_item * w.total(); }
+
+void scaling_probe_model(int32_t n, const std::vector<int32_t>& m_list, double inner,
+                         const GpuCostModel& g, double cpu_per_item, std::vector<double>& cpu_s,
+                         std::vector<double>& gpu_s) {
+  if (m_list.empty()) throw ValidationError("scaling probe needs at least one M");
+  cpu_s.clear();
+  gpu_s.clear();
+  for (int32_t m : m_list) {
+    const Work w{double(n - 2) * (m - 2), inner};
+    cpu_s.push_back(cpu_time_model(w, cpu_per_item));
+    gpu_s.push_back(kernel_time_sync_model(w, g));
+  }
 }
 
 }  // namespace odb

@@ -108,6 +108,39 @@ double plan_cost_model(const std::vector<MoveRec>& plan, const std::vector<int64
                        int32_t procs_per_node, int32_t nodes, double net_bandwidth,
                        double net_latency, const GpuCostModel& g);
 
+// B200 migration cost (replaces plan_cost's host staging, balancer.hpp:157-175):
+// a chunk moves as one peer copy between the two GPUs owning its old and new
+// processor (procs_per_gpu processors per GPU; moves inside a GPU are free).
+// GPUs copy concurrently; a GPU's sends and receives share its NVLink port, so
+// the plan costs max over GPUs of max(bytes out, bytes in) / link_bandwidth
+// plus latency per transfer touching that GPU.
+double plan_cost_nvlink_model(const std::vector<MoveRec>& plan,
+                              const std::vector<int64_t>& data_bytes, int32_t procs_per_gpu,
+                              int32_t gpus, double link_bandwidth, double latency);
+
+// ---- calibration (gpu_cost.hpp:82-258, engine.hpp:363-373) -----------------
+struct CalibSample {
+  Work w;
+  double seconds = 0;
+};
+struct GpuFit {
+  GpuCostModel model;
+  double max_rel_residual = 0;
+};
+// calibrate_gpu: rows within 10 % of the fastest are the saturated floor, the
+// others get a least-squares line; if that leaves a residual, a Nelder-Mead
+// pass on (launch, rate, floor) minimises the squared relative error of the
+// full hinge model and is kept when it is better
+GpuFit calibrate_gpu_model(const std::vector<CalibSample>& samples, const GpuCostModel& defaults);
+// calibrate_cpu: least squares through the origin (per-item seconds)
+double calibrate_cpu_model(const std::vector<CalibSample>& samples);
+double cpu_time_model(const Work& w, double cpu_per_item);
+// scaling_probe: an n x m grid with an `inner`-deep serial loop per interior
+// point, for each m: (cpu seconds, gpu seconds) under the two models
+void scaling_probe_model(int32_t n, const std::vector<int32_t>& m_list, double inner,
+                         const GpuCostModel& g, double cpu_per_item, std::vector<double>& cpu_s,
+                         std::vector<double>& gpu_s);
+
 // ---- epoch policy (Engine::run_epoch, engine.hpp:257-268) --------------------
 struct Decision {
   int32_t strategy = -1;  // -1: no strategy called
