@@ -19,6 +19,7 @@ Prints one JSON line on rank 0.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import statistics
@@ -43,6 +44,8 @@ def parse_args():
     p.add_argument("--n-inner", type=int, default=None)
     p.add_argument("--kernel-mode", type=int, default=None,
                    help="0 separate kernels, 4 fused, 5 fused persistent (default)")
+    p.add_argument("--threshold", type=float, default=None,
+                   help="override the config's LB trigger threshold")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-lb-off", action="store_true")
@@ -213,6 +216,8 @@ def main():
     if args.kernel_mode is not None:
         kw["overlap"] = args.kernel_mode
     cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
+    if args.threshold is not None:
+        cfg = cfg.replace(policy=dataclasses.replace(cfg.policy, trigger_threshold=args.threshold))
 
     if args.impl == "reference":
         if rank == 0:
