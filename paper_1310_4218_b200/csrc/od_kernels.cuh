@@ -196,6 +196,39 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// CTA-scope mbarrier in shared memory: arrive (release) and wait for a phase
+// (acquire) are separate, so a thread can signal "my reads of the ring are done
+// and my copies have landed" and then run physics while the others catch up.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_inval(uint64_t* b) {
+  asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  uint64_t state;
+  asm volatile("mbarrier.arrive.shared::cta.b64 %0, [%1];\n"
+               : "=l"(state)
+               : "r"(smem_u32(b))
+               : "memory");
+  (void)state;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
 // f(b, a) of Fig. 1 / Fig. 4: mix a and b, then n micro-steps of the
 // perturbed logistic map.  Every operation is a correctly rounded add/mul/fma.
 __device__ __forceinline__ double column_f(double b, double a, int n) {
@@ -667,27 +700,42 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     fast = 0;  // the level loop's budgets differ from the pre-roll's
   }
 
+  // ring hand-off: an mbarrier phase per level pair.  A thread arrives once its
+  // reads of the pair's planes are done and its copies for the next pair have
+  // landed, then runs its physics quota while the other warps catch up; the
+  // next pair starts (and refills the slots just read) when the phase is done.
+  __shared__ uint64_t s_ring_bar;
+  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (bar_lead) mbar_init(&s_ring_bar, blockDim.x * blockDim.y);
+  __syncthreads();
+
 #pragma unroll
   for (int L = 0; L < S; ++L) issue(L);
+  cp_async_wait<S - 3>();  // planes <= 2 landed for this thread
+  mbar_arrive(&s_ring_bar);
 
+  uint32_t parity = 0;
   int k = 0, L = 0;
   for (; L + 1 < levels; L += 2) {
-    cp_async_wait<S - 3>();  // planes <= L+2 landed
-    __syncthreads();
+    mbar_wait(&s_ring_bar, parity);  // everyone: planes <= L+2 landed, planes L-2, L-1 read
+    parity ^= 1;
     issue(L + S);
     issue(L + S + 1);
     level(L, k);
     if (++k == nz) k = 0;
     level(L + 1, k);
     if (++k == nz) k = 0;
+    cp_async_wait<S - 3>();  // this thread's planes <= L+4 landed
+    mbar_arrive(&s_ring_bar);
     physics(2 * q0, 2 * q1);
   }
   if (L < levels) {
-    cp_async_wait<0>();
-    __syncthreads();
+    mbar_wait(&s_ring_bar, parity);
     level(L, k);
   }
   cp_async_wait<0>();
+  __syncthreads();
+  if (bar_lead) mbar_inval(&s_ring_bar);
   if (ncell >= 1) physics_advance(s0, 0x7fffffff);
   if (ncell == 2) physics_advance(s1, 0x7fffffff);
 
