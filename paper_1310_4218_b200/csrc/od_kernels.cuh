@@ -171,14 +171,53 @@ struct HaloWait {
   const int32_t* senders;
   int32_t n;
   unsigned long long stamp;
-  unsigned long long* wait_ns;  // longest pre-roll (diagnostic), may be null
+  unsigned long long* wait_ns;  // longest blocking wait (diagnostic), may be null
+  // cross-step overlap: neighbour tiles on this GPU that must have finished the
+  // previous step (their U^t cells are this tile's halo)
+  const unsigned* done;
+  const int32_t* deps;
+  int32_t ndeps;
+  unsigned need;
 };
+
+__device__ __forceinline__ unsigned ld_acquire_gpu_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ bool stamps_ready(const HaloWait& hw) {
   for (int i = 0; i < hw.n; ++i)
     if (ld_acquire_sys(hw.flags + hw.senders[i]) < hw.stamp) return false;
+  for (int i = 0; i < hw.ndeps; ++i)
+    if (ld_acquire_gpu_u32(hw.done + hw.deps[i]) < hw.need) return false;
   return true;
 }
+
+// spin (one thread) until stamps_ready; trap after timeout_ns
+__device__ __forceinline__ void wait_ready(const HaloWait& hw, uint64_t timeout_ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (!stamps_ready(hw)) {
+    if (globaltimer_ns() - t0 > timeout_ns) __trap();
+    __nanosleep(64);
+  }
+}
+
+// Cross-step overlap of the step kernels (PDL): per-tile completion stamps and,
+// per tile, the tiles of this GPU whose cells it reads as halo (itself first).
+struct StepDeps {
+  const int32_t* off;   // [ntiles + 1] CSR over canonical tile ids
+  const int32_t* idx;
+  const int32_t* joff;  // [njobs + 1] pack job -> tiles holding its face cells
+  const int32_t* jidx;
+  unsigned* done;       // [ntiles] steps completed per tile
+  unsigned long long* end_ns;  // this step's last tile end (globaltimer), may be null
+  unsigned step;        // steps completed before this one
+  int32_t on;
+};
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
@@ -520,7 +559,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
                                           int32_t F, const double* __restrict__ cfield,
                                           int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
                                           unsigned long long* __restrict__ chunk_ns,
-                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr}) {
+                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr,
+                                                                       nullptr, nullptr, 0, 0}) {
   constexpr int R = 8;
   constexpr int TXC = 64;
   constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
@@ -671,7 +711,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     pout += ks;
   };
 
-  if (hw.n > 0) {
+  if (hw.n > 0 || hw.ndeps > 0) {
     // The tile reads strips a peer GPU stores into this GPU's receive buffer
     // during this step.  Until they have landed, run the tile's physics (which
     // reads only this GPU's U^t): the wait costs the SM nothing while the
@@ -686,7 +726,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
           // physics exhausted before the strips came: block (traps on a dead
           // peer); the longest such idle is kept out of the load measurement
           const uint64_t w0 = globaltimer_ns();
-          wait_stamps(hw.flags, hw.senders, hw.n, hw.stamp, 20ull * 1000 * 1000 * 1000);
+          wait_ready(hw, 20ull * 1000 * 1000 * 1000);
           if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
           lead_ready = true;
         } else {
@@ -792,7 +832,8 @@ struct PackArgs {
 };
 
 __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __restrict__ chunks,
-                                        int32_t nz, int32_t F, unsigned long long stamp) {
+                                        int32_t nz, int32_t F, unsigned long long stamp,
+                                        const StepDeps sd) {
   __shared__ int s_unit;
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
@@ -803,6 +844,19 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
     const int u = s_unit;
     __syncthreads();
     if (u >= total) break;
+    if (sd.on) {
+      // the face cells are U^t of this GPU's edge tiles: wait for their step
+      if (lead) {
+        const int jb = u / F;
+        const uint64_t t0 = globaltimer_ns();
+        for (int q = sd.joff[jb]; q < sd.joff[jb + 1]; ++q)
+          while (ld_acquire_gpu_u32(sd.done + sd.jidx[q]) < sd.step) {
+            if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+            __nanosleep(32);
+          }
+      }
+      __syncthreads();
+    }
     const PackJob j = pk.jobs[u / F];
     const int f = u - (u / F) * F;
     const ChunkDev& c = chunks[j.slot];
@@ -848,7 +902,7 @@ __global__ void __launch_bounds__(32 * TY, MINB)
   const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
   bool halo_ready = n_senders == 0;  // meaningful in the lead thread only
   if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
-    pack_units(pk, chunks, nz, F, stamp);
+    pack_units(pk, chunks, nz, F, stamp, StepDeps{});
   for (;;) {
     if (lead) s_next = int(atomicAdd(counter, 1u));
     __syncthreads();
@@ -860,7 +914,8 @@ __global__ void __launch_bounds__(32 * TY, MINB)
     // a tile reading a strip from another GPU before this CTA has seen the
     // strips land pre-rolls its physics while polling (tile_step)
     const bool poll = __syncthreads_or(lead && (t.pad & 1) && !halo_ready);
-    const HaloWait hw{halo_flags, senders, poll ? n_senders : 0, stamp, wait_ns};
+    const HaloWait hw{halo_flags, senders, poll ? n_senders : 0, stamp, wait_ns,
+                      nullptr, nullptr, 0, 0};
     if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
       tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
                                     chunk_ns, hw);
@@ -886,19 +941,49 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                      const unsigned long long* __restrict__ halo_flags,
                      const int32_t* __restrict__ senders, int32_t n_senders,
                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
-                     const PackArgs pk) {
+                     const PackArgs pk, const StepDeps sd) {
   __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  // cross-step overlap: let the next step's grid launch as soon as every CTA of
+  // this one has started; its tiles wait on per-tile stamps, not on this grid
+  if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
-    pack_units(pk, chunks, nz, F, stamp);
+    pack_units(pk, chunks, nz, F, stamp, sd);
   const TileDev t = tiles[blockIdx.x];
   const ChunkDev& c = chunks[t.slot];
-  const HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns};
+  const int self = t.pad >> 1;
+  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
+              nullptr, nullptr, 0, 0};
+  if (sd.on) {
+    // the tile's own columns (A, U^t) come from its previous step: block on it;
+    // its neighbours' halo cells are polled while the physics pre-rolls
+    if (lead) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
+        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    hw.done = sd.done;
+    hw.deps = sd.idx + sd.off[self] + 1;
+    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
+    hw.need = sd.step;
+  }
   if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
     tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
                                   chunk_ns, hw);
   else
     tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
                                     chunk_ns, hw);
+  if (sd.on) {
+    __syncthreads();  // every thread's U^{t+1} stores issued
+    if (lead) {
+      __threadfence();
+      st_release_gpu_u32(sd.done + self, sd.step + 1);
+      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1343,6 +1428,9 @@ __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
 
 // Diagnostic device timeline (OD_TIMELINE): one globaltimer stamp in stream order.
 __global__ void stamp_time(unsigned long long* __restrict__ slot) { *slot = globaltimer_ns(); }
+__global__ void fill_u32(unsigned* __restrict__ p, int n, unsigned v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
 __global__ void copy_u64(unsigned long long* __restrict__ dst,
                          const unsigned long long* __restrict__ src) { *dst = *src; }
 

@@ -86,6 +86,8 @@ struct StepRec {
   int ns_row = -1;                  // TIMER: row of the per-chunk ns counters
   int chunk_ev0 = -1;               // EVENTS: first event of the per-chunk pairs
   int kev0 = -1, kev1 = -1;         // TIMER: events around the step's compute kernels
+  bool ovl = false;                 // overlapped launch: wall from device stamps
+  bool ovl_chained = false;         // ... and the previous step was overlapped too
   std::vector<int32_t> slot_vps;    // resident vps at launch time (slot order)
 };
 
@@ -123,7 +125,7 @@ class Runtime {
   void rebuild_tables();
   FaceDev edge_of(const ChunkMem& s, int side, int par) const;
   int new_event();
-  void begin_window();
+  void begin_window(bool allow_overlap = true);
   void launch_step(int32_t mode, int32_t epoch_step, bool host_io);
   // waits for the window, gathers per-step walls and the K x S sample matrix
   void collect(std::vector<double>& walls, std::vector<double>& samples);
@@ -194,6 +196,21 @@ class Runtime {
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
   bool grid_launch_ = true;  // mode 5 as one CTA per tile (column_step_grid)
   void refresh_tile_order();
+  // cross-step overlap of the mode-5 step kernels (PDL + per-tile stamps;
+  // OD_OVERLAP=0 disables): tile -> same-GPU tiles whose cells it reads (itself first),
+  // pack job -> tiles holding its face cells; per-tile completed-step stamps
+  bool overlap_ = false;
+  std::vector<int32_t> deps_;  // [off (n+1) | idx | joff (nj+1) | jidx]
+  int32_t* d_deps_ = nullptr;
+  size_t d_deps_cap_ = 0;
+  int32_t dep_idx_at_ = 0, dep_joff_at_ = 0, dep_jidx_at_ = 0;
+  unsigned* d_done_ = nullptr;
+  size_t d_done_cap_ = 0;
+  unsigned long long* d_stepend_ = nullptr;  // [window steps + 1]: start, end of each step
+  unsigned* d_pcnt_ = nullptr;                // [window steps][2] fused-pack counters
+  int32_t win_cap_ = 0;
+  bool win_overlap_ = false;  // this window's steps ran overlapped
+  void build_step_deps();
   // host caches keyed on the load-field generation (set_shift bumps it)
   uint64_t field_gen_ = 0;
   std::vector<std::vector<double>> tile_work_;  // per vp, per tile of the chunk
@@ -334,6 +351,8 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // mode 5 launches one CTA per tile (column_step_grid) unless OD_GRID=0
     // selects the persistent tile-pulling kernel (column_step_persistent)
     grid_launch_ = !(std::getenv("OD_GRID") && std::string(std::getenv("OD_GRID")) == "0");
+    // cross-step overlap of the mode-5 step kernels unless OD_OVERLAP=0
+    overlap_ = !(std::getenv("OD_OVERLAP") && std::string(std::getenv("OD_OVERLAP")) == "0");
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
     phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
@@ -461,6 +480,10 @@ Runtime::~Runtime() {
   if (s0_) cudaStreamSynchronize(s0_);
   tl_dump();
   cudaFree(d_tl_);
+  cudaFree(d_deps_);
+  cudaFree(d_done_);
+  cudaFree(d_stepend_);
+  cudaFree(d_pcnt_);
   slog_dump();
   cudaFree(d_slog_);
   for (auto& m : chunks_)
@@ -732,6 +755,88 @@ static void upload(T*& dptr, size_t& cap, const std::vector<T>& h) {
   if (!h.empty()) OD_CU(cudaMemcpy(dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
 }
 
+void Runtime::build_step_deps() {
+  const size_t n = tiles4_.size();
+  std::vector<int32_t> slot_of(K(), -1);
+  for (size_t i = 0; i < resident_.size(); ++i) slot_of[resident_[i]] = int32_t(i);
+  struct Rect {
+    int32_t x0, x1, y0, y1;
+  };
+  auto rect = [&](const TileDev& t) {
+    const Sub& s = subs_[resident_[t.slot]];
+    return Rect{s.x0 + t.tx0, std::min(s.x1, s.x0 + t.tx0 + 2 * kTX), s.y0 + t.ty0,
+                std::min(s.y1, s.y0 + t.ty0 + kTY4)};
+  };
+  auto overlaps = [](const Rect& a, const Rect& b) {
+    return a.x0 < b.x1 && b.x0 < a.x1 && a.y0 < b.y1 && b.y0 < a.y1;
+  };
+  std::vector<int32_t> off(n + 1, 0), idx;
+  for (size_t t = 0; t < n; ++t) {
+    const TileDev& td = tiles4_[t];
+    off[t] = int32_t(idx.size());
+    idx.push_back(int32_t(t));
+    const Rect r = rect(td);
+    // the four one-cell halo strips of the tile
+    const Rect halo[4] = {{r.x0 - 1, r.x0, r.y0, r.y1}, {r.x1, r.x1 + 1, r.y0, r.y1},
+                          {r.x0, r.x1, r.y0 - 1, r.y0}, {r.x0, r.x1, r.y1, r.y1 + 1}};
+    const int32_t v = resident_[td.slot];
+    // candidate chunks: the tile's own and its four neighbours on this GPU
+    int32_t cand[5] = {td.slot, -1, -1, -1, -1};
+    for (int d = 0; d < 4; ++d) {
+      const int32_t nb = nbr(v, d);
+      cand[d + 1] = nb >= 0 ? slot_of[nb] : -1;
+    }
+    for (int c = 0; c < 5; ++c) {
+      if (cand[c] < 0) continue;
+      const int32_t j0 = tile4_begin_[cand[c]], j1 = j0 + tile4_count_[cand[c]];
+      for (int32_t j = j0; j < j1; ++j) {
+        if (size_t(j) == t) continue;
+        const Rect q = rect(tiles4_[j]);
+        bool hit = false;
+        for (int h = 0; h < 4 && !hit; ++h) hit = overlaps(halo[h], q);
+        if (hit && std::find(idx.begin() + off[t], idx.end(), j) == idx.end()) idx.push_back(j);
+      }
+    }
+  }
+  off[n] = int32_t(idx.size());
+  std::vector<int32_t> joff(jobs_.size() + 1, 0), jidx;
+  for (size_t jb = 0; jb < jobs_.size(); ++jb) {
+    joff[jb] = int32_t(jidx.size());
+    const PackJob& pj = jobs_[jb];
+    const Sub& s = subs_[resident_[pj.slot]];
+    const int32_t j0 = tile4_begin_[pj.slot], j1 = j0 + tile4_count_[pj.slot];
+    for (int32_t j = j0; j < j1; ++j) {
+      const TileDev& tj = tiles4_[j];
+      const bool edge = (pj.side == kLeft && tj.tx0 == 0) ||
+                        (pj.side == kRight && tj.tx0 + 2 * kTX >= s.w()) ||
+                        (pj.side == kTop && tj.ty0 == 0) ||
+                        (pj.side == kBottom && tj.ty0 + kTY4 >= s.h());
+      if (edge) jidx.push_back(j);
+    }
+  }
+  joff[jobs_.size()] = int32_t(jidx.size());
+  deps_.clear();
+  deps_.insert(deps_.end(), off.begin(), off.end());
+  dep_idx_at_ = int32_t(deps_.size());
+  deps_.insert(deps_.end(), idx.begin(), idx.end());
+  dep_joff_at_ = int32_t(deps_.size());
+  deps_.insert(deps_.end(), joff.begin(), joff.end());
+  dep_jidx_at_ = int32_t(deps_.size());
+  deps_.insert(deps_.end(), jidx.begin(), jidx.end());
+  upload(d_deps_, d_deps_cap_, deps_);
+  if (n > d_done_cap_) {
+    OD_CU(cudaStreamSynchronize(s0_));
+    cudaFree(d_done_);
+    d_done_cap_ = std::max<size_t>(n, tiles4_cap_);
+    OD_CU(cudaMalloc(&d_done_, d_done_cap_ * sizeof(unsigned)));
+  }
+  // every tile has completed every step launched so far (the stream drained)
+  if (n > 0) {
+    fill_u32<<<64, 256, 0, s0_>>>(d_done_, int(n), unsigned(st_.steps));
+    OD_CU(cudaGetLastError());
+  }
+}
+
 void Runtime::rebuild_tables() {
   const double r0 = now_s();
   resident_.clear();
@@ -782,7 +887,8 @@ void Runtime::rebuild_tables() {
       for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) {
         const bool needs = (remote[kLeft] && tx == 0) || (remote[kRight] && tx + 2 * kTX >= s.w()) ||
                            (remote[kTop] && ty == 0) || (remote[kBottom] && ty + kTY4 >= s.h());
-        tiles4_.push_back(TileDev{i, tx, ty, needs ? 1 : 0});
+        // pad: bit 0 = reads a remote strip, bits 1.. = canonical tile id
+        tiles4_.push_back(TileDev{i, tx, ty, (needs ? 1 : 0) | (int32_t(tiles4_.size()) << 1)});
       }
     tile4_count_[i] = int32_t(tiles4_.size()) - tile4_begin_[i];
   }
@@ -933,6 +1039,7 @@ void Runtime::rebuild_tables() {
     ns_rows_ = 0;
   }
   st_.resident_chunks = nres;
+  build_step_deps();
   if (trace_on())
     fprintf(stderr, "[od rank %d] rebuild: tiles %.2f ms, exchange %.2f ms, chunk tables %.2f ms\n",
             rank_, (r1 - r0) * 1e3, (r2 - r1) * 1e3, (now_s() - r2) * 1e3);
@@ -1007,10 +1114,41 @@ int Runtime::new_event() {
   return ev_used_++;
 }
 
-void Runtime::begin_window() {
+void Runtime::begin_window(bool allow_overlap) {
   window_.clear();
   ev_used_ = 0;
   ns_used_ = 0;
+  win_overlap_ = overlap_ && allow_overlap && cfg_.overlap == 5 && grid_launch_ && !d_tl_ &&
+                 (cfg_.measure == OD_MEASURE_TIMER || cfg_.measure == OD_MEASURE_TIMER_RAW);
+  if (win_overlap_) {
+    const int32_t S = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
+    if (win_cap_ < S) {
+      OD_CU(cudaStreamSynchronize(s0_));
+      cudaFree(d_stepend_);
+      cudaFree(d_pcnt_);
+      win_cap_ = S;
+      OD_CU(cudaMalloc(&d_stepend_, size_t(2 * S) * sizeof(unsigned long long)));
+      OD_CU(cudaMalloc(&d_pcnt_, size_t(2 * S) * sizeof(unsigned)));
+    }
+    OD_CU(cudaMemsetAsync(d_stepend_, 0, size_t(2 * win_cap_) * sizeof(unsigned long long), s0_));
+    OD_CU(cudaMemsetAsync(d_pcnt_, 0, size_t(2 * win_cap_) * sizeof(unsigned), s0_));
+    // every tile is current with every step launched so far (earlier steps may
+    // have run without the per-tile stamps)
+    if (!tiles4_.empty()) {
+      fill_u32<<<64, 256, 0, s0_>>>(d_done_, int(tiles4_.size()), unsigned(st_.steps));
+      OD_CU(cudaGetLastError());
+    }
+    // measured rows zeroed up front: no per-step memset between the kernels
+    if (ns_cols_ > 0) {
+      if (ns_rows_ < S) {
+        OD_CU(cudaStreamSynchronize(s0_));
+        cudaFree(d_ns_);
+        ns_rows_ = S;
+        OD_CU(cudaMalloc(&d_ns_, size_t(ns_rows_) * ns_cols_ * sizeof(unsigned long long)));
+      }
+      OD_CU(cudaMemsetAsync(d_ns_, 0, size_t(ns_rows_) * ns_cols_ * sizeof(unsigned long long), s0_));
+    }
+  }
   prof_j_.clear();
   prof_p_.clear();
   prof_f_.clear();
@@ -1029,8 +1167,18 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   const bool timer = host_io || (mode == kSync && (cfg_.measure == OD_MEASURE_TIMER ||
                                                     cfg_.measure == OD_MEASURE_TIMER_RAW ||
                                                     cfg_.measure == OD_MEASURE_OPS));
-  r.ev_begin = new_event();
-  OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
+  // overlapped step: launched with programmatic dependent launch right behind
+  // the previous step kernel; no stream operation may sit between them
+  r.ovl = win_overlap_ && !host_io && !tiles4_.empty() && (mode == kAsync || timer) &&
+          !(cfg_.measure == OD_MEASURE_TIMER_RAW && false);
+  if (r.ovl && order_dirty_) refresh_tile_order();  // (its upload breaks the chain once)
+  r.ovl_chained = r.ovl && !window_.empty() && window_.back().ovl;
+  if (!r.ovl) {
+    r.ev_begin = new_event();
+    OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
+  } else if (!r.ovl_chained) {
+    stamp_time<<<1, 1, 0, s0_>>>(d_stepend_ + 2 * epoch_step);  // start of a chain
+  }
   tl_mark(0);
 
   const double* cfield = d_cbase_;
@@ -1064,7 +1212,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
     r.ns_row = ns_used_++;
     ns = d_ns_ + size_t(r.ns_row) * ns_cols_;
-    OD_CU(cudaMemsetAsync(ns, 0, size_t(ns_cols_) * sizeof(unsigned long long), s0_));
+    if (!r.ovl)  // overlapped windows zero their rows up front
+      OD_CU(cudaMemsetAsync(ns, 0, size_t(ns_cols_) * sizeof(unsigned long long), s0_));
   }
 
   // boundaries of chunks that border another GPU
@@ -1074,7 +1223,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     // pack straight into the neighbours' receive buffers over NVLink, publish
     // the step, then wait for the neighbours' strips of this step
     int e0 = -1, e1 = -1, e2 = -1;
-    if (profiling_) {
+    const bool prof_x = profiling_ && !r.ovl;
+    if (prof_x) {
       e0 = new_event();
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
@@ -1090,7 +1240,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       ++st_.kernel_launches;
       for (int q = 0; q < world_; ++q) st_.halo_bytes_sent += send_cnt_[q] * int64_t(sizeof(double));
     }
-    if (profiling_) {
+    if (prof_x) {
       e1 = new_event();
       OD_CU(cudaEventRecord(events_[e1], s0_));
     }
@@ -1104,7 +1254,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       OD_CU(cudaGetLastError());
       ++st_.kernel_launches;
     }
-    if (profiling_) {
+    if (prof_x) {
       e2 = new_event();
       OD_CU(cudaEventRecord(events_[e2], s0_));
       prof_pack_.push_back({e0, e1});
@@ -1149,7 +1299,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   const bool slog = d_slog_ && timer && long(st_.steps) == slog_step_;
   if (slog) slog_arm(true);
   const dim3 blk(kTX, kTY);
-  if (timer) {
+  if (timer && !r.ovl) {
     r.kev0 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev0], s0_));
   }
@@ -1187,11 +1337,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   } else if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 5) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
-    if (profiling_) {
+    const bool prof_f = profiling_ && !r.ovl;
+    if (prof_f) {
       e0 = new_event();
       OD_CU(cudaEventRecord(events_[e0], s0_));
     }
-    OD_CU(cudaMemsetAsync(d_counter_, 0, 3 * sizeof(unsigned int), s0_));
+    if (!r.ovl) OD_CU(cudaMemsetAsync(d_counter_, 0, 3 * sizeof(unsigned int), s0_));
     tl_mark(2);
     const int nt = int(tiles4_.size());
     const int grid = std::min(nt, persist_grid_);
@@ -1206,7 +1357,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       pk.par = par;
       pk.n_notify = n_notify_;
       pk.my_rank = rank_;
-      pk.counters = d_counter_ + 1;
+      pk.counters = r.ovl ? d_pcnt_ + 2 * epoch_step : d_counter_ + 1;
       pk.peer_flags = d_peer_flags_;
       pk.notify = d_notify_;
     }
@@ -1227,20 +1378,47 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       // one CTA per tile, heaviest first; the fused pack rides on the last
       // CTAs of the first wave (the lightest tiles of it)
       if (pk.njobs > 0) pk.first = std::max(0, std::min(nt, persist_grid_) - pk.ctas);
+      StepDeps sd{};
+      if (r.ovl) {
+        sd.off = d_deps_;
+        sd.idx = d_deps_ + dep_idx_at_;
+        sd.joff = d_deps_ + dep_joff_at_;
+        sd.jidx = d_deps_ + dep_jidx_at_;
+        sd.done = d_done_;
+        sd.end_ns = d_stepend_ + 2 * epoch_step + 1;
+        sd.step = unsigned(st_.steps);
+        sd.on = 1;
+      }
+      // overlapped steps: programmatic dependent launch, so this grid starts
+      // while the previous step's last tiles drain (tiles wait on per-tile stamps)
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(unsigned(nt));
+      lc.blockDim = blk4;
+      lc.dynamicSmemBytes = 0;
+      lc.stream = s0_;
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      la[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = la;
+      lc.numAttrs = r.ovl ? 1 : 0;
+      const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
+      const ChunkDev* chk = d_chunks_[par];
       if (timer)
-        column_step_grid<4, kFusedPrefetch, true, 5><<<nt, blk4, 0, s0_>>>(
-            d_chunks_[par], d_tiles4s_[tiles4s_cur_], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend, stamp,
-            ns + (ns_cols_ - 1), pk);
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 5>, chk, tl4,
+                                 cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp,
+                                 ns + (ns_cols_ - 1), pk, sd));
       else
-        column_step_grid<4, kFusedPrefetch, false, 5><<<nt, blk4, 0, s0_>>>(
-            d_chunks_[par], d_tiles4s_[tiles4s_cur_], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, stamp,
-            tl_wait(), pk);
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 5>, chk, tl4,
+                                 cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, (unsigned long long*)nullptr,
+                                 (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
+                                 nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
     } else if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
-    if (profiling_) {
+    if (prof_f) {
       e1 = new_event();
       OD_CU(cudaEventRecord(events_[e1], s0_));
       prof_f_.push_back({e0, e1});
@@ -1345,7 +1523,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       st_.physics_launches += 1;
     }
   }
-  if (timer) {
+  if (timer && !r.ovl) {
     r.kev1 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev1], s0_));
   }
@@ -1358,8 +1536,10 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     OD_CU(cudaMemcpyAsync(h_loads_dst_, ns, size_t(2 * nres) * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s0_));
   }
-  r.ev_end = new_event();
-  OD_CU(cudaEventRecord(events_[r.ev_end], s0_));
+  if (!r.ovl) {
+    r.ev_end = new_event();
+    OD_CU(cudaEventRecord(events_[r.ev_end], s0_));
+  }
   parity_ ^= 1;
   ++st_.steps;
   r.host_launch_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1383,12 +1563,32 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
     OD_CU(cudaMemcpy(ns.data(), d_ns_, ns.size() * sizeof(unsigned long long),
                      cudaMemcpyDeviceToHost));
   }
+  // overlapped steps: device stamps (chain start, last tile end per step)
+  std::vector<unsigned long long> stamps;
+  if (std::any_of(window_.begin(), window_.end(), [](const StepRec& r) { return r.ovl; })) {
+    stamps.resize(size_t(2) * win_cap_);
+    OD_CU(cudaMemcpy(stamps.data(), d_stepend_, stamps.size() * sizeof(unsigned long long),
+                     cudaMemcpyDeviceToHost));
+  }
   // local rows: [S*K samples | S walls]
   const size_t row = size_t(S) * Kv + S;
   std::vector<double> local(row, 0.0);
   for (int32_t s = 0; s < S; ++s) {
     const StepRec& r = window_[s];
-    local[size_t(S) * Kv + s] = elapsed_s(events_[r.ev_begin], events_[r.ev_end]);
+    if (r.ovl) {
+      const int es = r.epoch_step;
+      const unsigned long long end = stamps[2 * es + 1];
+      const unsigned long long start =
+          r.ovl_chained && es > 0 ? stamps[2 * (es - 1) + 1] : stamps[2 * es];
+      const double w = end > start ? double(end - start) * 1e-9 : 0.0;
+      local[size_t(S) * Kv + s] = w;
+      if (profiling_) {
+        st_.fused_ms += w * 1e3;  // the step's kernel time, overlap included
+        st_.fused_timed += 1;
+      }
+    } else {
+      local[size_t(S) * Kv + s] = elapsed_s(events_[r.ev_begin], events_[r.ev_end]);
+    }
     // TIMER: the chunk's processor-sharing SM time (sum over its tiles of
     // integral dt / resident CTAs on the tile's SM) divided by the SM count, in
     // seconds of the whole GPU.  A GPU's samples sum to its mean SM busy time;
@@ -1585,6 +1785,10 @@ void Runtime::advance(int32_t n, int32_t* epochs_done) {
 void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads) {
   if (n < 0) throw ValidationError("negative step count");
   const size_t cells = size_t(cfg_.nx) * cfg_.ny;
+  if (win_overlap_) {
+    // host-staged steps are not overlapped: drain the window's overlapped steps
+    win_overlap_ = false;
+  }
   if (!h_cstage_[0]) {
     for (int b = 0; b < 2; ++b) {
       OD_CU(cudaMallocHost(&h_cstage_[b], cells * sizeof(double)));
@@ -1610,7 +1814,7 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
   // and are read once the stream has drained (epoch ends drain it anyway)
   std::vector<std::vector<int32_t>> step_vps(host_loads ? n : 0);
   for (int32_t i = 0; i < n; ++i) {
-    if (cur_step_ == 0) begin_window();
+    if (cur_step_ == 0) begin_window(false);
     advance_advection(cur_epoch_, cur_step_);
     h_loads_dst_ = h_loads_ + size_t(i) * row_words;
     launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true);
