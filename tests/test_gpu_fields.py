@@ -153,3 +153,20 @@ def test_measured_loads_track_work_and_balancing_helps():
         assert r1.imbalance_before > 1.3 and r1.plan.moves
         r2 = eng.run_epoch(2)
         assert r2.imbalance_before < 1.05
+
+
+@pytest.mark.parametrize("env", [{"OD_OVERLAP": "0"}, {"OD_OVERLAP": "1"},
+                                 {"OD_GRID": "0", "OD_OVERLAP": "0"},
+                                 {"OD_FIRSTWAVE": "0"}, {"OD_OVERLAP": "1", "OD_ORDER": "spt"}])
+def test_step_kernel_variants_bitwise(env, monkeypatch):
+    """The mode-5 launch variants (cross-step overlap on/off, one CTA per tile
+    or persistent, queue orders) compute identical fields, with multi-tile
+    chunks, advection and balancing moves across several epochs."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, adv=(35, 1, 3), n_inner=7, overlap=5,
+                nodes=1, ppn=3, threshold=1.0)
+    U, A, _ = device_fields(cfg, 12)
+    Uo, Ao = oracle_fields(cfg, 12)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
