@@ -217,6 +217,11 @@ struct StepDeps {
   unsigned long long* end_ns;  // this step's last tile end (globaltimer), may be null
   unsigned step;        // steps completed before this one
   int32_t on;
+  // host-facing steps: the CTA finishing the step's last tile writes the step's
+  // per-chunk measurement row straight into mapped pinned host memory
+  unsigned* tile_cnt;   // tiles of this step finished so far
+  int32_t ntiles, res_words;
+  unsigned long long* res_dst;
 };
 
 __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
@@ -978,10 +983,22 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                                     chunk_ns, hw);
   if (sd.on) {
     __syncthreads();  // every thread's U^{t+1} stores issued
+    __shared__ int s_last;
     if (lead) {
       __threadfence();
       st_release_gpu_u32(sd.done + self, sd.step + 1);
       if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
+      s_last = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
+    }
+    if (sd.res_dst) {
+      __syncthreads();
+      if (s_last) {
+        __threadfence();  // every tile's shares are in
+        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
+          sd.res_dst[i] = __ldcg(chunk_ns + i);
+        __threadfence_system();
+      }
     }
   }
 }

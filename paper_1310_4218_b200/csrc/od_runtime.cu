@@ -164,6 +164,11 @@ class Runtime {
   unsigned long long* h_loads_ = nullptr;  // pinned [rows][2 * K]
   size_t h_loads_rows_ = 0;
   unsigned long long* h_loads_dst_ = nullptr;  // row for the step being launched
+  // overlapped host-facing steps: per epoch step a mapped pinned field buffer
+  // the step kernel reads straight over the host link, and mapped result rows
+  std::vector<double*> h_ring_, d_ring_;
+  unsigned long long* d_loads_map_ = nullptr;  // device view of h_loads_ (mapped)
+  unsigned long long* d_loads_dst_ = nullptr;
   std::vector<ChunkMem> chunks_;  // indexed by vp; base == nullptr if not local
   std::multimap<size_t, double*> pool_;  // individually allocated (fallback) buffers
   double* slab_ = nullptr;                // preallocated chunk slots
@@ -500,6 +505,7 @@ Runtime::~Runtime() {
     if (cstage_ev_[b]) cudaEventDestroy(cstage_ev_[b]);
   }
   if (h_loads_) cudaFreeHost(h_loads_);
+  for (double* p : h_ring_) cudaFreeHost(p);
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
   cudaFree(d_tiles_);
@@ -1128,10 +1134,10 @@ void Runtime::begin_window(bool allow_overlap) {
       cudaFree(d_pcnt_);
       win_cap_ = S;
       OD_CU(cudaMalloc(&d_stepend_, size_t(2 * S) * sizeof(unsigned long long)));
-      OD_CU(cudaMalloc(&d_pcnt_, size_t(2 * S) * sizeof(unsigned)));
+      OD_CU(cudaMalloc(&d_pcnt_, size_t(4 * S) * sizeof(unsigned)));
     }
     OD_CU(cudaMemsetAsync(d_stepend_, 0, size_t(2 * win_cap_) * sizeof(unsigned long long), s0_));
-    OD_CU(cudaMemsetAsync(d_pcnt_, 0, size_t(2 * win_cap_) * sizeof(unsigned), s0_));
+    OD_CU(cudaMemsetAsync(d_pcnt_, 0, size_t(4 * win_cap_) * sizeof(unsigned), s0_));
     // every tile is current with every step launched so far (earlier steps may
     // have run without the per-tile stamps)
     if (!tiles4_.empty()) {
@@ -1169,8 +1175,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
                                                     cfg_.measure == OD_MEASURE_OPS));
   // overlapped step: launched with programmatic dependent launch right behind
   // the previous step kernel; no stream operation may sit between them
-  r.ovl = win_overlap_ && !host_io && !tiles4_.empty() && (mode == kAsync || timer) &&
-          !(cfg_.measure == OD_MEASURE_TIMER_RAW && false);
+  r.ovl = win_overlap_ && (!host_io || int32_t(d_ring_.size()) > epoch_step) &&
+          !tiles4_.empty() && (mode == kAsync || timer);
   if (r.ovl && order_dirty_) refresh_tile_order();  // (its upload breaks the chain once)
   r.ovl_chained = r.ovl && !window_.empty() && window_.back().ovl;
   if (!r.ovl) {
@@ -1183,8 +1189,14 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
 
   const double* cfield = d_cbase_;
   int32_t shift = shift_ % cfg_.ny;
-  if (host_io) {
-    // the reference keeps the shifted load field on the host (engine.hpp:337-342)
+  if (host_io && r.ovl) {
+    // the reference keeps the shifted load field on the host (engine.hpp:337-342);
+    // overlapped: the step kernel reads this step's mapped pinned copy over the
+    // host link (8 B per column per step, no copy operation between the kernels)
+    std::memcpy(h_ring_[epoch_step], field_.c.data(), field_.c.size() * sizeof(double));
+    cfield = d_ring_[epoch_step];
+    shift = 0;
+  } else if (host_io) {
     const int b = cstage_cur_ ^= 1;
     OD_CU(cudaEventSynchronize(cstage_ev_[b]));  // the copy two steps ago has left it
     std::memcpy(h_cstage_[b], field_.c.data(), field_.c.size() * sizeof(double));
@@ -1357,7 +1369,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       pk.par = par;
       pk.n_notify = n_notify_;
       pk.my_rank = rank_;
-      pk.counters = r.ovl ? d_pcnt_ + 2 * epoch_step : d_counter_ + 1;
+      pk.counters = r.ovl ? d_pcnt_ + 4 * epoch_step : d_counter_ + 1;
       pk.peer_flags = d_peer_flags_;
       pk.notify = d_notify_;
     }
@@ -1388,6 +1400,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
         sd.end_ns = d_stepend_ + 2 * epoch_step + 1;
         sd.step = unsigned(st_.steps);
         sd.on = 1;
+        if (host_io && nres > 0) {
+          sd.tile_cnt = d_pcnt_ + 4 * epoch_step + 2;
+          sd.ntiles = nt;
+          sd.res_words = 2 * nres;
+          sd.res_dst = d_loads_dst_;
+        }
       }
       // overlapped steps: programmatic dependent launch, so this grid starts
       // while the previous step's last tiles drain (tiles wait on per-tile stamps)
@@ -1531,8 +1549,9 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   if (slog) slog_arm(false);
   if (timer && ns && tl_wait()) copy_u64<<<1, 1, 0, s0_>>>(tl_wait(), ns + (ns_cols_ - 1));
   if (d_tl_ && tl_n_ < tl_cap_) ++tl_n_;
-  if (host_io && nres > 0) {
-    // the step's per-chunk device times back to the host
+  if (host_io && nres > 0 && !r.ovl) {
+    // the step's per-chunk device times back to the host (overlapped steps:
+    // written by the kernel's last CTA into the mapped row)
     OD_CU(cudaMemcpyAsync(h_loads_dst_, ns, size_t(2 * nres) * sizeof(unsigned long long),
                           cudaMemcpyDeviceToHost, s0_));
   }
@@ -1785,9 +1804,17 @@ void Runtime::advance(int32_t n, int32_t* epochs_done) {
 void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads) {
   if (n < 0) throw ValidationError("negative step count");
   const size_t cells = size_t(cfg_.nx) * cfg_.ny;
-  if (win_overlap_) {
-    // host-staged steps are not overlapped: drain the window's overlapped steps
-    win_overlap_ = false;
+  const int32_t Sw = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
+  if (int32_t(h_ring_.size()) < Sw) {
+    OD_CU(cudaStreamSynchronize(s0_));
+    while (int32_t(h_ring_.size()) < Sw) {
+      double* h = nullptr;
+      double* d = nullptr;
+      OD_CU(cudaHostAlloc(reinterpret_cast<void**>(&h), cells * sizeof(double), cudaHostAllocMapped));
+      OD_CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0));
+      h_ring_.push_back(h);
+      d_ring_.push_back(d);
+    }
   }
   if (!h_cstage_[0]) {
     for (int b = 0; b < 2; ++b) {
@@ -1801,7 +1828,9 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
     OD_CU(cudaStreamSynchronize(s0_));
     if (h_loads_) cudaFreeHost(h_loads_);
     h_loads_rows_ = size_t(std::max(n, 1));
-    OD_CU(cudaMallocHost(&h_loads_, h_loads_rows_ * row_words * sizeof(unsigned long long)));
+    OD_CU(cudaHostAlloc(reinterpret_cast<void**>(&h_loads_),
+                        h_loads_rows_ * row_words * sizeof(unsigned long long), cudaHostAllocMapped));
+    OD_CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_loads_map_), h_loads_, 0));
   }
   if (host_c && n_fields > 0) {
     // the caller's load multiplier field replaces the base field
@@ -1814,9 +1843,10 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
   // and are read once the stream has drained (epoch ends drain it anyway)
   std::vector<std::vector<int32_t>> step_vps(host_loads ? n : 0);
   for (int32_t i = 0; i < n; ++i) {
-    if (cur_step_ == 0) begin_window(false);
+    if (cur_step_ == 0) begin_window();
     advance_advection(cur_epoch_, cur_step_);
     h_loads_dst_ = h_loads_ + size_t(i) * row_words;
+    d_loads_dst_ = d_loads_map_ + size_t(i) * row_words;
     launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true);
     if (host_loads) step_vps[i] = window_.back().slot_vps;
     ++global_step_;
