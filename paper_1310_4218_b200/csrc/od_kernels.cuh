@@ -875,9 +875,28 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
     }
     double* out = pk.peer_base[j.peer] + int64_t(pk.par) * pk.half_elems + j.rdst +
                   int64_t(f) * nz * j.lenp;
-    for (int k = 0; k < nz; ++k)
-      for (int e = tid; e < j.len; e += nthr)
-        out[int64_t(k) * j.lenp + e] = base[off + k * c.kstride + e * es];
+    // (level, position) flattened; 8 independent loads in flight per thread
+    const int n = nz * j.len;
+    constexpr int U = 8;
+    for (int i0 = tid; i0 < n; i0 += U * nthr) {
+      double v[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int i = i0 + q * nthr;
+        if (i < n) {
+          const int k = i / j.len, e = i - k * j.len;
+          v[q] = __ldcs(base + off + k * c.kstride + int64_t(e) * es);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int i = i0 + q * nthr;
+        if (i < n) {
+          const int k = i / j.len, e = i - k * j.len;
+          out[int64_t(k) * j.lenp + e] = v[q];
+        }
+      }
+    }
     __threadfence_system();
     __syncthreads();
     if (lead && atomicAdd(&pk.counters[1], 1u) == unsigned(total - 1)) {
@@ -952,9 +971,13 @@ __global__ void __launch_bounds__(32 * TY, MINB)
   // cross-step overlap: let the next step's grid launch as soon as every CTA of
   // this one has started; its tiles wait on per-tile stamps, not on this grid
   if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
-    pack_units(pk, chunks, nz, F, stamp, sd);
-  const TileDev t = tiles[blockIdx.x];
+  // the first pk.ctas CTAs only pack this step's boundary strips into the
+  // peers' buffers (dynamically shared units) and exit; tiles start behind them
+  if (int(blockIdx.x) < pk.ctas) {
+    if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
+    return;
+  }
+  const TileDev t = tiles[blockIdx.x - pk.ctas];
   const ChunkDev& c = chunks[t.slot];
   const int self = t.pad >> 1;
   HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,

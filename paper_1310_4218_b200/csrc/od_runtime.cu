@@ -1389,7 +1389,13 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     if (grid_launch_) {
       // one CTA per tile, heaviest first; the fused pack rides on the last
       // CTAs of the first wave (the lightest tiles of it)
-      if (pk.njobs > 0) pk.first = std::max(0, std::min(nt, persist_grid_) - pk.ctas);
+      // pack-only CTAs ahead of the tiles (column_step_grid)
+      if (pk.njobs > 0) {
+        pk.first = 0;
+        pk.ctas = std::min(pack_ctas_, int(pk.njobs) * cfg_.fields);
+      } else {
+        pk.ctas = 0;
+      }
       StepDeps sd{};
       if (r.ovl) {
         sd.off = d_deps_;
@@ -1410,7 +1416,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       // overlapped steps: programmatic dependent launch, so this grid starts
       // while the previous step's last tiles drain (tiles wait on per-tile stamps)
       cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(unsigned(nt));
+      lc.gridDim = dim3(unsigned(nt + pk.ctas));
       lc.blockDim = blk4;
       lc.dynamicSmemBytes = 0;
       lc.stream = s0_;
