@@ -38,7 +38,10 @@ def parse_args():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=40)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=10,
+                   help="untimed steps; the default is one epoch of the cfg3/cfg4 window "
+                        "(6 async + 4 sync steps), so the timed steps are whole epochs "
+                        "after the first balancing decision")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", default="cfg4")
     p.add_argument("--n-inner", type=int, default=None)
