@@ -346,15 +346,17 @@ def main():
     if world > 1:
         per_rank = [None] * world
         dist.all_gather_object(per_rank, mine)
-    balanced = [h for h in hist if h["strategy"] >= 0 and h["n_moves"] > 0]
     post_lb = None
-    if balanced:
-        last = balanced[-1]
-        nxt = [h for h in hist if h["epoch"] == last["epoch"] + 1]
+    full = eng.epoch_history()
+    balanced_all = [h for h in full if h["n_moves"] > 0]
+    if balanced_all:
+        # the first (largest) rebalance, which may fall in the warm-up epoch
+        last = balanced_all[0]
+        nxt = [h for h in full if h["epoch"] == last["epoch"] + 1]
         post_lb = {"predicted": last["imbalance_after"],
                    "measured_next_epoch": nxt[0]["imbalance_before"] if nxt else None,
                    "before": last["imbalance_before"], "moves": last["n_moves"]}
-    eng_imb = [h["imbalance_before"] for h in hist]
+    eng_imb = [h["imbalance_before"] for h in full]  # every epoch so far, warm-up included
 
     # end to end through the host-facing C ABI call: per step H2D of the
     # step's load multiplier field (pinned) and D2H of per-chunk loads
