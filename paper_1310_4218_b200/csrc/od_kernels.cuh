@@ -546,6 +546,56 @@ __device__ __forceinline__ void physics_advance(ColumnState& s, int budget) {
   }
 }
 
+// Two columns with the same trip count advance in lockstep (equal budgets from
+// the same quota), so their trip boundaries coincide: handle both chains
+// together, interleaved, across the boundary -- the same operations per
+// chain as physics_advance, in the same order.
+__device__ __forceinline__ void physics_advance_pair(ColumnState& s0, ColumnState& s1,
+                                                     int budget) {
+  while (budget > 0 && s0.t <= s0.T) {
+    if (s0.i == 0) {
+      const double b0 = s0.bn, b1 = s1.bn;
+      const double hb0 = __dmul_rn(0.5, b0), hb1 = __dmul_rn(0.5, b1);
+      s0.eb = __fma_rn(b0, kEps, kEps);
+      s1.eb = __fma_rn(b1, kEps, kEps);
+      s0.y = __fma_rn(0.5, s0.a, hb0);
+      s1.y = __fma_rn(0.5, s1.a, hb1);
+      s0.i = s1.i = 1;
+      --budget;
+      const int ln = s0.l + 1 == s0.nz ? 0 : s0.l + 1;
+      if (s0.t < s0.T) {
+        s0.bn = s0.B[ln * s0.ks];
+        s1.bn = s1.B[ln * s1.ks];
+      }
+    }
+    const int m = min(budget, s0.n_inner + 1 - s0.i);
+    double y0 = s0.y, y1 = s1.y;
+    const double e0 = s0.eb, e1 = s1.eb;
+#pragma unroll 4
+    for (int j = 0; j < m; ++j) {
+      const double u0 = __fma_rn(-y0, y0, y0);
+      const double u1 = __fma_rn(-y1, y1, y1);
+      y0 = __fma_rn(kR, u0, e0);
+      y1 = __fma_rn(kR, u1, e1);
+    }
+    s0.y = y0;
+    s1.y = y1;
+    s0.i += m;
+    s1.i += m;
+    budget -= m;
+    if (s0.i == s0.n_inner + 1) {
+      s0.a = y0;
+      s1.a = y1;
+      s0.A[s0.l * s0.ks] = y0;
+      s1.A[s1.l * s1.ks] = y1;
+      s0.l = s1.l = s0.l + 1 == s0.nz ? 0 : s0.l + 1;
+      ++s0.t;
+      ++s1.t;
+      s0.i = s1.i = 0;
+    }
+  }
+}
+
 // Calls of physics_advance(s, budget) that stay inside the current trip.
 __device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
   return (s.i > 0 && budget > 0 && s.t <= s.T) ? (s.n_inner - s.i) / budget : 0;
@@ -671,6 +721,11 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       s0.i += b0;
       s1.i += b0;
       --fast;
+      return;
+    }
+    if (ncell == 2 && b0 == b1 && s0.T == s1.T) {
+      physics_advance_pair(s0, s1, b0);  // lockstep columns: keep both chains interleaved
+      fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
       return;
     }
     if (ncell >= 1) physics_advance(s0, b0);
