@@ -200,6 +200,8 @@ class Runtime {
   int sms_ = 1;
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
   bool grid_launch_ = true;  // mode 5 as one CTA per tile (column_step_grid)
+  int grid_minb_ = 5;        // OD_GRID_MINB=6: 6 CTAs/SM build (80 registers)
+  size_t grid_pad_smem_ = 0;  // OD_GRID_SMEM: unused dynamic smem per CTA (caps CTAs/SM)
   void refresh_tile_order();
   // cross-step overlap of the mode-5 step kernels (PDL + per-tile stamps;
   // OD_OVERLAP=0 disables): tile -> same-GPU tiles whose cells it reads (itself first),
@@ -356,6 +358,8 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // mode 5 launches one CTA per tile (column_step_grid) unless OD_GRID=0
     // selects the persistent tile-pulling kernel (column_step_persistent)
     grid_launch_ = !(std::getenv("OD_GRID") && std::string(std::getenv("OD_GRID")) == "0");
+    grid_minb_ = std::getenv("OD_GRID_MINB") ? std::atoi(std::getenv("OD_GRID_MINB")) : 5;
+    grid_pad_smem_ = std::getenv("OD_GRID_SMEM") ? size_t(std::atol(std::getenv("OD_GRID_SMEM"))) : 0;
     // cross-step overlap of the mode-5 step kernels unless OD_OVERLAP=0
     overlap_ = !(std::getenv("OD_OVERLAP") && std::string(std::getenv("OD_OVERLAP")) == "0");
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
@@ -1418,7 +1422,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       cudaLaunchConfig_t lc{};
       lc.gridDim = dim3(unsigned(nt + pk.ctas));
       lc.blockDim = blk4;
-      lc.dynamicSmemBytes = 0;
+      lc.dynamicSmemBytes = grid_pad_smem_;  // (occupancy experiments: OD_GRID_SMEM)
       lc.stream = s0_;
       cudaLaunchAttribute la[1];
       la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1427,18 +1431,33 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       lc.numAttrs = r.ovl ? 1 : 0;
       const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
       const ChunkDev* chk = d_chunks_[par];
-      if (timer)
-        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 5>, chk, tl4,
-                                 cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                 cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
-                                 (const int32_t*)d_senders_, nsend, stamp,
-                                 ns + (ns_cols_ - 1), pk, sd));
-      else
-        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 5>, chk, tl4,
-                                 cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                 cfg_.n_inner, (unsigned long long*)nullptr,
-                                 (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
-                                 nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
+      if (grid_minb_ == 6) {
+        if (timer)
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 6>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   ns + (ns_cols_ - 1), pk, sd));
+        else
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 6>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, (unsigned long long*)nullptr,
+                                   (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
+                                   nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
+} else {
+        if (timer)
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 5>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   ns + (ns_cols_ - 1), pk, sd));
+        else
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 5>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, (unsigned long long*)nullptr,
+                                   (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
+                                   nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
+}
     } else if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
 #undef OD_LAUNCH_PS
     OD_CU(cudaGetLastError());
