@@ -1140,13 +1140,68 @@ __device__ __forceinline__ int chain_fast(const Chain& q, int budget, int n_inne
   return (q.i > 0 && q.r > 0 && budget > 0) ? (n_inner - q.i) / budget : 0;
 }
 
+// Four chains with equal trip counts advance in lockstep: cross trip
+// boundaries with all four interleaved (same operations per chain as
+// chain_advance, in the same order).
+__device__ __forceinline__ void chain_advance4(Chain* q, int budget, const double* B,
+                                               double* A, const int64_t* off, int nz,
+                                               int64_t ks, int n_inner) {
+  while (budget > 0 && q[0].r > 0) {
+    if (q[0].i == 0) {
+      const int64_t lo = int64_t(q[0].l) * ks;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double b = B[off[j] + lo];
+        q[j].eb = __fma_rn(b, kEps, kEps);
+        q[j].y = __fma_rn(0.5, q[j].y, __dmul_rn(0.5, b));
+        q[j].i = 1;
+      }
+      --budget;
+    }
+    const int m = min(budget, n_inner + 1 - q[0].i);
+    double y0 = q[0].y, y1 = q[1].y, y2 = q[2].y, y3 = q[3].y;
+    const double e0 = q[0].eb, e1 = q[1].eb, e2 = q[2].eb, e3 = q[3].eb;
+#pragma unroll 2
+    for (int j = 0; j < m; ++j) {
+      const double u0 = __fma_rn(-y0, y0, y0);
+      const double u1 = __fma_rn(-y1, y1, y1);
+      const double u2 = __fma_rn(-y2, y2, y2);
+      const double u3 = __fma_rn(-y3, y3, y3);
+      y0 = __fma_rn(kR, u0, e0);
+      y1 = __fma_rn(kR, u1, e1);
+      y2 = __fma_rn(kR, u2, e2);
+      y3 = __fma_rn(kR, u3, e3);
+    }
+    q[0].y = y0;
+    q[1].y = y1;
+    q[2].y = y2;
+    q[3].y = y3;
+    budget -= m;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) q[j].i += m;
+    if (q[0].i == n_inner + 1) {
+      const int64_t lo = int64_t(q[0].l) * ks;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        A[off[j] + lo] = q[j].y;
+        q[j].l = q[j].l + 1 == nz ? 0 : q[j].l + 1;
+        --q[j].r;
+        q[j].i = 0;
+      }
+    }
+  }
+}
+
 template <int S, bool TIMED>
 __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const TileDev tile,
                                            const ChunkDev* __restrict__ chunks, int32_t nz,
                                            int32_t F, const double* __restrict__ cfield,
                                            int32_t nx, int32_t ny, int32_t shift,
                                            int32_t n_inner,
-                                           unsigned long long* __restrict__ chunk_ns) {
+                                           unsigned long long* __restrict__ chunk_ns,
+                                           const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0,
+                                                                        nullptr, nullptr, nullptr,
+                                                                        0, 0}) {
   constexpr int TY = 8, HALF = 4;
   constexpr int R = 8;
   constexpr int PW = 68;
@@ -1287,6 +1342,8 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
   }
   const bool uniform = quota[0] == quota[1] && quota[1] == quota[2] && quota[2] == quota[3] &&
                        ncells[0] && ncells[1] && ncells[2] && ncells[3];
+  // equal trip counts: the four chains stay in lockstep (equal budgets)
+  const bool lockstep = uniform && ch[0].r == ch[1].r && ch[1].r == ch[2].r && ch[2].r == ch[3].r;
   int fast = 0;
   auto physics = [&](int mult) {
     if (fast > 0) {
@@ -1315,9 +1372,14 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
       --fast;
       return;
     }
+    if (lockstep) {
+      chain_advance4(ch, quota[0] * mult, Bb, Ab, off, nz, ks, n_inner);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (ncells[j]) chain_advance(ch[j], quota[j] * mult, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+      for (int j = 0; j < 4; ++j)
+        if (ncells[j])
+          chain_advance(ch[j], quota[j] * mult, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+    }
     if (uniform) {
       const int b = quota[0] * mult;
       int f = chain_fast(ch[0], b, n_inner);
@@ -1364,13 +1426,55 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
     }
   };
 
+  if (hw.n > 0 || hw.ndeps > 0) {
+    // halo strips or neighbour tiles not ready yet: pre-roll the physics
+    // (reads only this tile's own columns) while polling, as tile_step does
+    int maxr = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) maxr = max(maxr, ch[j].r);
+    const int64_t need = int64_t(maxr) * (n_inner + 1);
+    int64_t done = 0;
+    bool lead_ready = false;
+    for (;;) {
+      const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+      if (lead) {
+        if (done >= need) {
+          const uint64_t w0 = globaltimer_ns();
+          wait_ready(hw, 20ull * 1000 * 1000 * 1000);
+          if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+          lead_ready = true;
+        } else {
+          lead_ready = stamps_ready(hw);
+        }
+      }
+      if (__syncthreads_or(lead && lead_ready)) break;
+      if (lockstep) {
+        chain_advance4(ch, kPreroll, Bb, Ab, off, nz, ks, n_inner);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ncells[j]) chain_advance(ch[j], kPreroll, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+      }
+      done += kPreroll;
+    }
+    fast = 0;
+  }
+
+  // ring hand-off through an mbarrier phase per level pair (see tile_step)
+  __shared__ uint64_t s_ring_bar4;
+  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (bar_lead) mbar_init(&s_ring_bar4, blockDim.x * blockDim.y);
+  __syncthreads();
 #pragma unroll
   for (int L = 0; L < S; ++L) issue(L);
+  cp_async_wait<S - 3>();
+  mbar_arrive(&s_ring_bar4);
 
+  uint32_t parity = 0;
   int k = 0, L = 0;
   for (; L + 1 < levels; L += 2) {
-    cp_async_wait<S - 3>();
-    __syncthreads();
+    mbar_wait(&s_ring_bar4, parity);
+    parity ^= 1;
     issue(L + S);
     issue(L + S + 1);
     cell_pair(rca, L, k, na, zma0, zma1, pouta);
@@ -1383,18 +1487,25 @@ __device__ __forceinline__ void tile_step4(double* __restrict__ ring, const Tile
     pouta += ks;
     poutb += ks;
     if (++k == nz) k = 0;
+    cp_async_wait<S - 3>();
+    mbar_arrive(&s_ring_bar4);
     physics(2);
   }
   if (L < levels) {
-    cp_async_wait<0>();
-    __syncthreads();
+    mbar_wait(&s_ring_bar4, parity);
     cell_pair(rca, L, k, na, zma0, zma1, pouta);
     cell_pair(rcb, L, k, nb, zmb0, zmb1, poutb);
   }
   cp_async_wait<0>();
+  __syncthreads();
+  if (bar_lead) mbar_inval(&s_ring_bar4);
+  if (lockstep) {
+    chain_advance4(ch, 0x7fffffff, Bb, Ab, off, nz, ks, n_inner);
+  } else {
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    if (ncells[j]) chain_advance(ch[j], 0x7fffffff, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+    for (int j = 0; j < 4; ++j)
+      if (ncells[j]) chain_advance(ch[j], 0x7fffffff, Bb + off[j], Ab + off[j], nz, ks, n_inner);
+  }
 
   if (TIMED) {
     charge_ops(chunk_ns, tile.slot, my_ops);
@@ -1412,6 +1523,66 @@ __global__ void __launch_bounds__(128, MINB)
   __shared__ __align__(16) double ring[8 * 10 * 68];
   tile_step4<S, TIMED>(ring, tiles[blockIdx.x], chunks, nz, F, cfield, nx, ny, shift, n_inner,
                        chunk_ns);
+}
+
+// Mode 6 on the mode-5 machinery: one CTA per 64x8 tile (four chains per
+// thread), heaviest first, pack-only CTAs ahead, cross-step overlap.
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+    column_step4_grid(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                      int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
+                      int32_t ny, int32_t shift, int32_t n_inner,
+                      unsigned long long* __restrict__ chunk_ns,
+                      const unsigned long long* __restrict__ halo_flags,
+                      const int32_t* __restrict__ senders, int32_t n_senders,
+                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
+                      const PackArgs pk, const StepDeps sd) {
+  __shared__ __align__(16) double ring[8 * 10 * 68];
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (int(blockIdx.x) < pk.ctas) {
+    if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
+    return;
+  }
+  const TileDev t = tiles[blockIdx.x - pk.ctas];
+  const int self = t.pad >> 1;
+  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
+              nullptr, nullptr, 0, 0};
+  if (sd.on) {
+    if (lead) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
+        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    hw.done = sd.done;
+    hw.deps = sd.idx + sd.off[self] + 1;
+    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
+    hw.need = sd.step;
+  }
+  tile_step4<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
+  if (sd.on) {
+    __syncthreads();
+    __shared__ int s_last4;
+    if (lead) {
+      __threadfence();
+      st_release_gpu_u32(sd.done + self, sd.step + 1);
+      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
+      s_last4 = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
+    }
+    if (sd.res_dst) {
+      __syncthreads();
+      if (s_last4) {
+        __threadfence();
+        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
+          sd.res_dst[i] = __ldcg(chunk_ns + i);
+        __threadfence_system();
+      }
+    }
+  }
 }
 
 template <int S, bool TIMED, int MINB>

@@ -1128,7 +1128,8 @@ void Runtime::begin_window(bool allow_overlap) {
   window_.clear();
   ev_used_ = 0;
   ns_used_ = 0;
-  win_overlap_ = overlap_ && allow_overlap && cfg_.overlap == 5 && grid_launch_ && !d_tl_ &&
+  win_overlap_ = overlap_ && allow_overlap && (cfg_.overlap == 5 || cfg_.overlap == 6) &&
+                 grid_launch_ && !d_tl_ &&
                  (cfg_.measure == OD_MEASURE_TIMER || cfg_.measure == OD_MEASURE_TIMER_RAW);
   if (win_overlap_) {
     const int32_t S = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
@@ -1233,7 +1234,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   // boundaries of chunks that border another GPU
-  const bool fused_pack = p2p_ && pack_ctas_ > 0 && cfg_.overlap == 5 && !tiles4_.empty() &&
+  const bool fused_pack = p2p_ && pack_ctas_ > 0 && !tiles4_.empty() &&
+                          (cfg_.overlap == 5 || (cfg_.overlap == 6 && grid_launch_)) &&
                           (mode == kAsync || timer);
   if (p2p_ && (!jobs_.empty() || n_senders_ > 0)) {
     // pack straight into the neighbours' receive buffers over NVLink, publish
@@ -1319,7 +1321,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     r.kev0 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev0], s0_));
   }
-  if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6) {
+  if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6 && !grid_launch_) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
     if (profiling_) {
@@ -1350,7 +1352,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
     st_.kernel_launches += 1;
     st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 5) {
+  } else if ((mode == kAsync || timer) && !tiles4_.empty() &&
+             (cfg_.overlap == 5 || cfg_.overlap == 6)) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
     const bool prof_f = profiling_ && !r.ovl;
@@ -1431,7 +1434,22 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       lc.numAttrs = r.ovl ? 1 : 0;
       const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
       const ChunkDev* chk = d_chunks_[par];
-      if (grid_minb_ == 6) {
+      if (cfg_.overlap == 6) {
+        // four chains per thread, 64x8 tiles (column_step4_grid)
+        if (timer)
+          OD_CU(cudaLaunchKernelEx(&lc, column_step4_grid<kFusedPrefetch, true, 4>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   ns + (ns_cols_ - 1), pk, sd));
+        else
+          OD_CU(cudaLaunchKernelEx(&lc, column_step4_grid<kFusedPrefetch, false, 4>, chk, tl4,
+                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                   cfg_.n_inner, (unsigned long long*)nullptr,
+                                   (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   r.ovl ? nullptr : tl_wait(), pk, sd));
+      } else if (grid_minb_ == 6) {
         if (timer)
           OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 6>, chk, tl4,
                                    cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
