@@ -21,8 +21,10 @@ def ngpus():
 
 
 @pytest.mark.skipif(ngpus() < 2, reason="needs 2 GPUs")
-@pytest.mark.parametrize("mode,halo", [(5, "p2p"), (5, "nccl"), (0, "p2p"), (6, "p2p")])
-def test_two_gpus_fields_and_plans(mode, halo):
+@pytest.mark.parametrize("mode,halo,extra", [(5, "p2p", {}), (5, "nccl", {}), (0, "p2p", {}),
+                                             (6, "p2p", {}), (5, "p2p", {"OD_OVERLAP": "0"}),
+                                             (5, "p2p", {"OD_PACK_CTAS": "0"})])
+def test_two_gpus_fields_and_plans(mode, halo, extra):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -30,7 +32,7 @@ def test_two_gpus_fields_and_plans(mode, halo):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.join(ROOT, "tools", "mgpu_check.py"), str(mode)]
-    env = dict(os.environ, OD_HALO=halo)
+    env = dict(os.environ, OD_HALO=halo, **extra)
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]
     rows = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
