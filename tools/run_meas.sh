@@ -1,7 +1,3 @@
 cd /root/repo
-T="timeout 900 python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1 --master-port 29533"
-for o in 0 1; do
-  OD_OVERLAP=$o timeout 900 python bench.py --no-e2e --no-cpu > gpurun_out/ovl_n1_$o.json 2> gpurun_out/ovl.err
-  OD_OVERLAP=$o $T --nproc-per-node 4 bench.py --gpus 4 --no-lb-off --no-e2e > gpurun_out/ovl_n4_$o.json 2> gpurun_out/ovl4.err
-  OD_OVERLAP=$o $T --nproc-per-node 2 bench.py --gpus 2 --no-lb-off --no-e2e > gpurun_out/ovl_n2_$o.json 2> gpurun_out/ovl2.err
-done
+timeout 600 python -m pytest tests/test_gpu_fields.py -q -x > gpurun_out/pt.txt 2>&1
+ncu --metrics gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum --clock-control none -k regex:column_step_grid -s 3 -c 2 --csv python tools/diag.py cfg4 2>/dev/null | grep '"ID"\|column_step_grid' > gpurun_out/shfl.csv
