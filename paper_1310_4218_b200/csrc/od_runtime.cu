@@ -844,6 +844,7 @@ void Runtime::build_step_deps() {
   if (n > 0) {
     fill_u32<<<64, 256, 0, s0_>>>(d_done_, int(n), unsigned(st_.steps));
     OD_CU(cudaGetLastError());
+    ++st_.kernel_launches;
   }
 }
 
@@ -1148,6 +1149,7 @@ void Runtime::begin_window(bool allow_overlap) {
     if (!tiles4_.empty()) {
       fill_u32<<<64, 256, 0, s0_>>>(d_done_, int(tiles4_.size()), unsigned(st_.steps));
       OD_CU(cudaGetLastError());
+      ++st_.kernel_launches;
     }
     // measured rows zeroed up front: no per-step memset between the kernels
     if (ns_cols_ > 0) {
@@ -1189,6 +1191,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
   } else if (!r.ovl_chained) {
     stamp_time<<<1, 1, 0, s0_>>>(d_stepend_ + 2 * epoch_step);  // start of a chain
+    ++st_.kernel_launches;
   }
   tl_mark(0);
 
