@@ -46,7 +46,8 @@ def parse_args():
     p.add_argument("--config", default="cfg4")
     p.add_argument("--n-inner", type=int, default=None)
     p.add_argument("--kernel-mode", type=int, default=None,
-                   help="0 separate kernels, 4 fused, 5 fused persistent (default)")
+                   help="0 separate kernels, 4 fused, 5 fused one CTA per tile with "
+                        "cross-step overlap (default), 6 the same, four columns per thread")
     p.add_argument("--threshold", type=float, default=None,
                    help="override the config's LB trigger threshold")
     p.add_argument("--no-e2e", action="store_true")
@@ -318,7 +319,8 @@ def main():
         grid5 = os.environ.get("OD_GRID", "1") != "0"
         kname = {5: ("column_step_grid (fused Jacobi + physics, one CTA per tile)" if grid5
                      else "column_step_persistent (fused Jacobi + physics)"),
-                 6: "column_step4_persistent (fused Jacobi + physics)"}.get(
+                 6: ("column_step4_grid (fused Jacobi + physics, four columns per thread)"
+                     if grid5 else "column_step4_persistent (fused Jacobi + physics)")}.get(
                      cfg.overlap, "column_step3 (fused Jacobi + physics)")
         kms, kflops = fus_ms, phys_flops + jac_flops
     else:

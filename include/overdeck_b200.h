@@ -235,8 +235,8 @@ typedef struct od_config {
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
   int32_t measure;      /* OD_MEASURE_EVENTS | _TIMER | _TIMER_RAW | _OPS */
   int32_t overlap;      /* kernel mode: 0 jacobi_step + physics_step, 4 fused
-                           column_step3, 5 persistent fused (default), 6 persistent
-                           fused, four columns per thread */
+                           column_step3, 5 fused one CTA per 64x4 tile with cross-step
+                           overlap (default), 6 the same with four columns per thread */
   int32_t reserved_[5];
 } od_config;
 

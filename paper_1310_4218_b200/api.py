@@ -735,8 +735,9 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
     # kernel mode: 0 jacobi_step then physics_step (two launches), 4 fused
-    # column_step3 (one CTA per 64x8 tile), 5 persistent fused, heaviest tiles
-    # first (default), 6 persistent fused with four columns per thread
+    # column_step3 (one CTA per 64x8 tile), 5 fused, one CTA per 64x4 tile,
+    # heaviest first, consecutive steps overlapped (default), 6 the same with
+    # four columns per thread (64x8 tiles)
     overlap: int = 5
 
     def vp_count(self) -> int:
