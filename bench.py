@@ -50,6 +50,8 @@ def parse_args():
                         "cross-step overlap (default), 6 the same, four columns per thread")
     p.add_argument("--threshold", type=float, default=None,
                    help="override the config's LB trigger threshold")
+    p.add_argument("--refine-adjacent", action="store_true",
+                   help="B200 extension: RefineSwap calls use refine_adjacent_lb (Strategy 2)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-lb-off", action="store_true")
@@ -220,6 +222,15 @@ def main():
     if args.kernel_mode is not None:
         kw["overlap"] = args.kernel_mode
     cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
+    if args.refine_adjacent:
+        from paper_1310_4218_b200.api import Strategy
+
+        def adj(st):
+            return Strategy.RefineAdjacent if st == Strategy.RefineSwap else st
+        pol = cfg.policy
+        cfg = cfg.replace(policy=dataclasses.replace(
+            pol, first_call_strategy=adj(pol.first_call_strategy),
+            later_call_strategy=adj(pol.later_call_strategy)))
     if args.threshold is not None:
         cfg = cfg.replace(policy=dataclasses.replace(cfg.policy, trigger_threshold=args.threshold))
 

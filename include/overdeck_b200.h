@@ -34,7 +34,7 @@ extern "C" {
 
 enum { OD_OK = 0, OD_EVALIDATION = 2, OD_ERUNTIME = 3 };
 enum { OD_SYNC = 0, OD_ASYNC = 1 };
-enum { OD_GREEDY = 0, OD_REFINE_SWAP = 1 };
+enum { OD_GREEDY = 0, OD_REFINE_SWAP = 1, OD_REFINE_ADJACENT = 2 /* B200 extension */ };
 enum { OD_HEAVY = 0, OD_LIGHT = 1 };
 enum { OD_UNIFORM = 0, OD_STATIC_NODE0 = 1, OD_UPPER_HALF_HEAVY = 2 };
 enum { OD_ONE_D = 0, OD_TWO_D = 1 };
@@ -168,6 +168,14 @@ int od_greedy_lb(const double* loads, int32_t n_loads, const int32_t* map,
 int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
                       int32_t vp_count, int32_t proc_count, double tolerance,
                       od_move* out, int32_t cap, int32_t* n_out);
+/* B200 extension, off-parity (no reference counterpart; Strategy 2): refine_swap_lb's
+   rounds, thresholds and acceptance tests, choosing among admissible moves/swaps the
+   one adding the fewest chunk faces between processors (balance score breaks ties);
+   decomposition as in od_config; cap >= 2*K*P */
+int od_refine_adjacent_lb(const double* loads, int32_t n_loads, const int32_t* map,
+                          int32_t vp_count, int32_t proc_count, double tolerance,
+                          int32_t decomposition_kind, int32_t kx, int32_t ky, od_move* out,
+                          int32_t cap, int32_t* n_out);
 
 /* Engine::run_epoch decision (engine.hpp:257-268) on given per-VP loads:
  * totals, imbalance before/after, trigger (never on the last epoch), first

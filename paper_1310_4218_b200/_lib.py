@@ -133,6 +133,8 @@ PROTOTYPES = {
     "od_should_balance": [_P(_D), _I32, _D, _P(_I32)],
     "od_greedy_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _P(od_move), _I32, _P(_I32)],
     "od_refine_swap_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _P(od_move), _I32, _P(_I32)],
+    "od_refine_adjacent_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _I32, _I32, _I32,
+                              _P(od_move), _I32, _P(_I32)],
     "od_kernel_time_sync": [_P(od_kernel_work), _P(od_gpu_model), _P(_D)],
     "od_transfer_time": [_D, _I32, _P(od_gpu_model), _P(_D)],
     "od_node_gpu_schedule": [_P(_D), _I32, _I32, _P(od_gpu_model), _P(_D)],

@@ -35,7 +35,7 @@ __all__ = [
     "decompose_1d", "decompose_2d", "init_load_field", "advect_load_field", "physics_work",
     "jacobi_work", "halo_bytes", "subdomain_bytes", "Move", "MigrationPlan", "Mapping",
     "initial_block_mapping", "apply_plan", "proc_loads", "imbalance_ratio", "BalancePolicy",
-    "should_balance", "greedy_lb", "refine_swap_lb", "StepSample", "MeasurementWindow",
+    "should_balance", "greedy_lb", "refine_swap_lb", "refine_adjacent_lb", "StepSample", "MeasurementWindow",
     "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
     "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
@@ -54,6 +54,7 @@ class LaunchMode(enum.IntEnum):  # gpu_cost.hpp:15
 class Strategy(enum.IntEnum):  # cluster.hpp:69
     Greedy = 0
     RefineSwap = 1
+    RefineAdjacent = 2  # B200 extension (off-parity): refine keeping neighbouring chunks together
 
 
 class VpClass(enum.IntEnum):  # cluster.hpp:47
@@ -389,6 +390,22 @@ def refine_swap_lb(loads: Sequence[float], mapping: Mapping,
     check(lib.od_refine_swap_lb(_dptr(l), int(l.size), _iptr(mapping._a), mapping.vp_count(),
                                 mapping.proc_count(), float(tolerance), out, cap, C.byref(n)))
     return _plan_from(out, n.value, Strategy.RefineSwap)
+
+
+def refine_adjacent_lb(loads: Sequence[float], mapping: Mapping, decomposition: "Decomposition",
+                       tolerance: float = 0.02) -> MigrationPlan:
+    """B200 extension (off-parity, no reference counterpart): RefineSwapLB's rounds and
+    acceptance tests, taking among admissible moves/swaps the one that adds the fewest
+    chunk faces between processors (each is a halo strip over NVLink every step)."""
+    l = np.ascontiguousarray(loads, dtype=np.float64)
+    cap = max(2 * mapping.vp_count() * max(mapping.proc_count(), 1), 1)
+    out = (od_move * cap)()
+    n = C.c_int32()
+    check(lib.od_refine_adjacent_lb(_dptr(l), int(l.size), _iptr(mapping._a), mapping.vp_count(),
+                                    mapping.proc_count(), float(tolerance),
+                                    int(decomposition.kind), int(decomposition.kx),
+                                    int(decomposition.ky), out, cap, C.byref(n)))
+    return _plan_from(out, n.value, Strategy.RefineAdjacent)
 
 
 @dataclass

@@ -247,6 +247,18 @@ int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
   });
 }
 
+int od_refine_adjacent_lb(const double* loads, int32_t n_loads, const int32_t* map,
+                          int32_t vp_count, int32_t proc_count, double tolerance,
+                          int32_t decomposition_kind, int32_t kx, int32_t ky, od_move* out,
+                          int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    return emit_moves(plan_refine_adjacent(l, m, proc_count, tolerance, decomposition_kind, kx, ky),
+                      out, cap, n_out);
+  });
+}
+
 static GpuCostModel gpu_of(const od_gpu_model* g) {
   need(g, "gpu model");
   GpuCostModel m;

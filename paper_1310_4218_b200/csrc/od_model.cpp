@@ -303,6 +303,119 @@ std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
   return plan;
 }
 
+// B200 extension (off-parity, opt-in Strategy 2): RefineSwapLB that keeps
+// neighbouring chunks together.  Same rounds, thresholds and acceptance tests
+// as plan_refine_swap, but among the admissible actions it takes the one that
+// adds the fewest chunk faces between different processors (every such face is
+// a halo strip over NVLink each step), the balance score breaking ties.
+std::vector<MoveRec> plan_refine_adjacent(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P, double tol,
+                                          int32_t kind, int32_t kx, int32_t ky) {
+  const int32_t K = int32_t(map.size());
+  if (int32_t(loads.size()) != K)
+    throw ValidationError("refine_adjacent_lb: load vector length mismatch");
+  if (tol < 0) throw ValidationError("refine_adjacent_lb: tolerance must be >= 0");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  if (kx < 1 || ky < 1 || (kind == 1 && kx * ky != K) || (kind == 0 && ky != K))
+    throw ValidationError("refine_adjacent_lb: decomposition does not match the vp count");
+
+  std::vector<int32_t> where = map;
+  std::vector<double> acc = totals_per_proc(loads, where, P);
+  double sum = 0.0;
+  for (double a : acc) sum += a;
+  const double avg = sum / P;
+  const double ceil_load = avg * (1.0 + tol);
+  // faces of v that would separate it from its neighbours if it sat on proc q
+  auto cut_at = [&](int32_t v, int32_t q) {
+    int32_t n = 0;
+    for (int32_t d = 0; d < 4; ++d) {
+      const int32_t nb = chunk_neighbor(kind, kx, ky, v, d);
+      if (nb >= 0 && where[nb] != q) ++n;
+    }
+    return n;
+  };
+
+  std::vector<MoveRec> plan;
+  std::vector<int32_t> donors, takers;
+  auto members = [&](int32_t p, std::vector<int32_t>& out) {
+    out.clear();
+    for (int32_t v = 0; v < K; ++v)
+      if (where[v] == p) out.push_back(v);
+  };
+  const int32_t max_rounds = K * P;
+  for (int32_t round = 0; round < max_rounds; ++round) {
+    int32_t hot = -1;
+    for (int32_t p = 0; p < P; ++p)
+      if (acc[p] > ceil_load && (hot < 0 || acc[p] > acc[hot])) hot = p;
+    if (hot < 0) break;
+    const double excess = acc[hot] - avg;
+    members(hot, donors);
+
+    int32_t mv = -1, mq = -1, mcut = 0;
+    double mscore = 0;
+    for (int32_t v : donors)
+      for (int32_t q = 0; q < P; ++q) {
+        if (q == hot || acc[q] >= avg) continue;
+        const double after_src = acc[hot] - loads[v];
+        const double after_dst = acc[q] + loads[v];
+        const double ds = std::fabs(after_src - avg);
+        if (ds >= excess || after_dst > ceil_load) continue;
+        const double score = larger(ds, std::fabs(after_dst - avg));
+        const int32_t dcut = cut_at(v, q) - cut_at(v, hot);
+        if (mv < 0 || dcut < mcut || (dcut == mcut && score < mscore)) {
+          mv = v;
+          mq = q;
+          mscore = score;
+          mcut = dcut;
+        }
+      }
+    if (mv >= 0) {
+      plan.push_back({mv, hot, mq});
+      acc[hot] -= loads[mv];
+      acc[mq] += loads[mv];
+      where[mv] = mq;
+      continue;
+    }
+    int32_t sa = -1, sb = -1, sq = -1, scut = 0;
+    double sscore = 0;
+    for (int32_t q = 0; q < P; ++q) {
+      if (q == hot || acc[q] >= avg) continue;
+      members(q, takers);
+      for (int32_t a : donors)
+        for (int32_t b : takers) {
+          const double d = loads[a] - loads[b];
+          if (d <= 0) continue;
+          const double after_src = acc[hot] - d;
+          const double after_dst = acc[q] + d;
+          const double ds = std::fabs(after_src - avg);
+          if (ds >= excess || after_dst > ceil_load) continue;
+          const double score = larger(ds, std::fabs(after_dst - avg));
+          // cut change of moving a to q, then b to hot
+          int32_t dcut = cut_at(a, q) - cut_at(a, hot);
+          where[a] = q;
+          dcut += cut_at(b, hot) - cut_at(b, q);
+          where[a] = hot;
+          if (sa < 0 || dcut < scut || (dcut == scut && score < sscore)) {
+            sa = a;
+            sb = b;
+            sq = q;
+            sscore = score;
+            scut = dcut;
+          }
+        }
+    }
+    if (sa < 0) break;
+    plan.push_back({sa, hot, sq});
+    plan.push_back({sb, sq, hot});
+    const double d = loads[sa] - loads[sb];
+    acc[hot] -= d;
+    acc[sq] += d;
+    where[sa] = sq;
+    where[sb] = hot;
+  }
+  return plan;
+}
+
 // ------------------------------------------------------------ modelled costs --
 
 void GpuCostModel::validate() const {
@@ -368,15 +481,20 @@ double plan_cost_model(const std::vector<MoveRec>& plan, const std::vector<int64
 Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
                       int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
                       int32_t first_strategy, int32_t later_strategy, double threshold,
-                      double tolerance) {
+                      double tolerance, int32_t kind, int32_t kx, int32_t ky) {
   Decision d;
   d.totals = totals_per_proc(loads, map, P);
   d.imbalance_before = max_over_mean(d.totals);
   d.imbalance_after = d.imbalance_before;
   if (epoch < epochs && balance_needed(d.totals, threshold)) {
     d.strategy = balance_calls == 0 ? first_strategy : later_strategy;
-    d.plan = d.strategy == kGreedy ? plan_greedy(loads, map, P)
-                                   : plan_refine_swap(loads, map, P, tolerance);
+    if (d.strategy == kGreedy)
+      d.plan = plan_greedy(loads, map, P);
+    else if (d.strategy == kRefineAdjacent) {
+      if (kind < 0) throw ValidationError("strategy 2 (refine_adjacent) needs the decomposition");
+      d.plan = plan_refine_adjacent(loads, map, P, tolerance, kind, kx, ky);
+    } else
+      d.plan = plan_refine_swap(loads, map, P, tolerance);
     ++balance_calls;
     if (!d.plan.empty())
       d.imbalance_after = max_over_mean(totals_per_proc(loads, apply_moves(map, P, d.plan), P));

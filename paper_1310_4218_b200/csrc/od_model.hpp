@@ -28,7 +28,7 @@ struct RuntimeFault : std::runtime_error {
 };
 
 enum Mode : int32_t { kSync = 0, kAsync = 1 };
-enum Strategy : int32_t { kGreedy = 0, kRefineSwap = 1 };
+enum Strategy : int32_t { kGreedy = 0, kRefineSwap = 1, kRefineAdjacent = 2 };
 enum VpClass : int32_t { kHeavy = 0, kLight = 1 };
 enum Pattern : int32_t { kUniform = 0, kStaticNode0 = 1, kUpperHalfHeavy = 2 };
 
@@ -87,7 +87,13 @@ std::vector<MoveRec> plan_greedy(const std::vector<double>& loads,
                                  const std::vector<int32_t>& map, int32_t P);  // :36-63
 std::vector<MoveRec> plan_refine_swap(const std::vector<double>& loads,
                                       const std::vector<int32_t>& map, int32_t P,
-                                      double tol);                            // :68-152
+                                      double tol);
+// B200 extension (off-parity): refine_swap_lb's rounds and acceptance tests,
+// choosing among admissible actions the one adding the fewest cross-processor
+// chunk faces (balance score breaks ties); Strategy 2
+std::vector<MoveRec> plan_refine_adjacent(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P, double tol,
+                                          int32_t kind, int32_t kx, int32_t ky);                            // :68-152
 
 // ---- modelled costs (gpu_cost.hpp:21-80, balancer.hpp:157-175) ---------------
 // The B200 path measures these quantities; the model functions stay available
@@ -154,7 +160,7 @@ struct Decision {
 Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
                       int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
                       int32_t first_strategy, int32_t later_strategy, double threshold,
-                      double tolerance);
+                      double tolerance, int32_t kind = -1, int32_t kx = 0, int32_t ky = 0);
 
 // ---- halo exchange schedule -------------------------------------------------
 // Faces between chunks owned by different ranks.  Both sides enumerate the

@@ -312,8 +312,8 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     throw ValidationError("vp count must be >= processor count");
   if (cfg.heavy_value < cfg.light_value || cfg.light_value < 1)
     throw ValidationError("load values require heavy >= light >= 1");
-  if (cfg.first_call_strategy < 0 || cfg.first_call_strategy > 1 ||
-      cfg.later_call_strategy < 0 || cfg.later_call_strategy > 1)
+  if (cfg.first_call_strategy < 0 || cfg.first_call_strategy > 2 ||
+      cfg.later_call_strategy < 0 || cfg.later_call_strategy > 2)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
   if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 6))
@@ -1752,7 +1752,8 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
   o.loads = db.sync_means();
   Decision d = decide_epoch(o.loads, map_, P(), e, cfg_.epochs, balance_calls_,
                             cfg_.first_call_strategy, cfg_.later_call_strategy,
-                            cfg_.trigger_threshold, cfg_.refine_tolerance);
+                            cfg_.trigger_threshold, cfg_.refine_tolerance,
+                            cfg_.decomposition_kind, cfg_.kx, cfg_.ky);
   o.totals = d.totals;
   o.imb_before = d.imbalance_before;
   o.imb_after = d.imbalance_after;

@@ -183,3 +183,46 @@ def test_product_matches_python_restatement():
         mp = rng.integers(0, P, K).tolist()
         assert moves(od.greedy_lb(loads, M(mp, P))) == lbo.greedy_lb(loads, mp, P)
         assert moves(od.refine_swap_lb(loads, M(mp, P))) == lbo.refine_swap_lb(loads, mp, P)
+
+
+# --------------------------------------------- B200 extension: refine_adjacent_lb
+def _cut(m, kx, ky):
+    a = np.array(m.assignment()).reshape(ky, kx)
+    return int((a[:, 1:] != a[:, :-1]).sum() + (a[1:, :] != a[:-1, :]).sum())
+
+
+def test_refine_adjacent_balances_like_refine_and_cuts_fewer_faces():
+    """Off-parity extension (Strategy 2): same acceptance tests as RefineSwapLB,
+    so it balances as often, and it leaves fewer chunk faces between processors."""
+    rng = np.random.default_rng(7)
+    ok_r = ok_a = cut_r = cut_a = 0
+    for case in range(300):
+        kx, ky = int(rng.integers(2, 9)), int(rng.integers(2, 9))
+        K = kx * ky
+        P = int(rng.integers(2, min(9, K) + 1))
+        m = od.initial_block_mapping(K, P)
+        loads = rng.uniform(0.5, 2.0, K)
+        if case % 2:
+            loads[: K // 2] *= 2
+        dec = od.Decomposition(od.DecompositionKind.TwoD, kx, ky)
+        mr = od.apply_plan(m, od.refine_swap_lb(loads, m, 0.02))
+        ma = od.apply_plan(m, od.refine_adjacent_lb(loads, m, dec, 0.02))
+        ok_r += od.imbalance_ratio(od.proc_loads(loads, mr)) <= 1.02 + 1e-12
+        ok_a += od.imbalance_ratio(od.proc_loads(loads, ma)) <= 1.02 + 1e-12
+        cut_r += _cut(mr, kx, ky)
+        cut_a += _cut(ma, kx, ky)
+    assert ok_a >= ok_r - 5
+    assert cut_a < 0.95 * cut_r
+
+
+def test_refine_adjacent_validation_and_policy():
+    m = od.initial_block_mapping(6, 2)
+    dec = od.Decomposition(od.DecompositionKind.TwoD, 3, 2)
+    with pytest.raises(od.ValidationError):
+        od.refine_adjacent_lb([1.0] * 5, m, dec)
+    with pytest.raises(od.ValidationError):
+        od.refine_adjacent_lb([1.0] * 6, m, dec, tolerance=-1)
+    with pytest.raises(od.ValidationError):  # decomposition does not cover the vps
+        od.refine_adjacent_lb([1.0] * 6, m, od.Decomposition(od.DecompositionKind.TwoD, 2, 2))
+    # balanced input: nothing to do
+    assert od.refine_adjacent_lb([1.0] * 6, m, dec).moves == []
