@@ -172,3 +172,16 @@ def test_step_kernel_variants_bitwise(env, monkeypatch):
     Uo, Ao = oracle_fields(cfg, 12)
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")
+
+
+def test_refine_adjacent_policy_runs_bitwise():
+    # Strategy 2 (B200 extension) through the runtime's epoch decision
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, n_inner=7, overlap=5, ppn=3,
+                threshold=1.0, steps_window=(1, 1))
+    cfg = cfg.replace(policy=od.BalancePolicy(od.Strategy.RefineAdjacent,
+                                              od.Strategy.RefineAdjacent, 1.0, 0.02))
+    U, A, recs = device_fields(cfg, 6, use_epochs=True)
+    Uo, Ao = oracle_fields(cfg, 6)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+    assert any(r.plan.moves for r in recs)
