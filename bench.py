@@ -222,6 +222,10 @@ def main():
     if args.kernel_mode is not None:
         kw["overlap"] = args.kernel_mode
     cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
+    if args.config == "cfg1" and 4 % world == 0:
+        # the reference's 4 PEs: one rank per GPU, 4 / N processors on each
+        from paper_1310_4218_b200.api import ClusterSpec
+        cfg = cfg.replace(cluster=ClusterSpec(world, 4 // world))
     if args.refine_adjacent:
         from paper_1310_4218_b200.api import Strategy
 
