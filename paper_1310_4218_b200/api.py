@@ -35,8 +35,8 @@ __all__ = [
     "decompose_1d", "decompose_2d", "init_load_field", "advect_load_field", "physics_work",
     "jacobi_work", "halo_bytes", "subdomain_bytes", "Move", "MigrationPlan", "Mapping",
     "initial_block_mapping", "apply_plan", "proc_loads", "imbalance_ratio", "BalancePolicy",
-    "should_balance", "greedy_lb", "refine_swap_lb", "refine_adjacent_lb", "StepSample", "MeasurementWindow",
-    "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
+    "should_balance", "greedy_lb", "refine_swap_lb", "refine_adjacent_lb", "StepSample",
+    "MeasurementWindow", "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
     "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
     "FaceXfer", "exchange_schedule", "GpuModel", "TransferDirection", "kernel_time_sync",
