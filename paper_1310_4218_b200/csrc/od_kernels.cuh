@@ -500,7 +500,7 @@ __device__ __forceinline__ void physics_init(ColumnState& s, const ChunkDev& c, 
 // Callers pass budgets that are multiples of 8 (or "everything") so the common
 // case -- the budget ends inside the current trip -- is a fully unrolled loop.
 __device__ __forceinline__ void physics_advance(ColumnState& s, int budget) {
-  if (s.i > 0 && s.i + budget <= s.n_inner) {
+  if (s.i > 0 && budget <= s.n_inner - s.i) {  // (no overflow for "everything" budgets)
     double y = s.y;
     const double eb = s.eb;
     for (int j = 0; j < budget; j += 8) {
