@@ -185,3 +185,14 @@ def test_refine_adjacent_policy_runs_bitwise():
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")
     assert any(r.plan.moves for r in recs)
+
+
+@pytest.mark.parametrize("overlap", [5, 6])
+@pytest.mark.parametrize("nz,F", [(2, 1), (3, 1), (2, 2), (5, 1)])
+def test_fields_few_levels(overlap, nz, F):
+    # fewer plane levels (F * nz) than the cp.async ring's prefetch depth
+    cfg = small(nz=nz, F=F, kx=2, ky=3, overlap=overlap)
+    U, A, _ = device_fields(cfg, 3)
+    Uo, Ao = oracle_fields(cfg, 3)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
