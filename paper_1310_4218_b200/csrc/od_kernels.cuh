@@ -1692,6 +1692,24 @@ __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
   }
 }
 
+// Chunk migration pulls: copy whole chunk arrays out of a peer GPU's slab (IPC
+// mapping) over NVLink with SM loads, 16 bytes per thread per iteration.
+struct CopyJob {
+  const double* src;
+  double* dst;
+  int64_t n;  // doubles, even
+};
+
+__global__ void pull_chunks(const CopyJob* __restrict__ jobs) {
+  const CopyJob j = jobs[blockIdx.y];
+  const double2* __restrict__ s = reinterpret_cast<const double2*>(j.src);
+  double2* __restrict__ d = reinterpret_cast<double2*>(j.dst);
+  const int64_t n2 = j.n / 2;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n2;
+       i += int64_t(gridDim.x) * blockDim.x)
+    d[i] = __ldcs(s + i);
+}
+
 // Diagnostic device timeline (OD_TIMELINE): one globaltimer stamp in stream order.
 __global__ void stamp_time(unsigned long long* __restrict__ slot) { *slot = globaltimer_ns(); }
 __global__ void fill_u32(unsigned* __restrict__ p, int n, unsigned v) {

@@ -240,6 +240,8 @@ class Runtime {
   int64_t recv_half_ = 0;  // elements per parity half of d_recv_ (p2p)
   unsigned long long* d_flags_ = nullptr;  // [world] step published by each sender
   std::vector<double*> peer_recv_;
+  std::vector<double*> peer_slab_;  // every rank's chunk slab (IPC), for migration pulls
+  bool peer_slabs_ok_ = false;
   std::vector<unsigned long long*> peer_flags_;
   double** d_peer_base_ = nullptr;
   unsigned long long** d_peer_flags_ = nullptr;
@@ -529,6 +531,7 @@ Runtime::~Runtime() {
   for (int q = 0; q < int(peer_recv_.size()); ++q) {
     if (q == rank_) continue;
     if (peer_recv_[q]) cudaIpcCloseMemHandle(peer_recv_[q]);
+    if (q < int(peer_slab_.size()) && peer_slab_[q]) cudaIpcCloseMemHandle(peer_slab_[q]);
     if (peer_flags_[q]) cudaIpcCloseMemHandle(peer_flags_[q]);
   }
   cudaFree(d_flags_);
@@ -1077,32 +1080,46 @@ void Runtime::setup_p2p() {
   OD_CU(cudaMemset(d_flags_, 0, sizeof(unsigned long long) * world_));
   OD_CU(cudaMalloc(&d_pack_counter_, sizeof(unsigned int)));
   OD_CU(cudaMemset(d_pack_counter_, 0, sizeof(unsigned int)));
-  cudaIpcMemHandle_t mine[2];
+  // [recv buffer, flags, chunk slab (migration pulls; zeroed if no slab)]
+  cudaIpcMemHandle_t mine[3];
+  std::memset(mine, 0, sizeof(mine));
   OD_CU(cudaIpcGetMemHandle(&mine[0], d_recv_));
   OD_CU(cudaIpcGetMemHandle(&mine[1], d_flags_));
+  if (slab_) OD_CU(cudaIpcGetMemHandle(&mine[2], slab_));
   const size_t hb = sizeof(mine);
   uint8_t* d_h = nullptr;
   OD_CU(cudaMalloc(&d_h, hb * (world_ + 1)));
   OD_CU(cudaMemcpy(d_h, mine, hb, cudaMemcpyHostToDevice));
   OD_CU(cudaDeviceSynchronize());
   OD_NC(odb::nccl().AllGather(d_h, d_h + hb, hb, ncclUint8, comm_, s0_));
-  std::vector<cudaIpcMemHandle_t> all(2 * world_);
+  std::vector<cudaIpcMemHandle_t> all(3 * world_);
   OD_CU(cudaMemcpyAsync(all.data(), d_h + hb, hb * world_, cudaMemcpyDeviceToHost, s0_));
   OD_CU(cudaStreamSynchronize(s0_));
   cudaFree(d_h);
   peer_recv_.assign(world_, nullptr);
   peer_flags_.assign(world_, nullptr);
+  peer_slab_.assign(world_, nullptr);
+  const cudaIpcMemHandle_t zero{};
+  peer_slabs_ok_ = true;
   for (int q = 0; q < world_; ++q) {
     if (q == rank_) {
       peer_recv_[q] = d_recv_;
       peer_flags_[q] = d_flags_;
+      peer_slab_[q] = slab_;
+      peer_slabs_ok_ = peer_slabs_ok_ && slab_ != nullptr;
       continue;
     }
     void* p = nullptr;
-    OD_CU(cudaIpcOpenMemHandle(&p, all[2 * q], cudaIpcMemLazyEnablePeerAccess));
+    OD_CU(cudaIpcOpenMemHandle(&p, all[3 * q], cudaIpcMemLazyEnablePeerAccess));
     peer_recv_[q] = static_cast<double*>(p);
-    OD_CU(cudaIpcOpenMemHandle(&p, all[2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    OD_CU(cudaIpcOpenMemHandle(&p, all[3 * q + 1], cudaIpcMemLazyEnablePeerAccess));
     peer_flags_[q] = static_cast<unsigned long long*>(p);
+    if (std::memcmp(&all[3 * q + 2], &zero, sizeof(zero)) != 0) {
+      OD_CU(cudaIpcOpenMemHandle(&p, all[3 * q + 2], cudaIpcMemLazyEnablePeerAccess));
+      peer_slab_[q] = static_cast<double*>(p);
+    } else {
+      peer_slabs_ok_ = false;
+    }
   }
   OD_CU(cudaMalloc(&d_peer_base_, sizeof(double*) * world_));
   OD_CU(cudaMemcpy(d_peer_base_, peer_recv_.data(), sizeof(double*) * world_,
@@ -1928,8 +1945,67 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
       if (rank_of_proc(next[v]) == rank_) incoming[v] = alloc_chunk(v);
     OD_CU(cudaStreamSynchronize(s0_));
     t1 = now_s();
-    OD_NC(odb::nccl().GroupStart());
+    // where every chunk lives in its owner's slab (elements; -1: outside the slab)
+    bool pulled = false;
+    if (p2p_ && peer_slabs_ok_ && !moved.empty() && !std::getenv("OD_MIGRATE_NCCL")) {
+      std::vector<int64_t> mine(K(), -1);
+      const int64_t slab_elems = int64_t(slab_slots_ * (slot_bytes_ / sizeof(double)));
+      for (int32_t v = 0; v < K(); ++v)
+        if (rank_of_proc(map_[v]) == rank_ && chunks_[v].base && chunks_[v].base >= slab_ &&
+            chunks_[v].base < slab_ + slab_elems)
+          mine[v] = int64_t(chunks_[v].base - slab_);
+      int64_t* d_off = nullptr;
+      OD_CU(cudaMalloc(&d_off, sizeof(int64_t) * size_t(K()) * (world_ + 1)));
+      OD_CU(cudaMemcpy(d_off, mine.data(), sizeof(int64_t) * K(), cudaMemcpyHostToDevice));
+      OD_NC(odb::nccl().AllGather(d_off, d_off + K(), size_t(K()), ncclInt64, comm_, s0_));
+      std::vector<int64_t> all(size_t(K()) * world_);
+      OD_CU(cudaMemcpyAsync(all.data(), d_off + K(), sizeof(int64_t) * all.size(),
+                            cudaMemcpyDeviceToHost, s0_));
+      OD_CU(cudaStreamSynchronize(s0_));
+      cudaFree(d_off);
+      bool ok = true;
+      for (int32_t v : moved) ok = ok && all[size_t(rank_of_proc(map_[v])) * K() + v] >= 0;
+      if (ok) {
+        // the new owner pulls U^t and A straight out of the old owner's slab over
+        // NVLink (copy engines, all pairs concurrently), then every rank waits
+        // for every pull before any source slot is reused
+        std::vector<CopyJob> pulls;
+        for (int32_t v : moved) {
+          const int src = rank_of_proc(map_[v]), dst = rank_of_proc(next[v]);
+          const size_t plane = size_t(subs_[v].h()) * ((subs_[v].w() + 15) / 16 * 16);
+          const size_t ae = plane * cfg_.nz, fe = ae * cfg_.fields;
+          if (src == rank_) st_.migrated_bytes += int64_t((fe + ae) * sizeof(double));
+          if (dst != rank_) continue;
+          const double* sb = peer_slab_[src] + all[size_t(src) * K() + v];
+          const ChunkMem& in = incoming[v];
+          pulls.push_back(CopyJob{sb + (in.u[parity_] - in.base), in.u[parity_], int64_t(fe)});
+          pulls.push_back(CopyJob{sb + (in.a - in.base), in.a, int64_t(ae)});
+        }
+        if (!pulls.empty()) {
+          CopyJob* d_jobs = nullptr;
+          OD_CU(cudaMalloc(&d_jobs, pulls.size() * sizeof(CopyJob)));
+          OD_CU(cudaMemcpyAsync(d_jobs, pulls.data(), pulls.size() * sizeof(CopyJob),
+                                cudaMemcpyHostToDevice, s0_));
+          // ~2 waves of 256-thread CTAs spread over the jobs
+          const unsigned per_job = std::max(1u, unsigned(2 * 148 * 8 / pulls.size()));
+          pull_chunks<<<dim3(per_job, unsigned(pulls.size())), 256, 0, s0_>>>(d_jobs);
+          OD_CU(cudaGetLastError());
+          ++st_.kernel_launches;
+          OD_CU(cudaStreamSynchronize(s0_));
+          cudaFree(d_jobs);
+        }
+        int32_t* d_one = nullptr;
+        OD_CU(cudaMalloc(&d_one, sizeof(int32_t)));
+        OD_CU(cudaMemsetAsync(d_one, 0, sizeof(int32_t), s0_));
+        OD_NC(odb::nccl().AllReduce(d_one, d_one, 1, ncclInt32, ncclSum, comm_, s0_));
+        OD_CU(cudaStreamSynchronize(s0_));
+        cudaFree(d_one);
+        pulled = true;
+      }
+    }
+    if (!pulled) OD_NC(odb::nccl().GroupStart());
     for (int32_t v : moved) {
+      if (pulled) break;
       const int src = rank_of_proc(map_[v]), dst = rank_of_proc(next[v]);
       const size_t plane = size_t(subs_[v].h()) * ((subs_[v].w() + 15) / 16 * 16);
       const size_t ae = plane * cfg_.nz, fe = ae * cfg_.fields;
@@ -1943,7 +2019,7 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
         OD_NC(odb::nccl().Recv(incoming[v].a, ae, ncclFloat64, src, comm_, s0_));
       }
     }
-    OD_NC(odb::nccl().GroupEnd());
+    if (!pulled) OD_NC(odb::nccl().GroupEnd());
     OD_CU(cudaStreamSynchronize(s0_));
     t2 = now_s();
     for (int32_t v : moved) {
