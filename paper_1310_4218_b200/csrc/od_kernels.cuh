@@ -1081,6 +1081,305 @@ __global__ void __launch_bounds__(32 * TY, MINB)
   }
 }
 
+template <int TY, int S, bool TIMED, bool FULL = false>
+__device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const TileDev tile,
+                                          const ChunkDev* __restrict__ chunks, int32_t nz,
+                                          int32_t F, const double* __restrict__ cfield,
+                                          int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
+                                          unsigned long long* __restrict__ chunk_ns,
+                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr,
+                                                                       nullptr, nullptr, 0, 0}) {
+  constexpr int R = 8;
+  constexpr int TXC = 64;
+  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
+  constexpr int PLANE = (TY + 2) * PW;
+  static_assert(S + 2 <= R && S >= 3, "prefetch depth");
+  double t_start = 0;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
+
+  const ChunkDev& c = chunks[tile.slot];
+  // warp roles: threadIdx.y < TY physics of row ly, >= TY Jacobi of row ly - TY
+  const bool phys = threadIdx.y < TY;
+  const int lx = threadIdx.x, ly = threadIdx.y % TY;
+  const int w = c.w, h = c.h, pitch = c.pitch;
+  const int64_t ks = c.kstride;
+  // FULL: the tile lies inside the chunk, every thread owns two cells (the
+  // common case); the compiler drops all partial-tile predicates
+  const int wv = FULL ? TXC : min(TXC, w - tile.tx0);
+  const int hv = FULL ? TY : min(TY, h - tile.ty0);
+  const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
+  // cells of this thread's pair inside the chunk (compile-time 2 for full tiles:
+  // the compiler cannot know threadIdx < blockDim)
+  const int pair = FULL ? 2 : max(0, min(2, wv - 2 * lx));
+  const int ncell = FULL ? 2 : (ly < hv ? pair : 0);
+  const int64_t own = int64_t(y) * pitch + x;
+
+  const double* pc = c.in + own;
+  const double* px = nullptr;
+  const double* py = nullptr;
+  int64_t xstep = 0, ystep = 0;
+  int ox = 0, oy = 0, ny_cells = 0;
+  if (ly < hv && (lx == 0 || lx == 31)) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
+    ox = (ly + 1) * PW + (left ? 1 : wv + 2);
+    if (xs >= 0 && xs < w) {
+      px = c.in + int64_t(y) * pitch + xs;
+      xstep = ks;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      px = fd.p + int64_t(y) * fd.es;
+      xstep = fd.ks;
+    }
+  }
+  if (pair > 0 && (ly == 0 || ly == TY - 1)) {
+    const bool top = ly == 0;
+    const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
+    oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
+    ny_cells = pair;
+    if (ys >= 0 && ys < h) {
+      py = c.in + int64_t(ys) * pitch + x;
+      ystep = ks;
+    } else {
+      const FaceDev& fd = c.face[top ? kTop : kBottom];
+      py = fd.p + int64_t(x) * fd.es;
+      ystep = fd.ks;
+    }
+  }
+  const int oc = (ly + 1) * PW + 2 + 2 * lx;
+  const int levels = F * nz;
+
+  auto issue = [&](int L) {
+    if (L < levels) {
+      double* slot = ring + (L & (R - 1)) * PLANE;
+      if (ncell == 2) cp_async16(slot + oc, pc);
+      else if (ncell == 1) cp_async8(slot + oc, pc);
+      if (px) cp_async8(slot + ox, px);
+      if (ny_cells == 2) cp_async16(slot + oy, py);
+      else if (ny_cells == 1) cp_async8(slot + oy, py);
+      pc += ks;
+      px += xstep;
+      py += ystep;
+    }
+    cp_async_commit();
+  };
+
+  ColumnState s0, s1;
+  int q0 = 0, q1 = 0;
+  if (phys && ncell >= 1) {
+    physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+    q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
+    q0 = (q0 + 7) & ~7;
+  }
+  if (phys && ncell == 2) {
+    physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
+    q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
+    q1 = (q1 + 7) & ~7;
+  }
+  int fast = 0;  // interleaved iterations left before a trip boundary
+  auto physics = [&](int b0, int b1) {
+    if (fast > 0) {
+      double y0 = s0.y, y1 = s1.y;
+      const double e0 = s0.eb, e1 = s1.eb;
+      // b0 is a multiple of 16 (quota rounded to 8, two levels per call)
+      for (int j = 0; j < b0; j += 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double u0 = __fma_rn(-y0, y0, y0);
+          const double u1 = __fma_rn(-y1, y1, y1);
+          y0 = __fma_rn(kR, u0, e0);
+          y1 = __fma_rn(kR, u1, e1);
+        }
+      }
+      s0.y = y0;
+      s1.y = y1;
+      s0.i += b0;
+      s1.i += b0;
+      --fast;
+      return;
+    }
+    if (ncell == 2 && b0 == b1 && s0.T == s1.T) {
+      physics_advance_pair(s0, s1, b0);  // lockstep columns: keep both chains interleaved
+      fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
+      return;
+    }
+    if (ncell >= 1) physics_advance(s0, b0);
+    if (ncell == 2) {
+      physics_advance(s1, b1);
+      if (b0 == b1) fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
+    }
+  };
+
+  // one level of one field for this thread's cells (plane in slot L & 7)
+  double zm0 = 0.0, zm1 = 0.0;
+  double* pout = c.out + own;
+  const double* rc = ring + oc;
+  auto level = [&](int L, int k) {
+    const double* pl = rc + (L & (R - 1)) * PLANE;
+    if (ncell == 2) {
+      const double2 uc = *reinterpret_cast<const double2*>(pl);
+      const double xl = pl[-1], xr = pl[2];
+      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
+      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
+      double2 zu = uc;
+      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
+      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                  __dadd_rn(zd0, zu.x));
+      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                  __dadd_rn(zd1, zu.y));
+      double2 o;
+      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+      __stcs(reinterpret_cast<double2*>(pout), o);
+      zm0 = uc.x;
+      zm1 = uc.y;
+    } else if (ncell == 1) {
+      const double uc = pl[0];
+      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
+      const double zd = k > 0 ? zm0 : uc;
+      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
+                                   __dadd_rn(zd, zu));
+      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
+      zm0 = uc;
+    }
+    pout += ks;
+  };
+
+  __shared__ uint64_t s_ring_bar;
+  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == TY;  // first Jacobi thread
+  if (bar_lead) mbar_init(&s_ring_bar, 32 * TY);
+  __syncthreads();
+  if (phys) {
+    // physics warps: both chains to the end, nothing else
+    if (ncell == 2 && s0.T == s1.T) {
+      physics_advance_pair(s0, s1, 0x7fffffff);
+    } else {
+      if (ncell >= 1) physics_advance(s0, 0x7fffffff);
+      if (ncell == 2) physics_advance(s1, 0x7fffffff);
+    }
+  } else {
+    // Jacobi warps: wait for remote strips / neighbour tiles, then stream the ring
+    if (hw.n > 0 || hw.ndeps > 0) {
+      if (bar_lead) {
+        const uint64_t w0 = globaltimer_ns();
+        wait_ready(hw, 20ull * 1000 * 1000 * 1000);
+        if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * TY) : "memory");
+    }
+#pragma unroll
+    for (int L = 0; L < S; ++L) issue(L);
+    cp_async_wait<S - 3>();
+    mbar_arrive(&s_ring_bar);
+    uint32_t parity = 0;
+    int k = 0, L = 0;
+    for (; L + 1 < levels; L += 2) {
+      mbar_wait(&s_ring_bar, parity);
+      parity ^= 1;
+      issue(L + S);
+      issue(L + S + 1);
+      level(L, k);
+      if (++k == nz) k = 0;
+      level(L + 1, k);
+      if (++k == nz) k = 0;
+      cp_async_wait<S - 3>();
+      mbar_arrive(&s_ring_bar);
+    }
+    if (L < levels) {
+      mbar_wait(&s_ring_bar, parity);
+      level(L, k);
+    }
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+  if (bar_lead) mbar_inval(&s_ring_bar);
+
+  if (TIMED) {
+    unsigned long long ops = 0;
+    if (phys) {
+      if (ncell >= 1) ops += (unsigned long long)s0.T * trip_ops(n_inner);
+      if (ncell == 2) ops += (unsigned long long)s1.T * trip_ops(n_inner);
+    } else {
+      ops = (unsigned long long)ncell * nz * F * kJacobiOps;
+    }
+    charge_ops(chunk_ns, tile.slot, ops);
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+  }
+}
+
+// Mode 7 (opt-in): warp-specialised tile.  Same tile geometry and Jacobi code
+// as tile_step, but warps 0..TY-1 run only the physics of their row's two
+// columns (chains back to back, no ring, no barrier) while warps TY..2TY-1
+// stream the Jacobi planes of the same rows through the ring; a tile lasts
+// max(physics, Jacobi) instead of their sum, which is what counts when the
+// GPU holds few tiles (latency-bound sizes).
+template <int TY, bool TIMED, int MINB>
+__global__ void __launch_bounds__(64 * TY, MINB)
+    column_step_ws(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
+                   int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
+                   int32_t ny, int32_t shift, int32_t n_inner,
+                   unsigned long long* __restrict__ chunk_ns,
+                   const unsigned long long* __restrict__ halo_flags,
+                   const int32_t* __restrict__ senders, int32_t n_senders,
+                   unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
+                   const PackArgs pk, const StepDeps sd) {
+  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (int(blockIdx.x) < pk.ctas) {
+    if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
+    return;
+  }
+  const TileDev t = tiles[blockIdx.x - pk.ctas];
+  const ChunkDev& c = chunks[t.slot];
+  const int self = t.pad >> 1;
+  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
+              nullptr, nullptr, 0, 0};
+  if (sd.on) {
+    if (lead) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
+        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+    hw.done = sd.done;
+    hw.deps = sd.idx + sd.off[self] + 1;
+    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
+    hw.need = sd.step;
+  }
+  if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
+    tile_step_ws<TY, 6, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                     chunk_ns, hw);
+  else
+    tile_step_ws<TY, 6, TIMED, false>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                      chunk_ns, hw);
+  if (sd.on) {
+    __syncthreads();
+    __shared__ int s_lastw;
+    if (lead) {
+      __threadfence();
+      st_release_gpu_u32(sd.done + self, sd.step + 1);
+      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
+      s_lastw = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
+    }
+    if (sd.res_dst) {
+      __syncthreads();
+      if (s_lastw) {
+        __threadfence();
+        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
+          sd.res_dst[i] = __ldcg(chunk_ns + i);
+        __threadfence_system();
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Four columns per thread: a 64 x 8 tile on 32 x 4 threads, each thread owning
 // columns (x, x+1) of rows y and y+4.  Four independent FP64 chains per thread

@@ -318,7 +318,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       cfg.later_call_strategy < 0 || cfg.later_call_strategy > 2)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
-  if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 6))
+  if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 7))
     throw ValidationError("unknown kernel mode (overlap): 0, 4, 5 or 6");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER &&
       cfg.measure != OD_MEASURE_TIMER_RAW && cfg.measure != OD_MEASURE_OPS)
@@ -1146,7 +1146,7 @@ void Runtime::begin_window(bool allow_overlap) {
   window_.clear();
   ev_used_ = 0;
   ns_used_ = 0;
-  win_overlap_ = overlap_ && allow_overlap && (cfg_.overlap == 5 || cfg_.overlap == 6) &&
+  win_overlap_ = overlap_ && allow_overlap && (cfg_.overlap >= 5) &&
                  grid_launch_ && !d_tl_ &&
                  (cfg_.measure == OD_MEASURE_TIMER || cfg_.measure == OD_MEASURE_TIMER_RAW);
   if (win_overlap_) {
@@ -1255,7 +1255,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
 
   // boundaries of chunks that border another GPU
   const bool fused_pack = p2p_ && pack_ctas_ > 0 && !tiles4_.empty() &&
-                          (cfg_.overlap == 5 || (cfg_.overlap == 6 && grid_launch_)) &&
+                          (cfg_.overlap == 5 || cfg_.overlap == 7 ||
+                           (cfg_.overlap == 6 && grid_launch_)) &&
                           (mode == kAsync || timer);
   if (p2p_ && (!jobs_.empty() || n_senders_ > 0)) {
     // pack straight into the neighbours' receive buffers over NVLink, publish
@@ -1284,7 +1285,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     }
     // the persistent kernels wait inside, before the first tile that needs a
     // remote strip; the other kernels wait here
-    const bool in_kernel = (cfg_.overlap == 5 || cfg_.overlap == 6) &&
+    const bool in_kernel = (cfg_.overlap >= 5) &&
                            (mode == kAsync || timer);
     if (n_senders_ > 0 && !in_kernel) {
       wait_halo<<<1, 32, 0, s0_>>>(d_flags_, d_senders_, n_senders_, stamp,
@@ -1373,7 +1374,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     st_.kernel_launches += 1;
     st_.fused_launches += 1;
   } else if ((mode == kAsync || timer) && !tiles4_.empty() &&
-             (cfg_.overlap == 5 || cfg_.overlap == 6)) {
+             (cfg_.overlap == 5 || cfg_.overlap == 6 || cfg_.overlap == 7)) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
     const bool prof_f = profiling_ && !r.ovl;
@@ -1454,7 +1455,23 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       lc.numAttrs = r.ovl ? 1 : 0;
       const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
       const ChunkDev* chk = d_chunks_[par];
-      if (cfg_.overlap == 6) {
+      if (cfg_.overlap == 7) {
+        // warp-specialised tiles (column_step_ws): physics and Jacobi warps
+        lc.blockDim = dim3(kTX, 8);
+        if (timer)
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<4, true, 3>, chk, tl4, cfg_.nz,
+                                   cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns,
+                                   (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   ns + (ns_cols_ - 1), pk, sd));
+        else
+          OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<4, false, 3>, chk, tl4, cfg_.nz,
+                                   cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner,
+                                   (unsigned long long*)nullptr,
+                                   (const unsigned long long*)d_flags_,
+                                   (const int32_t*)d_senders_, nsend, stamp,
+                                   r.ovl ? nullptr : tl_wait(), pk, sd));
+      } else if (cfg_.overlap == 6) {
         // four chains per thread, 64x8 tiles (column_step4_grid)
         if (timer)
           OD_CU(cudaLaunchKernelEx(&lc, column_step4_grid<kFusedPrefetch, true, 4>, chk, tl4,
