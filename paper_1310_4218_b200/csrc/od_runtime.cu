@@ -200,6 +200,7 @@ class Runtime {
   int sms_ = 1;
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
   bool grid_launch_ = true;  // mode 5 as one CTA per tile (column_step_grid)
+  int ws_mode_ = -1;         // OD_WS: -1 auto (less than a wave of tiles), 0 never, 1 always
   int grid_minb_ = 5;        // OD_GRID_MINB=6: 6 CTAs/SM build (80 registers)
   size_t grid_pad_smem_ = 0;  // OD_GRID_SMEM: unused dynamic smem per CTA (caps CTAs/SM)
   void refresh_tile_order();
@@ -361,6 +362,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // selects the persistent tile-pulling kernel (column_step_persistent)
     grid_launch_ = !(std::getenv("OD_GRID") && std::string(std::getenv("OD_GRID")) == "0");
     grid_minb_ = std::getenv("OD_GRID_MINB") ? std::atoi(std::getenv("OD_GRID_MINB")) : 5;
+    ws_mode_ = std::getenv("OD_WS") ? std::atoi(std::getenv("OD_WS")) : -1;
     grid_pad_smem_ = std::getenv("OD_GRID_SMEM") ? size_t(std::atol(std::getenv("OD_GRID_SMEM"))) : 0;
     // cross-step overlap of the mode-5 step kernels unless OD_OVERLAP=0
     overlap_ = !(std::getenv("OD_OVERLAP") && std::string(std::getenv("OD_OVERLAP")) == "0");
@@ -1455,7 +1457,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       lc.numAttrs = r.ovl ? 1 : 0;
       const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
       const ChunkDev* chk = d_chunks_[par];
-      if (cfg_.overlap == 7) {
+      // mode 5 on a GPU holding less than one wave of tiles is latency-bound:
+      // there the warp-specialised tile (mode 7) overlaps a tile's physics with
+      // its Jacobi instead of running them back to back (OD_WS=0/1 overrides)
+      const bool ws = cfg_.overlap == 7 ||
+                      (cfg_.overlap == 5 && (ws_mode_ == 1 || (ws_mode_ < 0 && nt < persist_grid_)));
+      if (ws) {
         // warp-specialised tiles (column_step_ws): physics and Jacobi warps
         lc.blockDim = dim3(kTX, 8);
         if (timer)

@@ -159,7 +159,8 @@ def test_measured_loads_track_work_and_balancing_helps():
 
 @pytest.mark.parametrize("env", [{"OD_OVERLAP": "0"}, {"OD_OVERLAP": "1"},
                                  {"OD_GRID": "0", "OD_OVERLAP": "0"},
-                                 {"OD_FIRSTWAVE": "0"}, {"OD_OVERLAP": "1", "OD_ORDER": "spt"}])
+                                 {"OD_FIRSTWAVE": "0"}, {"OD_OVERLAP": "1", "OD_ORDER": "spt"},
+                                 {"OD_WS": "0"}, {"OD_WS": "1"}, {"OD_WS": "1", "OD_OVERLAP": "0"}])
 def test_step_kernel_variants_bitwise(env, monkeypatch):
     """The mode-5 launch variants (cross-step overlap on/off, one CTA per tile
     or persistent, queue orders) compute identical fields, with multi-tile
@@ -176,8 +177,8 @@ def test_step_kernel_variants_bitwise(env, monkeypatch):
 
 def test_refine_adjacent_policy_runs_bitwise():
     # Strategy 2 (B200 extension) through the runtime's epoch decision
-    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, n_inner=7, overlap=5, ppn=3,
-                threshold=1.0, steps_window=(1, 1))
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, n_inner=60, overlap=5, ppn=3,
+                threshold=1.0, steps_window=(1, 1), heavy=4.0)
     cfg = cfg.replace(policy=od.BalancePolicy(od.Strategy.RefineAdjacent,
                                               od.Strategy.RefineAdjacent, 1.0, 0.02))
     U, A, recs = device_fields(cfg, 6, use_epochs=True)
