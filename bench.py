@@ -169,6 +169,8 @@ def reference_arm(args, cfg):
     base = np.ones((ny, nx))
     if int(cfg.pattern) == 2:
         base[: ny // 2] = cfg.heavy_value
+    elif int(cfg.pattern) == 1:
+        base[: ny // 2, : nx // 2] = cfg.heavy_value
     for _ in range(args.warmup):
         of.step(U, A, base, 0, cfg.n_inner)
     t0 = time.perf_counter()
@@ -190,7 +192,7 @@ def reference_arm(args, cfg):
               f"n_inner={cfg.n_inner}, {args.steps} steps")
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "host_only": True, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "sample_columns": nx * ny},
