@@ -46,8 +46,8 @@ def parse_args():
     p.add_argument("--config", default="cfg4")
     p.add_argument("--n-inner", type=int, default=None)
     p.add_argument("--kernel-mode", type=int, default=None,
-                   help="0 separate kernels, 4 fused, 5 fused one CTA per tile with "
-                        "cross-step overlap (default), 6 the same, four columns per thread")
+                   help="0 separate kernels, 4 fused interleaved tiles, 5 automatic "
+                        "(default), 7 fused warp-specialised tiles")
     p.add_argument("--threshold", type=float, default=None,
                    help="override the config's LB trigger threshold")
     p.add_argument("--refine-adjacent", action="store_true",
@@ -127,57 +127,112 @@ class ClockSampler:
 
 # --------------------------------------------------------------- CPU legs --
 
-def cpu_sample_rate(cfg, min_seconds=10.0, max_steps=64, side=256, warmup=0):
-    """Column-updates/s of the CPU oracle port (oracle/field_oracle.c, OpenMP,
-    all host threads) on a side x side sub-grid with the workload's nz, F,
-    n_inner and load pattern."""
+# The workloads as plain numbers, so the reference arm never imports (and so
+# never dlopens) the product package.  tests/test_bench_tables.py checks this
+# table against paper_1310_4218_b200.configs.
+#   name: (nx, ny, nz, fields, pattern, heavy, light, kind, kx, ky, nodes, ppn, n_inner, seed)
+WORKLOADS = {
+    "cfg1": (64, 64, 32, 50, 1, 2.0, 1.0, 1, 4, 4, 4, 1, 1536, 20260826),
+    "cfg2": (64, 64, 32, 50, 2, 2.0, 1.0, 1, 8, 8, 1, 1, 1536, 20260826),
+    "cfg3": (512, 512, 64, 50, 2, 2.0, 1.0, 1, 16, 16, 8, 1, 1536, 54),
+    "cfg4": (1024, 1024, 64, 50, 2, 2.0, 1.0, 1, 16, 16, 1, 1, 1536, 54),
+    "cfg5": (2048, 2048, 96, 16, 2, 2.0, 1.0, 1, 2, 4, 1, 1, 1536, 54),
+    "expA": (1024, 1024, 40, 100, 1, 2.0, 1.0, 1, 2, 2, 2, 1, 1536, 20260826),
+    "expB": (1024, 1024, 40, 50, 2, 2.0, 1.0, 0, 1, 8, 2, 2, 1536, 54),
+    "expC": (1024, 1024, 40, 50, 2, 2.0, 1.0, 0, 1, 16, 2, 2, 1536, 54),
+}
+# columns of the CPU sample (a strided subset of the grid; whole grid when smaller)
+CPU_SAMPLE_SIDE = 512
+
+
+def host_info():
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def workload_ns(name, n_inner=None):
+    """An ExperimentConfig-shaped namespace of WORKLOADS[name] (what
+    oracle.ref.base_field reads)."""
+    from types import SimpleNamespace as NS
+    (nx, ny, nz, F, pat, heavy, light, kind, kx, ky, nodes, ppn, ni, seed) = WORKLOADS[name]
+    return NS(domain=NS(nx=nx, ny=ny, nz=nz, fields=F), pattern=pat, heavy_value=heavy,
+              light_value=light, decomposition=NS(kind=kind, kx=kx, ky=ky),
+              cluster=NS(nodes=nodes, procs_per_node=ppn),
+              n_inner=ni if n_inner is None else n_inner, seed=seed)
+
+
+def cpu_sample(name, n_inner=None, side=CPU_SAMPLE_SIDE):
+    """(oracle state, sample base field, description) of a strided side x side
+    column subset of the workload's initial load field (the reference's own
+    init_load_field via oracle/_ref, the whole grid when it is smaller).  The
+    subset keeps the grid's mix of heavy and light columns, so the CPU's
+    column-updates/s on it is the full grid's up to cache effects."""
     import numpy as np
+    from oracle import fields as of
+    from oracle import ref as oref
+    w = workload_ns(name, n_inner)
+    d = w.domain
+    if oref.available():
+        full = oref.base_field(w)
+    else:  # (prebuilt oracle/_ref missing: same field, restated)
+        full = np.full((d.ny, d.nx), w.light_value)
+        if w.pattern == 2:
+            full[: d.ny // 2] = w.heavy_value
+    sy, sx = max(1, d.ny // side), max(1, d.nx // side)
+    base = np.ascontiguousarray(full[::sy, ::sx])
+    ny, nx = base.shape
+    U, A = of.init_state(nx, ny, d.nz, d.fields, w.seed)
+    trips = lambda c: float(np.maximum(np.floor(d.nz * c) - 1, 0).mean())
+    desc = (f"oracle/field_oracle.c (OpenMP) on a {nx}x{ny} column subset (stride {sx}x{sy}) "
+            f"of the {d.nx}x{d.ny} grid x {d.nz} levels x {d.fields} fields, n_inner={w.n_inner}; "
+            f"mean trips/column {trips(base):.3f} (full grid {trips(full):.3f})")
+    return (U, A, base, w), desc, nx * ny
+
+
+def cpu_run(state, steps, warmup=0, min_seconds=None):
+    from oracle import fields as of
+    U, A, base, w = state
+    for _ in range(warmup):
+        of.step(U, A, base, 0, w.n_inner)
+    n, t0 = 0, time.perf_counter()
+    while n < steps:
+        of.step(U, A, base, 0, w.n_inner)
+        n += 1
+        if min_seconds is not None and time.perf_counter() - t0 >= min_seconds:
+            break
+    return n, time.perf_counter() - t0
+
+
+def cpu_baseline_leg(name, n_inner=None):
+    """cpu_baseline of our arm: 10-30 s of the oracle port on all host threads."""
     from oracle import fields as of
     threads = of.set_threads(os.cpu_count() or 1)
-    d = cfg.domain
-    nx, ny = min(side, d.nx), min(side, d.ny)
-    U, A = of.init_state(nx, ny, d.nz, d.fields, cfg.seed)
-    base = np.ones((ny, nx))
-    if int(cfg.pattern) == 2:
-        base[: ny // 2] = cfg.heavy_value
-    elif int(cfg.pattern) == 1:
-        base[: ny // 2, : nx // 2] = cfg.heavy_value
-    for _ in range(warmup):
-        of.step(U, A, base, 0, cfg.n_inner)
-    steps, t0 = 0, time.perf_counter()
-    while steps < max_steps:
-        of.step(U, A, base, 0, cfg.n_inner)
-        steps += 1
-        if time.perf_counter() - t0 >= min_seconds:
-            break
-    dt = time.perf_counter() - t0
-    return nx * ny * steps / dt, {"grid": [nx, ny, d.nz], "fields": d.fields, "steps": steps,
-                                  "seconds": dt, "threads": threads}
+    state, desc, cols = cpu_sample(name, n_inner)
+    n, dt = cpu_run(state, 64, warmup=1, min_seconds=10.0)
+    return {"value": cols * n / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{desc}; {n} steps in {dt:.1f} s", **host_info()}
 
 
-def reference_arm(args, cfg):
-    """--impl reference: the oracle port (the reference simulator computes no
-    field values) timed on this host's cores for W + K steps of a
-    bounded sample of the same workload."""
-    import numpy as np
+def reference_arm(args):
+    """--impl reference: the reference's CPU path for this workload, timed on
+    this host's cores.  The reference simulator computes no field values
+    (SPEC.md:221), so the timed work is the oracle port of the path (C, OpenMP
+    over all host threads) over a strided column subset of the workload; the
+    reference's own run_experiment (oracle/_ref) is timed beside it.  Nothing
+    of paper_1310_4218_b200 is imported on this path."""
     from oracle import fields as of
     cores = of.set_threads(os.cpu_count() or 1)
-    d = cfg.domain
-    side = 128
-    nx, ny = min(side, d.nx), min(side, d.ny)
-    U, A = of.init_state(nx, ny, d.nz, d.fields, cfg.seed)
-    base = np.ones((ny, nx))
-    if int(cfg.pattern) == 2:
-        base[: ny // 2] = cfg.heavy_value
-    elif int(cfg.pattern) == 1:
-        base[: ny // 2, : nx // 2] = cfg.heavy_value
-    for _ in range(args.warmup):
-        of.step(U, A, base, 0, cfg.n_inner)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        of.step(U, A, base, 0, cfg.n_inner)
-    dt = time.perf_counter() - t0
-    value = nx * ny * args.steps / dt
+    state, desc, cols = cpu_sample(args.config, args.n_inner)
+    cpu_run(state, args.warmup)
+    steps, dt = cpu_run(state, args.steps)
+    value = cols * steps / dt
     sim = None
     try:
         from oracle import ref as oref
@@ -188,16 +243,22 @@ def reference_arm(args, cfg):
                    "seconds": time.perf_counter() - t1}
     except Exception as e:  # informational only
         sim = {"error": str(e)}
-    sample = (f"oracle port, {nx}x{ny} columns x {d.nz} levels x {d.fields} fields, "
-              f"n_inner={cfg.n_inner}, {args.steps} steps")
+    w = workload_ns(args.config, args.n_inner)
+    d = w.domain
+    full = cols == d.nx * d.ny
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "host_only": True, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.config, "sample_columns": nx * ny},
+        "config": {"workload": args.config, "grid": [d.nx, d.ny, d.nz], "fields": d.fields,
+                   "n_inner": w.n_inner, "sample_columns": cols, "same_config": full,
+                   "sampling": None if full else
+                   "strided column subset with the grid's heavy/light mix; each column's "
+                   "work is independent of the grid size, so column-updates/s carries over "
+                   "(profiles/r2_cpu_full_grid_check.json times the whole grid)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": f"{desc}; {steps} steps", **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "reference_simulator": sim,
     }
@@ -216,6 +277,11 @@ def main():
     # keep stdout for the single JSON line: libraries (NCCL, torch) may print
     json_out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
+    if args.impl == "reference":
+        # CPU arm: rank 0 only, and nothing of the product package is imported
+        if rank == 0:
+            print(json.dumps(reference_arm(args)), file=json_out, flush=True)
+        return
     from paper_1310_4218_b200 import configs
     make = configs.CONFIGS[args.config]
     kw = {"epochs": 1 << 30}
@@ -223,11 +289,9 @@ def main():
         kw["n_inner"] = args.n_inner
     if args.kernel_mode is not None:
         kw["overlap"] = args.kernel_mode
-    cfg = make(nodes=world, **kw) if args.config not in ("cfg1", "cfg2") else make(**kw)
-    if args.config == "cfg1" and 4 % world == 0:
-        # the reference's 4 PEs: one rank per GPU, 4 / N processors on each
-        from paper_1310_4218_b200.api import ClusterSpec
-        cfg = cfg.replace(cluster=ClusterSpec(world, 4 // world))
+    # cfg3/4/5: one processor per GPU; cfg1/cfg2 and the paper presets keep
+    # their processor counts (the runtime deals processors to the GPUs)
+    cfg = make(nodes=world, **kw) if args.config in ("cfg3", "cfg4", "cfg5") else make(**kw)
     if args.refine_adjacent:
         from paper_1310_4218_b200.api import Strategy
 
@@ -240,10 +304,6 @@ def main():
     if args.threshold is not None:
         cfg = cfg.replace(policy=dataclasses.replace(cfg.policy, trigger_threshold=args.threshold))
 
-    if args.impl == "reference":
-        if rank == 0:
-            print(json.dumps(reference_arm(args, cfg)), file=json_out, flush=True)
-        return
 
     import torch
     import torch.distributed as dist
@@ -298,20 +358,29 @@ def main():
     st1 = eng.stats()
     hist = eng.epoch_history()[hist0:]
     value = cols * args.steps / (ms * 1e-3)
+    # finish the open epoch (untimed) so every timed step's device wall has been
+    # collected, then average exactly the timed steps
+    S = cfg.window.epoch_steps()
+    eng.advance((-(args.warmup + args.steps)) % S)
+    eng.synchronize()
+    walls = eng.step_walls(args.warmup, args.steps)
+    wall_ms = float(np.nanmean(walls)) * 1e3 if np.isfinite(walls).any() else None
 
-    # roofline of the dominant kernel (physics: FP64 pipe) and of the Jacobi (HBM)
+    # roofline of the dominant kernel: the fused step kernel is the whole device
+    # work of a step, so its achieved FP64 rate is the step's algorithmic flops
+    # over the step's device wall (for overlapped step kernels: the interval
+    # between consecutive step ends, i.e. the amortised kernel duration)
     mapping = eng.mapping().assignment()
     subs = eng.subdomains()
     ppn = cfg.cluster.procs_per_node
     res_cols = sum(s.cells() for v, s in enumerate(subs) if mapping[v] // ppn == rank)
-    n_phys = st1["physics_timed"] - st0["physics_timed"]
-    n_jac = st1["jacobi_timed"] - st0["jacobi_timed"]
-    n_fus = st1["fused_timed"] - st0["fused_timed"]
-    phys_ms = (st1["physics_ms"] - st0["physics_ms"]) / max(n_phys, 1)
-    jac_ms = (st1["jacobi_ms"] - st0["jacobi_ms"]) / max(n_jac, 1)
-    fus_ms = (st1["fused_ms"] - st0["fused_ms"]) / max(n_fus, 1)
-    phys_flops = st1["physics_trips"] * physics_flops_per_trip(cfg.n_inner)
-    jac_cells = float(res_cols) * d.nz * d.fields
+    fus_ms = ((st1["fused_ms"] - st0["fused_ms"]) /
+              max(st1["fused_timed"] - st0["fused_timed"], 1))
+    # physics trips of the whole grid (every rank's columns) under the current field
+    lf = eng.load_field().as_array()
+    all_trips = float(np.maximum(np.floor(d.nz * lf) - 1, 0).sum())
+    phys_flops = all_trips * physics_flops_per_trip(cfg.n_inner)
+    jac_cells = float(cols) * d.nz * d.fields
     jac_flops = 8.0 * jac_cells  # 5 add + 1 mul + 1 fma per cell
     jac_bytes = 16.0 * jac_cells  # read U^t and write U^{t+1} once (FP64)
     peaks = {}
@@ -324,40 +393,39 @@ def main():
         own = json.load(open(os.path.join(ROOT, "profiles", "peaks_fp64.json")))
     except Exception:
         pass
-    fp64_peak = own.get("fp64_fma_tflops", 36.2)
-    hbm_peak = peaks.get("hbm_gbs", 6555.8)
+    fp64_peak = own.get("fp64_fma_tflops", 36.2) * world
+    hbm_peak = peaks.get("hbm_gbs", 6555.8) * world
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
     except Exception:
         pass
     step_ms = ms / args.steps
-    if n_fus > 0:
-        grid5 = os.environ.get("OD_GRID", "1") != "0"
-        kname = {5: ("column_step_grid (fused Jacobi + physics, one CTA per tile)" if grid5
-                     else "column_step_persistent (fused Jacobi + physics)"),
-                 6: ("column_step4_grid (fused Jacobi + physics, four columns per thread)"
-                     if grid5 else "column_step4_persistent (fused Jacobi + physics)")}.get(
-                     cfg.overlap, "column_step3 (fused Jacobi + physics)")
-        kms, kflops = fus_ms, phys_flops + jac_flops
-    else:
-        kname, kms, kflops = "physics_step", phys_ms, phys_flops
-    k_tf = kflops / (kms * 1e-3) / 1e12 if kms > 0 else None
+    kname = eng.kernel_name()
+    kflops = phys_flops + jac_flops
+    kms = wall_ms if wall_ms else step_ms
+    k_tf = kflops / (kms * 1e-3) / 1e12
     roofline = {"bound": "fp64", "kernel": kname, "achieved": k_tf, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": k_tf / fp64_peak if k_tf else None,
-                "traffic": traffic,
-                "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)",
-                "share_of_step": kms / step_ms if step_ms > 0 else None, "avg_ms": kms,
-                "flops_per_launch": kflops}
-    hbm_ms = fus_ms if n_fus > 0 else jac_ms
-    hbm_gbs = jac_bytes / (hbm_ms * 1e-3) / 1e9 if hbm_ms > 0 else None
-    roofline_hbm = {"bound": "hbm", "kernel": kname if n_fus > 0 else "jacobi_step",
-                    "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": hbm_gbs / hbm_peak if hbm_gbs else None, "avg_ms": hbm_ms,
-                    "bytes_per_launch": jac_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+                "unit": "TFLOP/s", "frac": k_tf / fp64_peak, "traffic": traffic,
+                "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)"
+                               + (f" x {world} GPUs" if world > 1 else ""),
+                "avg_ms": kms, "share_of_step": kms / step_ms,
+                "avg_ms_def": "mean device wall of exactly the timed steps (step-kernel "
+                              "interval on the device clock; epoch-boundary host work "
+                              "falls between steps)",
+                "frac_whole_step": kflops / (step_ms * 1e-3) / 1e12 / fp64_peak,
+                "flops_per_launch": kflops,
+                "flops_def": "sum over columns of trips x (5 + 4 n_inner) + 8 per Jacobi "
+                             "cell (nz x F per column), whole grid"}
+    hbm_gbs = jac_bytes / (kms * 1e-3) / 1e9
+    roofline_hbm = {"bound": "hbm", "kernel": kname, "achieved": hbm_gbs, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": hbm_gbs / hbm_peak, "avg_ms": kms,
+                    "bytes_per_launch": jac_bytes, "peak_source": "MEASURED_PEAKS.json hbm_gbs"
+                    + (f" x {world} GPUs" if world > 1 else "")}
 
     launches = st1["kernel_launches"] - st0["kernel_launches"]
-    mine = {"rank": rank, "kernel_avg_ms": round(kms, 3), "resident_chunks": st1["resident_chunks"],
+    mine = {"rank": rank, "kernel_avg_ms": round(fus_ms, 3),
+            "resident_chunks": st1["resident_chunks"],
             "exchange_ms_total": round(st1["exchange_ms"] - st0["exchange_ms"], 2),
             "halo_bytes": st1["halo_bytes_sent"] - st0["halo_bytes_sent"],
             "physics_trips": st1["physics_trips"]}
@@ -381,14 +449,18 @@ def main():
     # step's load multiplier field (pinned) and D2H of per-chunk loads
     e2e = None
     if not args.no_e2e:
+        # the caller hands its load multiplier field to every step from host
+        # memory and gets every step's per-chunk loads back in host memory
         K = eng.vp_count()
         loads = np.zeros((args.steps, K))
-        base = np.ascontiguousarray(eng.load_field().as_array())
-        eng.advance_host(1, base, loads[:1])
-        ms_e2e = timed(lambda: eng.advance_host(args.steps, None, loads))
+        field = np.ascontiguousarray(eng.load_field().as_array())
+        eng.advance_host(1, field, loads[:1])
+        ms_e2e = timed(lambda: eng.advance_host(args.steps, field, loads))
         e2e = {"value": cols * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": cols * 8,
-               "d2h_bytes_per_step": int(st1["resident_chunks"]) * 16}
+               "d2h_bytes_per_step": int(st1["resident_chunks"]) * 16,
+               "path": "od_rt_advance_host: the caller's (ny, nx) float64 load field is read "
+                       "from host memory every step, per-chunk loads written back every step"}
     eng.close()
     del eng
 
@@ -417,12 +489,8 @@ def main():
                           "LB on and off are the same run"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        rate, info = cpu_sample_rate(cfg)
-        cpu = {"value": rate, "unit": UNIT, "cores": info["threads"], "kind": "port",
-               "sample": f"oracle/field_oracle.c (OpenMP) on {info['grid'][0]}x{info['grid'][1]}"
-                         f" columns x {info['grid'][2]} levels x {info['fields']} fields, "
-                         f"{info['steps']} steps, {info['seconds']:.1f} s"}
+    if rank == 0 and world == 1 and not args.no_cpu and args.config in WORKLOADS:
+        cpu = cpu_baseline_leg(args.config, args.n_inner)
 
     if rank != 0:
         if world > 1:

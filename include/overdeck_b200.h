@@ -242,9 +242,12 @@ typedef struct od_config {
   /* B200 path parameters (no reference counterpart) */
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
   int32_t measure;      /* OD_MEASURE_EVENTS | _TIMER | _TIMER_RAW | _OPS */
-  int32_t overlap;      /* kernel mode: 0 jacobi_step + physics_step, 4 fused
-                           column_step3, 5 fused one CTA per 64x4 tile with cross-step
-                           overlap (default), 6 the same with four columns per thread */
+  int32_t overlap;      /* kernel mode: 0 separate jacobi_step + physics_step;
+                           4 fused interleaved tiles (column_step_grid); 5 automatic
+                           (default): column_step_grid from one wave of tiles per
+                           GPU up, column_step_ws below; 7 warp-specialised tiles
+                           (column_step_ws).  Fused modes overlap consecutive step
+                           kernels (programmatic dependent launch) */
   int32_t reserved_[5];
 } od_config;
 
@@ -256,8 +259,9 @@ typedef struct od_epoch_record {
   double compute_total;      /* out: sum of step_times */
   int32_t strategy;          /* out: OD_GREEDY / OD_REFINE_SWAP, -1 = no call */
   int32_t n_moves;           /* out */
-  od_move* moves;            /* in: cap moves_cap */
-  int32_t moves_cap;
+  od_move* moves;            /* in: cap moves_cap; min(n_moves, moves_cap) are written */
+  int32_t moves_cap;         /* n_moves > moves_cap signals a truncated copy (snprintf
+                                convention); the epoch and its migration are committed */
   double migration_seconds;  /* out: measured device time of the chunk moves */
   double imbalance_before, imbalance_after;
   double* proc_loads;        /* in: P */
@@ -305,8 +309,15 @@ int od_rt_run_epoch(od_runtime* rt, int32_t epoch_index, od_epoch_record* rec);
 int od_rt_advance(od_runtime* rt, int32_t n_steps, int32_t* epochs_done);
 /*
  * End-to-end variant of od_rt_advance for the host-facing path: every step
- * copies the step's load multiplier field (nx*ny doubles, pinned host memory)
- * H2D and the step's per-chunk device times (K doubles) D2H.
+ * reads that step's load multiplier field (nx*ny doubles, [y][x]) from host
+ * memory and writes the step's per-chunk device times (K doubles per step,
+ * seconds; 0 for chunks on other ranks) to host_step_loads[step][vp].
+ * host_c_fields: n_fields >= 1 caller fields; step i uses field min(i,
+ * n_fields - 1) as its (already advected) load field.  NULL / n_fields = 0:
+ * the runtime's own advected field crosses the host link each step.  The
+ * runtime's advection schedule keeps advancing either way, so steps driven
+ * afterwards by od_rt_advance continue it.  Both pointers must hold the sizes
+ * above (the Python wrapper checks shape, dtype and contiguity).
  */
 int od_rt_advance_host(od_runtime* rt, int32_t n_steps, const double* host_c_fields,
                        int32_t n_fields, double* host_step_loads /* n_steps*K */);
@@ -332,7 +343,11 @@ typedef struct od_rt_stats {
   int64_t jacobi_timed, physics_timed; /* launches whose event time is in *_ms */
   double fused_ms;
   int64_t fused_launches, fused_timed;
+  int32_t last_kernel;         /* OD_KERNEL_* of the last step kernel launched */
+  int32_t pad2_;
 } od_rt_stats;
+enum { OD_KERNEL_NONE = 0, OD_KERNEL_SEPARATE = 1, OD_KERNEL_STEP_GRID = 2,
+       OD_KERNEL_STEP_WS = 3 };
 int od_rt_stats_get(od_runtime* rt, od_rt_stats* out);
 /* one row per completed epoch (od_rt_run_epoch, od_rt_advance, ..._host) */
 typedef struct od_epoch_summary {
@@ -344,6 +359,15 @@ int od_rt_epoch_history(od_runtime* rt, od_epoch_summary* out, int32_t cap, int3
 /* enable per-kernel event timing (adds events around each batched kernel) */
 int od_rt_set_profiling(od_runtime* rt, int32_t on);
 int od_rt_synchronize(od_runtime* rt);
+/*
+ * Device wall time of individual steps by global step index (0 = the first
+ * step this runtime ran): the wall Engine::step_time returns
+ * (engine.hpp:183-233), i.e. for overlapped step kernels the interval between
+ * consecutive step ends on the device clock.  out[i] = wall of step first+i in
+ * seconds (max over ranks), NaN for steps whose epoch window has not been
+ * collected yet.  Used by the benchmark to average exactly its timed steps.
+ */
+int od_rt_step_walls(od_runtime* rt, int64_t first, int32_t n, double* out);
 
 #ifdef __cplusplus
 }

@@ -87,6 +87,7 @@ class od_rt_stats(C.Structure):
         ("resident_chunks", C.c_int32), ("pad_", C.c_int32),
         ("jacobi_timed", C.c_int64), ("physics_timed", C.c_int64),
         ("fused_ms", C.c_double), ("fused_launches", C.c_int64), ("fused_timed", C.c_int64),
+        ("last_kernel", C.c_int32), ("pad2_", C.c_int32),
     ]
 
 
@@ -178,6 +179,7 @@ PROTOTYPES = {
     "od_rt_set_profiling": [_VP, _I32],
     "od_rt_epoch_history": [_VP, _P(od_epoch_summary), _I32, _P(_I32)],
     "od_rt_synchronize": [_VP],
+    "od_rt_step_walls": [_VP, C.c_int64, _I32, _P(_D)],
 }
 _RESTYPE = {"od_last_error": C.c_char_p, "od_abi_version": _I32,
             "od_loaddb_destroy": None, "od_rt_destroy": None}

@@ -751,10 +751,12 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     seed: int = 1
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
-    # kernel mode: 0 jacobi_step then physics_step (two launches), 4 fused
-    # column_step3 (one CTA per 64x8 tile), 5 fused, one CTA per 64x4 tile,
-    # heaviest first, consecutive steps overlapped (default), 6 the same with
-    # four columns per thread (64x8 tiles)
+    # kernel mode: 0 jacobi_step then physics_step (two launches); 4 fused
+    # interleaved tiles (column_step_grid); 5 automatic (default): interleaved
+    # from one wave of tiles per GPU up, warp-specialised below; 7
+    # warp-specialised tiles (column_step_ws).  Fused tiles are tw x 256/tw
+    # columns (tw = 64/32/16/8 by chunk width), heaviest first, consecutive
+    # step kernels overlapped.
     overlap: int = 5
 
     def vp_count(self) -> int:
@@ -820,9 +822,12 @@ def nccl_unique_id() -> bytes:
 class Engine:
     """The timestep/migration loop of engine.hpp:131-355, executed on a B200.
 
-    One Engine per rank; ``world > 1`` needs the same ``nccl_id`` (from
-    :func:`nccl_unique_id` on rank 0) on every rank and ``config.cluster.nodes
-    == world``.
+    One Engine per rank (= GPU); ``world > 1`` needs the same ``nccl_id``
+    (from :func:`nccl_unique_id` on rank 0) on every rank.  The reference's
+    processors (``cluster.nodes x cluster.procs_per_node``) are dealt to the
+    ``world`` GPUs in contiguous blocks (1 <= world <= processors), so the
+    paper presets keep their processor count and node semantics (the
+    static_node0 hotspot, plan_cost's node pairs) on any GPU count.
     """
 
     def __init__(self, config: ExperimentConfig, rank: int = 0, world: int = 1,
@@ -939,11 +944,33 @@ class Engine:
         check(lib.od_rt_advance(self._h, int(n_steps), C.byref(done)))
         return done.value
 
-    def advance_host(self, n_steps: int, base_field: Optional[np.ndarray] = None,
+    def advance_host(self, n_steps: int, fields: Optional[np.ndarray] = None,
                      step_loads: Optional[np.ndarray] = None) -> None:
-        bf = None if base_field is None else np.ascontiguousarray(base_field, dtype=np.float64)
-        check(lib.od_rt_advance_host(self._h, int(n_steps),
-                                     None if bf is None else _dptr(bf), 0 if bf is None else 1,
+        """od_rt_advance_host: n_steps timesteps whose load fields come from the
+        host.  ``fields``: None (the engine's own advected field crosses the
+        host link every step), one (ny, nx) field for every step, or
+        (n, ny, nx) with step i using fields[min(i, n - 1)].  ``step_loads``:
+        optional (n_steps, K) float64 C-contiguous array receiving each step's
+        per-chunk device seconds."""
+        d = self._cfg.domain
+        nf, fp = 0, None
+        if fields is not None:
+            f = np.asarray(fields)
+            if f.dtype != np.float64 or not f.flags.c_contiguous:
+                raise ValidationError("fields must be a C-contiguous float64 array")
+            if f.ndim == 2:
+                f = f[None]
+            if f.ndim != 3 or f.shape[1:] != (d.ny, d.nx) or f.shape[0] < 1:
+                raise ValidationError(f"fields must have shape (ny, nx) or (n, ny, nx) with "
+                                      f"(ny, nx) = ({d.ny}, {d.nx}); got {np.shape(fields)}")
+            nf, fp = f.shape[0], _dptr(f)
+        if step_loads is not None:
+            sl = step_loads
+            if (not isinstance(sl, np.ndarray) or sl.dtype != np.float64
+                    or not sl.flags.c_contiguous or sl.shape != (int(n_steps), self._k)):
+                raise ValidationError(f"step_loads must be a C-contiguous float64 array of "
+                                      f"shape ({int(n_steps)}, {self._k})")
+        check(lib.od_rt_advance_host(self._h, int(n_steps), fp, nf,
                                      None if step_loads is None else _dptr(step_loads)))
 
     def migrate(self, plan: MigrationPlan) -> None:
@@ -995,6 +1022,21 @@ class Engine:
 
     def synchronize(self) -> None:
         check(lib.od_rt_synchronize(self._h))
+
+    KERNEL_NAMES = {0: None, 1: "jacobi_step + physics_step (separate kernels)",
+                    2: "column_step_grid (fused Jacobi + physics, interleaved tile)",
+                    3: "column_step_ws (fused Jacobi + physics, warp-specialised tile)"}
+
+    def kernel_name(self) -> Optional[str]:
+        """The step kernel the last step launched."""
+        return self.KERNEL_NAMES.get(self.stats()["last_kernel"])
+
+    def step_walls(self, first: int, n: int) -> np.ndarray:
+        """Device wall seconds of global steps first..first+n-1 (NaN until the
+        step's epoch window has been collected)."""
+        out = np.empty(int(n), dtype=np.float64)
+        check(lib.od_rt_step_walls(self._h, int(first), int(n), _dptr(out)))
+        return out
 
 
 def run_experiment(config: ExperimentConfig) -> Timeline:  # engine.hpp:357-360

@@ -43,7 +43,10 @@ struct ChunkDev {
 };
 
 struct TileDev {
-  int32_t slot, tx0, ty0, pad;
+  int32_t slot, tx0, ty0;
+  int32_t pad;     // fused tiles: bit 0 = reads a remote strip, bits 1.. = canonical id
+  int32_t tw, th;  // fused tiles: width 8/16/32/64 and height 256 / tw (4 row warps)
+  int32_t lg, pad2;  // log2(tw / 2)
 };
 __device__ __forceinline__ int share_tag(const TileDev& t) {
   return (t.slot << 20) | (t.ty0 << 8) | (t.tx0 >> 5);
@@ -601,50 +604,80 @@ __device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
   return (s.i > 0 && budget > 0 && s.t <= s.T) ? (s.n_inner - s.i) / budget : 0;
 }
 
-// Pair kernel, second generation: two levels per barrier, uniform plane
-// strides (fs == nz * ks holds for chunk buffers, neighbour faces and packed
-// receive faces alike, so every walker is p += ks), and a countdown that keeps
-// the two physics chains on the branch-free interleaved loop between trip
-// boundaries.  Same arithmetic as every other path.
-// One 64 x TY column tile, all fields and levels (shared by the one-CTA-per-
-// tile launch and the persistent launch).
-template <int TY, int S, bool TIMED, bool FULL = false>
+// ---------------------------------------------------------------------------
+// Fused tile kernels.  A tile is tw x th columns of one chunk: tw in {8, 16, 32,
+// 64} is chosen per chunk width on the host (tile_shape in od_runtime.cu), a
+// thread owns two adjacent columns of one row, so a warp covers 64 / tw rows of
+// tw / 2 threads and the four row-warps of a CTA cover th = 256 / tw rows.
+// Narrow chunks (cfg3's 32, cfg1's 16, cfg2's 8 columns) thus fill every lane
+// of a warp instead of leaving lanes 16..31 without a column.  The ring plane
+// is (th + 2) x (tw + 4) doubles ([pad][left halo][tw][right halo][pad]): at
+// most 408 doubles for every shape.
+// ---------------------------------------------------------------------------
+constexpr int kRingSlots = 8;
+constexpr int kPlaneMax = 408;  // (th + 2) * (tw + 4) over the four shapes
+constexpr int kRowWarps = 4;
+
+struct TileGeom {
+  int tw, th, pw;  // tile width, height, ring row pitch
+  int lx, ly;      // this thread's column pair and row inside the tile
+};
+
+// row warp `wr` (0..3) and lane of this thread
+__device__ __forceinline__ TileGeom tile_geom(const TileDev& t, int wr, int lane) {
+  TileGeom g;
+  g.tw = t.tw;
+  g.th = t.th;
+  g.pw = t.tw + 4;
+  const int lg = t.lg;  // log2(tw / 2): threads per row = 1 << lg
+  g.lx = lane & ((1 << lg) - 1);
+  g.ly = wr * (32 >> lg) + (lane >> lg);
+  return g;
+}
+
+// One tile, all fields and levels: the Jacobi of every (field, level) plane
+// through a cp.async plane ring (two levels per mbarrier phase) interleaved in
+// the same warps with the two physics recurrences of each thread.  Uniform
+// plane strides (fs == nz * ks holds for chunk buffers, neighbour faces and
+// packed receive faces alike, so every walker is p += ks) and a countdown that
+// keeps the two chains on the branch-free interleaved loop between trip
+// boundaries.  FULL: the tile lies inside the chunk (compile-time two cells
+// per thread, no partial-tile predicates).  Same arithmetic as every path.
+template <int S, bool TIMED, bool FULL>
 __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileDev tile,
                                           const ChunkDev* __restrict__ chunks, int32_t nz,
                                           int32_t F, const double* __restrict__ cfield,
                                           int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
                                           unsigned long long* __restrict__ chunk_ns,
-                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr,
-                                                                       nullptr, nullptr, 0, 0}) {
-  constexpr int R = 8;
-  constexpr int TXC = 64;
-  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
-  constexpr int PLANE = (TY + 2) * PW;
+                                          const HaloWait hw) {
+  constexpr int R = kRingSlots;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
   double t_start = 0;
   if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
 
   const ChunkDev& c = chunks[tile.slot];
-  const int lx = threadIdx.x, ly = threadIdx.y;
+  const TileGeom g = tile_geom(tile, threadIdx.y, threadIdx.x);
+  const int PW = g.pw, PLANE = (g.th + 2) * PW;
+  const int lx = g.lx, ly = g.ly;
   const int w = c.w, h = c.h, pitch = c.pitch;
   const int64_t ks = c.kstride;
-  // FULL: the tile lies inside the chunk, every thread owns two cells (the
-  // common case); the compiler drops all partial-tile predicates
-  const int wv = FULL ? TXC : min(TXC, w - tile.tx0);
-  const int hv = FULL ? TY : min(TY, h - tile.ty0);
+  const int wv = FULL ? g.tw : min(g.tw, w - tile.tx0);
+  const int hv = FULL ? g.th : min(g.th, h - tile.ty0);
   const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
-  // cells of this thread's pair inside the chunk (compile-time 2 for full tiles:
-  // the compiler cannot know threadIdx < blockDim)
+  // cells of this thread's pair inside the chunk (compile-time 2 for full tiles)
   const int pair = FULL ? 2 : max(0, min(2, wv - 2 * lx));
   const int ncell = FULL ? 2 : (ly < hv ? pair : 0);
   const int64_t own = int64_t(y) * pitch + x;
+  const int tpr = g.tw >> 1;
 
   const double* pc = c.in + own;
   const double* px = nullptr;
   const double* py = nullptr;
   int64_t xstep = 0, ystep = 0;
   int ox = 0, oy = 0, ny_cells = 0;
-  if (ly < hv && (lx == 0 || lx == 31)) {
+  if (ly < hv && (lx == 0 || lx == tpr - 1)) {
+    // x-halo duty: the row's first thread loads the left, its last the right
+    // halo cell (a one-thread row, tw = 2, never occurs: tw >= 8)
     const bool left = lx == 0;
     const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
     ox = (ly + 1) * PW + (left ? 1 : wv + 2);
@@ -657,7 +690,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       xstep = fd.ks;
     }
   }
-  if (pair > 0 && (ly == 0 || ly == TY - 1)) {
+  if (pair > 0 && (ly == 0 || ly == g.th - 1)) {
     const bool top = ly == 0;
     const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
     oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
@@ -676,7 +709,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 
   auto issue = [&](int L) {
     if (L < levels) {
-      double* slot = ring + (L & (R - 1)) * PLANE;
+      double* slot = ring + (L & (R - 1)) * kPlaneMax;
       if (ncell == 2) cp_async16(slot + oc, pc);
       else if (ncell == 1) cp_async8(slot + oc, pc);
       if (px) cp_async8(slot + ox, px);
@@ -740,14 +773,14 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   double* pout = c.out + own;
   const double* rc = ring + oc;
   auto level = [&](int L, int k) {
-    const double* pl = rc + (L & (R - 1)) * PLANE;
+    const double* pl = rc + (L & (R - 1)) * kPlaneMax;
     if (ncell == 2) {
       const double2 uc = *reinterpret_cast<const double2*>(pl);
       const double xl = pl[-1], xr = pl[2];
       const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
       const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
       double2 zu = uc;
-      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * kPlaneMax);
       const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
       const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
                                   __dadd_rn(zd0, zu.x));
@@ -761,7 +794,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       zm1 = uc.y;
     } else if (ncell == 1) {
       const double uc = pl[0];
-      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
+      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * kPlaneMax] : uc;
       const double zd = k > 0 ? zm0 : uc;
       const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
                                    __dadd_rn(zd, zu));
@@ -770,12 +803,14 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     }
     pout += ks;
   };
+  (void)PLANE;
 
   if (hw.n > 0 || hw.ndeps > 0) {
     // The tile reads strips a peer GPU stores into this GPU's receive buffer
-    // during this step.  Until they have landed, run the tile's physics (which
-    // reads only this GPU's U^t): the wait costs the SM nothing while the
-    // physics lasts, so such tiles can sit anywhere in the heaviest-first queue.
+    // during this step, or cells of same-GPU tiles still finishing the previous
+    // step.  Until they are there, run the tile's physics (which reads only
+    // this tile's own U^t): the wait costs the SM nothing while the physics
+    // lasts, so such tiles can sit anywhere in the heaviest-first queue.
     const int64_t need = int64_t(max(ncell >= 1 ? s0.T : 0, ncell == 2 ? s1.T : 0)) * (n_inner + 1);
     int64_t done = 0;
     bool lead_ready = false;
@@ -850,19 +885,10 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   }
 }
 
-template <int TY, int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(32 * TY, MINB)
-    column_step3(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
-  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
-  tile_step<TY, S, TIMED>(ring, tiles[blockIdx.x], chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                          chunk_ns);
-}
-
-// Partial tiles (chunk edges narrower than 64 x TY) take an out-of-line path so
-// their predicates do not cost registers in the common full-tile code.
-template <int TY, int S, bool TIMED>
+// Partial tiles (chunk edges narrower or shorter than the tile) take an
+// out-of-line path so their predicates do not cost registers in the common
+// full-tile code.
+template <int S, bool TIMED>
 __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const TileDev tile,
                                                const ChunkDev* __restrict__ chunks, int32_t nz,
                                                int32_t F, const double* __restrict__ cfield,
@@ -870,16 +896,20 @@ __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const 
                                                int32_t n_inner,
                                                unsigned long long* __restrict__ chunk_ns,
                                                const HaloWait hw) {
-  tile_step<TY, S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                 chunk_ns, hw);
+  tile_step<S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
+                             hw);
 }
 
-// Halo pack fused into the persistent kernel (P2P halos): the first `ctas`
-// CTAs store this step's boundary strips straight into the peers' receive
-// buffers over NVLink, one (face, field) unit at a time, before they join the
-// tile queue; the other CTAs start on tiles at once, so the NVLink transfer
-// overlaps the compute.  The CTA that completes the last unit publishes the
-// step to the peers (same protocol as pack_faces_p2p).
+__device__ __forceinline__ bool tile_full(const TileDev& t, const ChunkDev& c) {
+  return t.tx0 + t.tw <= c.w && t.ty0 + t.th <= c.h;
+}
+
+// Halo pack fused into the step kernel (P2P halos): the first `ctas` CTAs
+// store this step's boundary strips straight into the peers' receive buffers
+// over NVLink, one (face, field) unit at a time; the other CTAs start on tiles
+// at once, so the NVLink transfer overlaps the compute.  The CTA that
+// completes the last unit publishes the step to the peers (same protocol as
+// pack_faces_p2p).
 struct PackArgs {
   const PackJob* jobs;
   int32_t njobs, ctas;
@@ -962,57 +992,59 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
   }
 }
 
-// Persistent variant: a fixed grid (one wave) pulls tiles, heaviest first,
-// from a counter, so the per-GPU time follows the work even when the GPU holds
-// few tiles (strong scaling) and heavy tiles do not end up in a ragged tail.
-template <int TY, int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(32 * TY, MINB)
-    column_step_persistent(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                           int32_t ntiles, unsigned int* __restrict__ counter, int32_t nz,
-                           int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                           int32_t shift, int32_t n_inner,
-                           unsigned long long* __restrict__ chunk_ns,
-                           const unsigned long long* __restrict__ halo_flags,
-                           const int32_t* __restrict__ senders, int32_t n_senders,
-                           unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
-                           const PackArgs pk) {
-  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
-  __shared__ int s_next;
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-  bool halo_ready = n_senders == 0;  // meaningful in the lead thread only
-  if (pk.njobs > 0 && int(blockIdx.x) >= pk.first && int(blockIdx.x) < pk.first + pk.ctas)
-    pack_units(pk, chunks, nz, F, stamp, StepDeps{});
-  for (;;) {
-    if (lead) s_next = int(atomicAdd(counter, 1u));
+// Cross-step overlap, tile side: block on the tile's own previous step (its
+// columns' A and U^t), then hand the same-GPU neighbour tiles to tile_step's
+// pre-roll poll.
+__device__ __forceinline__ void tile_deps(const StepDeps& sd, int self, HaloWait& hw) {
+  if (!sd.on) return;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
+      if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  hw.done = sd.done;
+  hw.deps = sd.idx + sd.off[self] + 1;
+  hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
+  hw.need = sd.step;
+}
+
+// Publish the tile's step; the CTA that finishes the step's last tile copies
+// the step's per-chunk measurement row into mapped pinned host memory.
+__device__ __forceinline__ void tile_publish(const StepDeps& sd, int self,
+                                             const unsigned long long* __restrict__ chunk_ns) {
+  if (!sd.on) return;
+  __syncthreads();  // every thread's U^{t+1} stores issued
+  __shared__ int s_last;
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    __threadfence();
+    st_release_gpu_u32(sd.done + self, sd.step + 1);
+    if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
+    s_last = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
+  }
+  if (sd.res_dst) {
     __syncthreads();
-    const int ti = s_next;
-    __syncthreads();  // everyone has read s_next and left the previous tile's ring
-    if (ti >= ntiles) break;
-    const TileDev t = tiles[ti];
-    const ChunkDev& c = chunks[t.slot];
-    // a tile reading a strip from another GPU before this CTA has seen the
-    // strips land pre-rolls its physics while polling (tile_step)
-    const bool poll = __syncthreads_or(lead && (t.pad & 1) && !halo_ready);
-    const HaloWait hw{halo_flags, senders, poll ? n_senders : 0, stamp, wait_ns,
-                      nullptr, nullptr, 0, 0};
-    if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
-      tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                    chunk_ns, hw);
-    else
-      tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                      chunk_ns, hw);
-    if (poll) halo_ready = true;
+    if (s_last) {
+      __threadfence();  // every tile's shares are in
+      const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+      for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
+        sd.res_dst[i] = __ldcg(chunk_ns + i);
+      __threadfence_system();
+    }
   }
 }
 
-// One CTA per tile over the heaviest-first tile list.  The block scheduler
-// starts CTAs in index order as earlier ones retire, and the warp scheduler
-// favours older warps, so tiles are served roughly first-come-first-served: an
-// early (heavy) tile is never starved behind a stream of later tiles the way a
-// young CTA of the persistent kernel is (its oldest CTAs keep the pipe while
-// they pull tile after tile).  Same tile body, halo pre-roll and fused pack.
-template <int TY, int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(32 * TY, MINB)
+// Mode 4 (and mode 5 from one wave of tiles up): one CTA (4 row-warps) per
+// tile over the heaviest-first tile list.  The block scheduler starts CTAs in
+// index order as earlier ones retire, and the warp scheduler favours older
+// warps, so tiles are served roughly first-come-first-served.  With P2P halos
+// the first pk.ctas CTAs only pack this step's boundary strips into the peers'
+// buffers and exit; with sd.on the grid is launched with programmatic
+// dependent launch behind the previous step's (cross-step overlap).
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(32 * kRowWarps, MINB)
     column_step_grid(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
                      int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
                      int32_t ny, int32_t shift, int32_t n_inner,
@@ -1021,13 +1053,10 @@ __global__ void __launch_bounds__(32 * TY, MINB)
                      const int32_t* __restrict__ senders, int32_t n_senders,
                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                      const PackArgs pk, const StepDeps sd) {
-  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  __shared__ __align__(16) double ring[kRingSlots * kPlaneMax];
   // cross-step overlap: let the next step's grid launch as soon as every CTA of
   // this one has started; its tiles wait on per-tile stamps, not on this grid
   if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  // the first pk.ctas CTAs only pack this step's boundary strips into the
-  // peers' buffers (dynamically shared units) and exit; tiles start behind them
   if (int(blockIdx.x) < pk.ctas) {
     if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
     return;
@@ -1037,89 +1066,56 @@ __global__ void __launch_bounds__(32 * TY, MINB)
   const int self = t.pad >> 1;
   HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
               nullptr, nullptr, 0, 0};
-  if (sd.on) {
-    // the tile's own columns (A, U^t) come from its previous step: block on it;
-    // its neighbours' halo cells are polled while the physics pre-rolls
-    if (lead) {
-      const uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
-        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
-        __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    hw.done = sd.done;
-    hw.deps = sd.idx + sd.off[self] + 1;
-    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
-    hw.need = sd.step;
-  }
-  if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
-    tile_step<TY, S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                  chunk_ns, hw);
+  tile_deps(sd, self, hw);
+  if (tile_full(t, c))
+    tile_step<S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
   else
-    tile_step_partial<TY, S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                    chunk_ns, hw);
-  if (sd.on) {
-    __syncthreads();  // every thread's U^{t+1} stores issued
-    __shared__ int s_last;
-    if (lead) {
-      __threadfence();
-      st_release_gpu_u32(sd.done + self, sd.step + 1);
-      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
-      s_last = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
-    }
-    if (sd.res_dst) {
-      __syncthreads();
-      if (s_last) {
-        __threadfence();  // every tile's shares are in
-        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
-          sd.res_dst[i] = __ldcg(chunk_ns + i);
-        __threadfence_system();
-      }
-    }
-  }
+    tile_step_partial<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
+                                hw);
+  tile_publish(sd, self, chunk_ns);
 }
 
-template <int TY, int S, bool TIMED, bool FULL = false>
+// Warp-specialised tile (mode 7; mode 5 when a GPU holds less than one wave of
+// tiles): the same tile shapes, ring and Jacobi code as tile_step, but 8 warps:
+// warps 0..3 run only the physics of their rows' column pairs (chains back to
+// back, no ring, no barrier) while warps 4..7 stream the Jacobi planes of the
+// same rows.  A tile lasts max(physics, Jacobi) instead of their sum, which is
+// what counts when the GPU holds few tiles (latency-bound sizes).
+template <int S, bool TIMED, bool FULL>
 __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const TileDev tile,
-                                          const ChunkDev* __restrict__ chunks, int32_t nz,
-                                          int32_t F, const double* __restrict__ cfield,
-                                          int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
-                                          unsigned long long* __restrict__ chunk_ns,
-                                          const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0, nullptr,
-                                                                       nullptr, nullptr, 0, 0}) {
-  constexpr int R = 8;
-  constexpr int TXC = 64;
-  constexpr int PW = TXC + 4;  // [pad][left halo][64 columns][right halo][pad]
-  constexpr int PLANE = (TY + 2) * PW;
+                                             const ChunkDev* __restrict__ chunks, int32_t nz,
+                                             int32_t F, const double* __restrict__ cfield,
+                                             int32_t nx, int32_t ny, int32_t shift,
+                                             int32_t n_inner,
+                                             unsigned long long* __restrict__ chunk_ns,
+                                             const HaloWait hw) {
+  constexpr int R = kRingSlots;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
   double t_start = 0;
   if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
 
   const ChunkDev& c = chunks[tile.slot];
-  // warp roles: threadIdx.y < TY physics of row ly, >= TY Jacobi of row ly - TY
-  const bool phys = threadIdx.y < TY;
-  const int lx = threadIdx.x, ly = threadIdx.y % TY;
+  // warp roles: threadIdx.y < 4 physics, >= 4 Jacobi, both over row warp y % 4
+  const bool phys = threadIdx.y < kRowWarps;
+  const TileGeom g = tile_geom(tile, threadIdx.y % kRowWarps, threadIdx.x);
+  const int PW = g.pw;
+  const int lx = g.lx, ly = g.ly;
   const int w = c.w, h = c.h, pitch = c.pitch;
   const int64_t ks = c.kstride;
-  // FULL: the tile lies inside the chunk, every thread owns two cells (the
-  // common case); the compiler drops all partial-tile predicates
-  const int wv = FULL ? TXC : min(TXC, w - tile.tx0);
-  const int hv = FULL ? TY : min(TY, h - tile.ty0);
+  const int wv = FULL ? g.tw : min(g.tw, w - tile.tx0);
+  const int hv = FULL ? g.th : min(g.th, h - tile.ty0);
   const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
-  // cells of this thread's pair inside the chunk (compile-time 2 for full tiles:
-  // the compiler cannot know threadIdx < blockDim)
   const int pair = FULL ? 2 : max(0, min(2, wv - 2 * lx));
   const int ncell = FULL ? 2 : (ly < hv ? pair : 0);
   const int64_t own = int64_t(y) * pitch + x;
+  const int tpr = g.tw >> 1;
 
   const double* pc = c.in + own;
   const double* px = nullptr;
   const double* py = nullptr;
   int64_t xstep = 0, ystep = 0;
   int ox = 0, oy = 0, ny_cells = 0;
-  if (ly < hv && (lx == 0 || lx == 31)) {
+  if (!phys && ly < hv && (lx == 0 || lx == tpr - 1)) {
     const bool left = lx == 0;
     const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
     ox = (ly + 1) * PW + (left ? 1 : wv + 2);
@@ -1132,7 +1128,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       xstep = fd.ks;
     }
   }
-  if (pair > 0 && (ly == 0 || ly == TY - 1)) {
+  if (!phys && pair > 0 && (ly == 0 || ly == g.th - 1)) {
     const bool top = ly == 0;
     const int ys = top ? tile.ty0 - 1 : tile.ty0 + hv;
     oy = (top ? 0 : hv + 1) * PW + 2 + 2 * lx;
@@ -1151,7 +1147,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
 
   auto issue = [&](int L) {
     if (L < levels) {
-      double* slot = ring + (L & (R - 1)) * PLANE;
+      double* slot = ring + (L & (R - 1)) * kPlaneMax;
       if (ncell == 2) cp_async16(slot + oc, pc);
       else if (ncell == 1) cp_async8(slot + oc, pc);
       if (px) cp_async8(slot + ox, px);
@@ -1165,64 +1161,21 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   };
 
   ColumnState s0, s1;
-  int q0 = 0, q1 = 0;
-  if (phys && ncell >= 1) {
-    physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
-    q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
-    q0 = (q0 + 7) & ~7;
-  }
-  if (phys && ncell == 2) {
-    physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
-    q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
-    q1 = (q1 + 7) & ~7;
-  }
-  int fast = 0;  // interleaved iterations left before a trip boundary
-  auto physics = [&](int b0, int b1) {
-    if (fast > 0) {
-      double y0 = s0.y, y1 = s1.y;
-      const double e0 = s0.eb, e1 = s1.eb;
-      // b0 is a multiple of 16 (quota rounded to 8, two levels per call)
-      for (int j = 0; j < b0; j += 16) {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const double u0 = __fma_rn(-y0, y0, y0);
-          const double u1 = __fma_rn(-y1, y1, y1);
-          y0 = __fma_rn(kR, u0, e0);
-          y1 = __fma_rn(kR, u1, e1);
-        }
-      }
-      s0.y = y0;
-      s1.y = y1;
-      s0.i += b0;
-      s1.i += b0;
-      --fast;
-      return;
-    }
-    if (ncell == 2 && b0 == b1 && s0.T == s1.T) {
-      physics_advance_pair(s0, s1, b0);  // lockstep columns: keep both chains interleaved
-      fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
-      return;
-    }
-    if (ncell >= 1) physics_advance(s0, b0);
-    if (ncell == 2) {
-      physics_advance(s1, b1);
-      if (b0 == b1) fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
-    }
-  };
+  if (phys && ncell >= 1) physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+  if (phys && ncell == 2) physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
 
-  // one level of one field for this thread's cells (plane in slot L & 7)
   double zm0 = 0.0, zm1 = 0.0;
   double* pout = c.out + own;
   const double* rc = ring + oc;
   auto level = [&](int L, int k) {
-    const double* pl = rc + (L & (R - 1)) * PLANE;
+    const double* pl = rc + (L & (R - 1)) * kPlaneMax;
     if (ncell == 2) {
       const double2 uc = *reinterpret_cast<const double2*>(pl);
       const double xl = pl[-1], xr = pl[2];
       const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
       const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
       double2 zu = uc;
-      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
+      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * kPlaneMax);
       const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
       const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
                                   __dadd_rn(zd0, zu.x));
@@ -1236,7 +1189,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       zm1 = uc.y;
     } else if (ncell == 1) {
       const double uc = pl[0];
-      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
+      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * kPlaneMax] : uc;
       const double zd = k > 0 ? zm0 : uc;
       const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
                                    __dadd_rn(zd, zu));
@@ -1247,8 +1200,8 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   };
 
   __shared__ uint64_t s_ring_bar;
-  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == TY;  // first Jacobi thread
-  if (bar_lead) mbar_init(&s_ring_bar, 32 * TY);
+  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == kRowWarps;  // first Jacobi thread
+  if (bar_lead) mbar_init(&s_ring_bar, 32 * kRowWarps);
   __syncthreads();
   if (phys) {
     // physics warps: both chains to the end, nothing else
@@ -1266,7 +1219,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
         wait_ready(hw, 20ull * 1000 * 1000 * 1000);
         if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * TY) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kRowWarps) : "memory");
     }
 #pragma unroll
     for (int L = 0; L < S; ++L) issue(L);
@@ -1310,14 +1263,20 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   }
 }
 
-// Mode 7 (opt-in): warp-specialised tile.  Same tile geometry and Jacobi code
-// as tile_step, but warps 0..TY-1 run only the physics of their row's two
-// columns (chains back to back, no ring, no barrier) while warps TY..2TY-1
-// stream the Jacobi planes of the same rows through the ring; a tile lasts
-// max(physics, Jacobi) instead of their sum, which is what counts when the
-// GPU holds few tiles (latency-bound sizes).
-template <int TY, bool TIMED, int MINB>
-__global__ void __launch_bounds__(64 * TY, MINB)
+template <int S, bool TIMED>
+__device__ __noinline__ void tile_step_ws_partial(double* __restrict__ ring, const TileDev tile,
+                                                  const ChunkDev* __restrict__ chunks, int32_t nz,
+                                                  int32_t F, const double* __restrict__ cfield,
+                                                  int32_t nx, int32_t ny, int32_t shift,
+                                                  int32_t n_inner,
+                                                  unsigned long long* __restrict__ chunk_ns,
+                                                  const HaloWait hw) {
+  tile_step_ws<S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                chunk_ns, hw);
+}
+
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(64 * kRowWarps, MINB)
     column_step_ws(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
                    int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
                    int32_t ny, int32_t shift, int32_t n_inner,
@@ -1326,8 +1285,7 @@ __global__ void __launch_bounds__(64 * TY, MINB)
                    const int32_t* __restrict__ senders, int32_t n_senders,
                    unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                    const PackArgs pk, const StepDeps sd) {
-  __shared__ __align__(16) double ring[8 * (TY + 2) * 68];
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  __shared__ __align__(16) double ring[kRingSlots * kPlaneMax];
   if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (int(blockIdx.x) < pk.ctas) {
     if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
@@ -1338,586 +1296,14 @@ __global__ void __launch_bounds__(64 * TY, MINB)
   const int self = t.pad >> 1;
   HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
               nullptr, nullptr, 0, 0};
-  if (sd.on) {
-    if (lead) {
-      const uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
-        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
-        __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    hw.done = sd.done;
-    hw.deps = sd.idx + sd.off[self] + 1;
-    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
-    hw.need = sd.step;
-  }
-  if (t.tx0 + 64 <= c.w && t.ty0 + TY <= c.h)
-    tile_step_ws<TY, 6, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                     chunk_ns, hw);
+  tile_deps(sd, self, hw);
+  if (tile_full(t, c))
+    tile_step_ws<S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
+                                 hw);
   else
-    tile_step_ws<TY, 6, TIMED, false>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                      chunk_ns, hw);
-  if (sd.on) {
-    __syncthreads();
-    __shared__ int s_lastw;
-    if (lead) {
-      __threadfence();
-      st_release_gpu_u32(sd.done + self, sd.step + 1);
-      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
-      s_lastw = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
-    }
-    if (sd.res_dst) {
-      __syncthreads();
-      if (s_lastw) {
-        __threadfence();
-        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
-          sd.res_dst[i] = __ldcg(chunk_ns + i);
-        __threadfence_system();
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Four columns per thread: a 64 x 8 tile on 32 x 4 threads, each thread owning
-// columns (x, x+1) of rows y and y+4.  Four independent FP64 chains per thread
-// (the pipe saturates with one warp per SMSP) and twice the columns per CTA of
-// the pair kernel, so a GPU's whole share of columns fits in one wave at
-// strong-scaling sizes: the time follows the work, not the wave count.
-// Same arithmetic as every other path.
-// ---------------------------------------------------------------------------
-struct Chain {  // one column's recurrence; y doubles as A(l-1) between trips
-  double y, eb;
-  int l, i, r;  // level of the current trip, unit within it, trips left
-};
-
-__device__ __forceinline__ void chain_init(Chain& q, const double* B, const double* A, int T,
-                                           int nz, int64_t ks) {
-  q.y = A[0];
-  q.eb = 0.0;
-  q.l = nz > 1 ? 1 : 0;
-  q.i = 0;
-  q.r = T;
-  (void)B;
-  (void)ks;
-}
-
-// advance one chain by `budget` units (general path: trip setup / finish)
-__device__ __forceinline__ void chain_advance(Chain& q, int budget, const double* B, double* A,
-                                              int nz, int64_t ks, int n_inner) {
-  while (budget > 0 && q.r > 0) {
-    if (q.i == 0) {
-      const double b = B[q.l * ks];
-      q.eb = __fma_rn(b, kEps, kEps);
-      q.y = __fma_rn(0.5, q.y, __dmul_rn(0.5, b));
-      q.i = 1;
-      --budget;
-    }
-    const int m = min(budget, n_inner + 1 - q.i);
-    double y = q.y;
-    const double eb = q.eb;
-#pragma unroll 4
-    for (int j = 0; j < m; ++j) {
-      const double u = __fma_rn(-y, y, y);
-      y = __fma_rn(kR, u, eb);
-    }
-    q.y = y;
-    q.i += m;
-    budget -= m;
-    if (q.i == n_inner + 1) {
-      A[q.l * ks] = y;
-      q.l = q.l + 1 == nz ? 0 : q.l + 1;
-      --q.r;
-      q.i = 0;
-    }
-  }
-}
-
-__device__ __forceinline__ int chain_fast(const Chain& q, int budget, int n_inner) {
-  return (q.i > 0 && q.r > 0 && budget > 0) ? (n_inner - q.i) / budget : 0;
-}
-
-// Four chains with equal trip counts advance in lockstep: cross trip
-// boundaries with all four interleaved (same operations per chain as
-// chain_advance, in the same order).
-__device__ __forceinline__ void chain_advance4(Chain* q, int budget, const double* B,
-                                               double* A, const int64_t* off, int nz,
-                                               int64_t ks, int n_inner) {
-  while (budget > 0 && q[0].r > 0) {
-    if (q[0].i == 0) {
-      const int64_t lo = int64_t(q[0].l) * ks;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double b = B[off[j] + lo];
-        q[j].eb = __fma_rn(b, kEps, kEps);
-        q[j].y = __fma_rn(0.5, q[j].y, __dmul_rn(0.5, b));
-        q[j].i = 1;
-      }
-      --budget;
-    }
-    const int m = min(budget, n_inner + 1 - q[0].i);
-    double y0 = q[0].y, y1 = q[1].y, y2 = q[2].y, y3 = q[3].y;
-    const double e0 = q[0].eb, e1 = q[1].eb, e2 = q[2].eb, e3 = q[3].eb;
-#pragma unroll 2
-    for (int j = 0; j < m; ++j) {
-      const double u0 = __fma_rn(-y0, y0, y0);
-      const double u1 = __fma_rn(-y1, y1, y1);
-      const double u2 = __fma_rn(-y2, y2, y2);
-      const double u3 = __fma_rn(-y3, y3, y3);
-      y0 = __fma_rn(kR, u0, e0);
-      y1 = __fma_rn(kR, u1, e1);
-      y2 = __fma_rn(kR, u2, e2);
-      y3 = __fma_rn(kR, u3, e3);
-    }
-    q[0].y = y0;
-    q[1].y = y1;
-    q[2].y = y2;
-    q[3].y = y3;
-    budget -= m;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) q[j].i += m;
-    if (q[0].i == n_inner + 1) {
-      const int64_t lo = int64_t(q[0].l) * ks;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        A[off[j] + lo] = q[j].y;
-        q[j].l = q[j].l + 1 == nz ? 0 : q[j].l + 1;
-        --q[j].r;
-        q[j].i = 0;
-      }
-    }
-  }
-}
-
-template <int S, bool TIMED>
-__device__ __forceinline__ void tile_step4(double* __restrict__ ring, const TileDev tile,
-                                           const ChunkDev* __restrict__ chunks, int32_t nz,
-                                           int32_t F, const double* __restrict__ cfield,
-                                           int32_t nx, int32_t ny, int32_t shift,
-                                           int32_t n_inner,
-                                           unsigned long long* __restrict__ chunk_ns,
-                                           const HaloWait hw = HaloWait{nullptr, nullptr, 0, 0,
-                                                                        nullptr, nullptr, nullptr,
-                                                                        0, 0}) {
-  constexpr int TY = 8, HALF = 4;
-  constexpr int R = 8;
-  constexpr int PW = 68;
-  constexpr int PLANE = (TY + 2) * PW;
-  static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  double t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
-
-  const ChunkDev& c = chunks[tile.slot];
-  const int lx = threadIdx.x, ly = threadIdx.y;  // ly in [0, 4)
-  const int w = c.w, h = c.h, pitch = c.pitch;
-  const int64_t ks = c.kstride;
-  const int wv = min(64, w - tile.tx0), hv = min(TY, h - tile.ty0);
-  const int x = tile.tx0 + 2 * lx;
-  const int ya = tile.ty0 + ly, yb = ya + HALF;
-  const int pair = max(0, min(2, wv - 2 * lx));
-  const int na = ly < hv ? pair : 0;          // active cells, row a
-  const int nb = ly + HALF < hv ? pair : 0;   // row b
-  const int64_t own_a = int64_t(ya) * pitch + x;
-  const int64_t own_b = own_a + int64_t(HALF) * pitch;
-
-  const double* pa = c.in + own_a;
-  const double* pb = c.in + own_b;
-  // x halos: lane 0 (left) / lane 31 (right), for both rows of this thread
-  const double* pxa = nullptr;
-  const double* pxb = nullptr;
-  int64_t xstep = 0;
-  int oxa = 0, oxb = 0;
-  if (lx == 0 || lx == 31) {
-    const bool left = lx == 0;
-    const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
-    const int col = left ? 1 : wv + 2;
-    oxa = (ly + 1) * PW + col;
-    oxb = (ly + 1 + HALF) * PW + col;
-    if (xs >= 0 && xs < w) {
-      if (ly < hv) pxa = c.in + int64_t(ya) * pitch + xs;
-      if (ly + HALF < hv) pxb = c.in + int64_t(yb) * pitch + xs;
-      xstep = ks;
-    } else {
-      const FaceDev& fd = c.face[left ? kLeft : kRight];
-      if (ly < hv) pxa = fd.p + int64_t(ya) * fd.es;
-      if (ly + HALF < hv) pxb = fd.p + int64_t(yb) * fd.es;
-      xstep = fd.ks;
-    }
-  }
-  // y halos: row -1 by ly == 0, row hv by the thread owning row hv - 1
-  const double* py = nullptr;
-  int64_t ystep = 0;
-  int oy = 0, ycells = 0;
-  const bool top_duty = ly == 0;
-  const bool bot_duty = (hv - 1) == ly || (hv - 1) == ly + HALF;
-  const double* py2 = nullptr;
-  int64_t ystep2 = 0;
-  int oy2 = 0;
-  if (pair > 0 && top_duty) {
-    const int ys = tile.ty0 - 1;
-    oy = pair > 0 ? 2 + 2 * lx : 0;
-    ycells = pair;
-    if (ys >= 0) {
-      py = c.in + int64_t(ys) * pitch + x;
-      ystep = ks;
-    } else {
-      const FaceDev& fd = c.face[kTop];
-      py = fd.p + int64_t(x) * fd.es;
-      ystep = fd.ks;
-    }
-  }
-  if (pair > 0 && bot_duty) {
-    const int ys = tile.ty0 + hv;
-    oy2 = (hv + 1) * PW + 2 + 2 * lx;
-    ycells = pair;
-    if (ys < h) {
-      py2 = c.in + int64_t(ys) * pitch + x;
-      ystep2 = ks;
-    } else {
-      const FaceDev& fd = c.face[kBottom];
-      py2 = fd.p + int64_t(x) * fd.es;
-      ystep2 = fd.ks;
-    }
-  }
-  const int oca = (ly + 1) * PW + 2 + 2 * lx;
-  const int ocb = oca + HALF * PW;
-  const int levels = F * nz;
-
-  auto cp_cells = [&](double* dst, const double* src, int n) {
-    if (n == 2) cp_async16(dst, src);
-    else if (n == 1) cp_async8(dst, src);
-  };
-  auto issue = [&](int L) {
-    if (L < levels) {
-      double* slot = ring + (L & (R - 1)) * PLANE;
-      cp_cells(slot + oca, pa, na);
-      cp_cells(slot + ocb, pb, nb);
-      if (pxa) cp_async8(slot + oxa, pxa);
-      if (pxb) cp_async8(slot + oxb, pxb);
-      if (py) cp_cells(slot + oy, py, ycells);
-      if (py2) cp_cells(slot + oy2, py2, ycells);
-      pa += ks;
-      pb += ks;
-      if (pxa) pxa += xstep;  // a null duty pointer must stay null
-      if (pxb) pxb += xstep;
-      if (py) py += ystep;
-      if (py2) py2 += ystep2;
-    }
-    cp_async_commit();
-  };
-
-  // physics: chains 0,1 = row a (x, x+1); 2,3 = row b
-  const double* Bb = c.in;  // field 0 of U^t
-  double* Ab = c.a;
-  Chain ch[4];
-  int quota[4] = {0, 0, 0, 0};
-  int64_t off[4];
-  const int ncells[4] = {na >= 1, na == 2, nb >= 1, nb == 2};
-  unsigned long long my_ops = 0;  // TIMED: executed FP64 ops of this thread's cells
-  off[0] = own_a;
-  off[1] = own_a + 1;
-  off[2] = own_b;
-  off[3] = own_b + 1;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    int T = 0;
-    if (ncells[j]) {
-      const int cx = x + (j & 1), cy = (j < 2 ? ya : yb);
-      int row = c.y0 + cy - shift;
-      if (row < 0) row += ny;
-      const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + cx);
-      T = int(floor(__dmul_rn(double(nz), cm))) - 1;
-      if (T < 0) T = 0;
-      chain_init(ch[j], Bb + off[j], Ab + off[j], T, nz, ks);
-      if (TIMED) my_ops += (unsigned long long)T * trip_ops(n_inner) +
-                           (unsigned long long)nz * F * kJacobiOps;
-      quota[j] = int((int64_t(T) * (n_inner + 1) + levels - 1) / levels);
-      quota[j] = (quota[j] + 7) & ~7;
-    } else {
-      ch[j] = Chain{0.0, 0.0, 0, 0, 0};
-    }
-  }
-  const bool uniform = quota[0] == quota[1] && quota[1] == quota[2] && quota[2] == quota[3] &&
-                       ncells[0] && ncells[1] && ncells[2] && ncells[3];
-  // equal trip counts: the four chains stay in lockstep (equal budgets)
-  const bool lockstep = uniform && ch[0].r == ch[1].r && ch[1].r == ch[2].r && ch[2].r == ch[3].r;
-  int fast = 0;
-  auto physics = [&](int mult) {
-    if (fast > 0) {
-      const int b = quota[0] * mult;
-      double y0 = ch[0].y, y1 = ch[1].y, y2 = ch[2].y, y3 = ch[3].y;
-      const double e0 = ch[0].eb, e1 = ch[1].eb, e2 = ch[2].eb, e3 = ch[3].eb;
-      for (int j = 0; j < b; j += 8) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const double u0 = __fma_rn(-y0, y0, y0);
-          const double u1 = __fma_rn(-y1, y1, y1);
-          const double u2 = __fma_rn(-y2, y2, y2);
-          const double u3 = __fma_rn(-y3, y3, y3);
-          y0 = __fma_rn(kR, u0, e0);
-          y1 = __fma_rn(kR, u1, e1);
-          y2 = __fma_rn(kR, u2, e2);
-          y3 = __fma_rn(kR, u3, e3);
-        }
-      }
-      ch[0].y = y0;
-      ch[1].y = y1;
-      ch[2].y = y2;
-      ch[3].y = y3;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) ch[j].i += b;
-      --fast;
-      return;
-    }
-    if (lockstep) {
-      chain_advance4(ch, quota[0] * mult, Bb, Ab, off, nz, ks, n_inner);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (ncells[j])
-          chain_advance(ch[j], quota[j] * mult, Bb + off[j], Ab + off[j], nz, ks, n_inner);
-    }
-    if (uniform) {
-      const int b = quota[0] * mult;
-      int f = chain_fast(ch[0], b, n_inner);
-#pragma unroll
-      for (int j = 1; j < 4; ++j) f = min(f, chain_fast(ch[j], b, n_inner));
-      fast = f;
-    }
-  };
-
-  double zma0 = 0, zma1 = 0, zmb0 = 0, zmb1 = 0;
-  double* pouta = c.out + own_a;
-  double* poutb = c.out + own_b;
-  const double* rca = ring + oca;
-  const double* rcb = ring + ocb;
-  auto cell_pair = [&](const double* rc, int L, int k, int n, double& zm0, double& zm1,
-                       double* pout) {
-    const double* pl = rc + (L & (R - 1)) * PLANE;
-    if (n == 2) {
-      const double2 uc = *reinterpret_cast<const double2*>(pl);
-      const double xl = pl[-1], xr = pl[2];
-      const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
-      const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
-      double2 zu = uc;
-      if (k + 1 < nz) zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * PLANE);
-      const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
-      const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
-                                  __dadd_rn(zd0, zu.x));
-      const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
-                                  __dadd_rn(zd1, zu.y));
-      double2 o;
-      o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
-      o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
-      __stcs(reinterpret_cast<double2*>(pout), o);
-      zm0 = uc.x;
-      zm1 = uc.y;
-    } else if (n == 1) {
-      const double uc = pl[0];
-      const double zu = k + 1 < nz ? rc[((L + 1) & (R - 1)) * PLANE] : uc;
-      const double zd = k > 0 ? zm0 : uc;
-      const double sum = __dadd_rn(__dadd_rn(__dadd_rn(pl[-1], pl[1]), __dadd_rn(pl[-PW], pl[PW])),
-                                   __dadd_rn(zd, zu));
-      __stcs(pout, __fma_rn(kW1, sum, __dmul_rn(kW0, uc)));
-      zm0 = uc;
-    }
-  };
-
-  if (hw.n > 0 || hw.ndeps > 0) {
-    // halo strips or neighbour tiles not ready yet: pre-roll the physics
-    // (reads only this tile's own columns) while polling, as tile_step does
-    int maxr = 0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) maxr = max(maxr, ch[j].r);
-    const int64_t need = int64_t(maxr) * (n_inner + 1);
-    int64_t done = 0;
-    bool lead_ready = false;
-    for (;;) {
-      const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-      if (lead) {
-        if (done >= need) {
-          const uint64_t w0 = globaltimer_ns();
-          wait_ready(hw, 20ull * 1000 * 1000 * 1000);
-          if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
-          lead_ready = true;
-        } else {
-          lead_ready = stamps_ready(hw);
-        }
-      }
-      if (__syncthreads_or(lead && lead_ready)) break;
-      if (lockstep) {
-        chain_advance4(ch, kPreroll, Bb, Ab, off, nz, ks, n_inner);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (ncells[j]) chain_advance(ch[j], kPreroll, Bb + off[j], Ab + off[j], nz, ks, n_inner);
-      }
-      done += kPreroll;
-    }
-    fast = 0;
-  }
-
-  // ring hand-off through an mbarrier phase per level pair (see tile_step)
-  __shared__ uint64_t s_ring_bar4;
-  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == 0;
-  if (bar_lead) mbar_init(&s_ring_bar4, blockDim.x * blockDim.y);
-  __syncthreads();
-#pragma unroll
-  for (int L = 0; L < S; ++L) issue(L);
-  cp_async_wait<S - 3>();
-  mbar_arrive(&s_ring_bar4);
-
-  uint32_t parity = 0;
-  int k = 0, L = 0;
-  for (; L + 1 < levels; L += 2) {
-    mbar_wait(&s_ring_bar4, parity);
-    parity ^= 1;
-    issue(L + S);
-    issue(L + S + 1);
-    cell_pair(rca, L, k, na, zma0, zma1, pouta);
-    cell_pair(rcb, L, k, nb, zmb0, zmb1, poutb);
-    pouta += ks;
-    poutb += ks;
-    if (++k == nz) k = 0;
-    cell_pair(rca, L + 1, k, na, zma0, zma1, pouta);
-    cell_pair(rcb, L + 1, k, nb, zmb0, zmb1, poutb);
-    pouta += ks;
-    poutb += ks;
-    if (++k == nz) k = 0;
-    cp_async_wait<S - 3>();
-    mbar_arrive(&s_ring_bar4);
-    physics(2);
-  }
-  if (L < levels) {
-    mbar_wait(&s_ring_bar4, parity);
-    cell_pair(rca, L, k, na, zma0, zma1, pouta);
-    cell_pair(rcb, L, k, nb, zmb0, zmb1, poutb);
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  if (bar_lead) mbar_inval(&s_ring_bar4);
-  if (lockstep) {
-    chain_advance4(ch, 0x7fffffff, Bb, Ab, off, nz, ks, n_inner);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (ncells[j]) chain_advance(ch[j], 0x7fffffff, Bb + off[j], Ab + off[j], nz, ks, n_inner);
-  }
-
-  if (TIMED) {
-    charge_ops(chunk_ns, tile.slot, my_ops);
-    __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
-  }
-}
-
-template <int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(128, MINB)
-    column_step4(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                 int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                 int32_t shift, int32_t n_inner, unsigned long long* __restrict__ chunk_ns) {
-  __shared__ __align__(16) double ring[8 * 10 * 68];
-  tile_step4<S, TIMED>(ring, tiles[blockIdx.x], chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                       chunk_ns);
-}
-
-// Mode 6 on the mode-5 machinery: one CTA per 64x8 tile (four chains per
-// thread), heaviest first, pack-only CTAs ahead, cross-step overlap.
-template <int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(128, MINB)
-    column_step4_grid(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
-                      int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
-                      int32_t ny, int32_t shift, int32_t n_inner,
-                      unsigned long long* __restrict__ chunk_ns,
-                      const unsigned long long* __restrict__ halo_flags,
-                      const int32_t* __restrict__ senders, int32_t n_senders,
-                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
-                      const PackArgs pk, const StepDeps sd) {
-  __shared__ __align__(16) double ring[8 * 10 * 68];
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-  if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  if (int(blockIdx.x) < pk.ctas) {
-    if (pk.njobs > 0) pack_units(pk, chunks, nz, F, stamp, sd);
-    return;
-  }
-  const TileDev t = tiles[blockIdx.x - pk.ctas];
-  const int self = t.pad >> 1;
-  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
-              nullptr, nullptr, 0, 0};
-  if (sd.on) {
-    if (lead) {
-      const uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
-        if (globaltimer_ns() - t0 > 20ull * 1000 * 1000 * 1000) __trap();
-        __nanosleep(32);
-      }
-    }
-    __syncthreads();
-    hw.done = sd.done;
-    hw.deps = sd.idx + sd.off[self] + 1;
-    hw.ndeps = sd.off[self + 1] - sd.off[self] - 1;
-    hw.need = sd.step;
-  }
-  tile_step4<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
-  if (sd.on) {
-    __syncthreads();
-    __shared__ int s_last4;
-    if (lead) {
-      __threadfence();
-      st_release_gpu_u32(sd.done + self, sd.step + 1);
-      if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
-      s_last4 = sd.res_dst ? atomicAdd(sd.tile_cnt, 1u) == unsigned(sd.ntiles - 1) : 0;
-    }
-    if (sd.res_dst) {
-      __syncthreads();
-      if (s_last4) {
-        __threadfence();
-        const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-        for (int i = tid; i < sd.res_words; i += blockDim.x * blockDim.y)
-          sd.res_dst[i] = __ldcg(chunk_ns + i);
-        __threadfence_system();
-      }
-    }
-  }
-}
-
-template <int S, bool TIMED, int MINB>
-__global__ void __launch_bounds__(128, MINB)
-    column_step4_persistent(const ChunkDev* __restrict__ chunks,
-                            const TileDev* __restrict__ tiles, int32_t ntiles,
-                            unsigned int* __restrict__ counter, int32_t nz, int32_t F,
-                            const double* __restrict__ cfield, int32_t nx, int32_t ny,
-                            int32_t shift, int32_t n_inner,
-                            unsigned long long* __restrict__ chunk_ns,
-                            const unsigned long long* __restrict__ halo_flags,
-                            const int32_t* __restrict__ senders, int32_t n_senders,
-                            unsigned long long stamp, unsigned long long* __restrict__ wait_ns) {
-  __shared__ __align__(16) double ring[8 * 10 * 68];
-  __shared__ int s_next;
-  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
-  bool halo_ready = n_senders == 0;
-  for (;;) {
-    if (lead) s_next = int(atomicAdd(counter, 1u));
-    __syncthreads();
-    const int ti = s_next;
-    __syncthreads();
-    if (ti >= ntiles) break;
-    if (tiles[ti].pad & 1) {
-      if (lead && !halo_ready) {
-        const uint64_t w0 = globaltimer_ns();
-        wait_stamps(halo_flags, senders, n_senders, stamp, 20ull * 1000 * 1000 * 1000);
-        // time this SM idled for the neighbours (kept out of the load measurement)
-        if (wait_ns) atomicMax(wait_ns, (unsigned long long)(globaltimer_ns() - w0));
-        halo_ready = true;
-      }
-      __syncthreads();
-    }
-    tile_step4<S, TIMED>(ring, tiles[ti], chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                         chunk_ns);
-  }
+    tile_step_ws_partial<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                   chunk_ns, hw);
+  tile_publish(sd, self, chunk_ns);
 }
 
 // ---------------------------------------------------------------------------

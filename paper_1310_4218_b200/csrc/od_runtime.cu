@@ -64,6 +64,30 @@ static double now_s() {
 }
 
 constexpr int kTX = 32, kTY = 8, kPrefetch = 4, kFusedPrefetch = 6;
+constexpr int kGridMinBlocks = 5;  // column_step_grid CTAs per SM (94 registers)
+constexpr int kWsMinBlocks = 3;    // column_step_ws CTAs per SM
+
+// Fused-tile width for a chunk of w x h columns: the shape (tw x 256/tw, two
+// columns per thread, four row warps) that leaves the fewest idle lanes in the
+// warps that hold any cell of the chunk; ties go to the wider tile.  64-wide
+// chunks keep 64 x 4 tiles, cfg3's 32-wide chunks get 32 x 8, cfg1's 16 x 16,
+// cfg2's 8 x 8 chunks one fully used warp of an 8 x 32 tile.
+static int32_t tile_width(int32_t w, int32_t h) {
+  int32_t best = 64;
+  int64_t best_idle = -1;
+  for (int32_t tw = 64; tw >= 8; tw >>= 1) {
+    const int32_t th = 256 / tw, rpw = 64 / tw;  // rows per CTA, rows per warp
+    const int64_t tiles_x = (w + tw - 1) / tw;
+    const int64_t full_y = h / th, rem = h % th;
+    const int64_t warps_y = full_y * kRowWarps + (rem + rpw - 1) / rpw;
+    const int64_t idle = tiles_x * warps_y * 64 - int64_t(w) * h;
+    if (best_idle < 0 || idle < best_idle) {
+      best_idle = idle;
+      best = tw;
+    }
+  }
+  return best;
+}
 
 static int opposite(int d) { return d ^ 1; }
 
@@ -80,7 +104,9 @@ struct ChunkMem {
 
 struct StepRec {
   int32_t mode = kAsync;
-  int32_t epoch_step = 0;
+  int32_t epoch_step = 0;          // the caller's label (reference semantics: any value)
+  int32_t pos = 0;                 // position in the window: indexes the per-step device slots
+  int64_t gstep = 0;               // global step index (st_.steps at launch)
   int ev_begin = -1, ev_end = -1;
   double host_launch_s = 0;
   int ns_row = -1;                  // TIMER: row of the per-chunk ns counters
@@ -112,10 +138,13 @@ class Runtime {
   void stats(od_rt_stats* s);
   void set_profiling(bool on) { profiling_ = on; }
   const std::vector<od_epoch_summary>& history() const { return history_; }
+  void step_walls(int64_t first, int32_t n, double* out) const;
   void sync() { OD_CU(cudaStreamSynchronize(s0_)); }
 
  private:
-  int rank_of_proc(int32_t p) const { return p / cfg_.procs_per_node; }
+  // processors (the reference's nodes x procs_per_node) are dealt to the GPUs
+  // (ranks) in contiguous blocks; world == nodes gives node = GPU
+  int rank_of_proc(int32_t p) const { return int(int64_t(p) * world_ / P()); }
   int rank_of_vp(int32_t v) const { return rank_of_proc(map_[v]); }
   int32_t nbr(int32_t v, int d) const;
   void set_shift(int32_t rows);
@@ -126,7 +155,8 @@ class Runtime {
   FaceDev edge_of(const ChunkMem& s, int side, int par) const;
   int new_event();
   void begin_window(bool allow_overlap = true);
-  void launch_step(int32_t mode, int32_t epoch_step, bool host_io);
+  void launch_step(int32_t mode, int32_t epoch_step, bool host_io,
+                   const double* host_field = nullptr);
   // waits for the window, gathers per-step walls and the K x S sample matrix
   void collect(std::vector<double>& walls, std::vector<double>& samples);
   struct EpochOut {
@@ -137,6 +167,7 @@ class Runtime {
     double mig_s = 0, imb_before = 1, imb_after = 1;
   };
   void finish_epoch(int32_t e, int32_t steps, EpochOut& out);
+  void require_no_open_window(const char* who) const;
 
   od_config cfg_;
   int rank_, world_, device_;
@@ -151,7 +182,6 @@ class Runtime {
 
   cudaStream_t s0_ = nullptr;
   unsigned int* d_counter_ = nullptr;
-  int phys_ctas_ = 0;               // persistent physics grid
   ncclComm_t comm_ = nullptr;
   double* d_cbase_ = nullptr;   // base load field (device copy)
   // host_io path: the shifted field staged from pinned host memory every step
@@ -179,13 +209,8 @@ class Runtime {
   std::vector<int32_t> resident_;  // slot -> vp
   std::vector<int32_t> tile_begin_, tile_count_;
   int32_t ntiles_ = 0;
-  // 64 x 8 tiles of the one-CTA-per-tile fused kernel (column_step3, mode 4)
-  std::vector<int32_t> tile2_begin_, tile2_count_;
-  int32_t ntiles2_ = 0;
-  TileDev* d_tiles2_ = nullptr;
-  size_t d_tiles2_cap_ = 0;
-  // persistent fused kernel: 64 x kTY4 tiles in descending-work order
-  int kTY4 = 4;  // persistent tile height: 4 (mode 5) or 8 (mode 6)
+  // fused-kernel tiles (tw x th, shape per chunk width: tile_shape), grouped by
+  // chunk, and a heaviest-first copy for the batched launch
   std::vector<TileDev> tiles4_;          // grouped by chunk
   std::vector<int32_t> tile4_begin_, tile4_count_;
   TileDev* d_tiles4_ = nullptr;          // grouped (per-chunk launches)
@@ -195,15 +220,16 @@ class Runtime {
   size_t tiles4_cap_ = 0;
   int tiles4s_cur_ = 0;
   bool order_dirty_ = true;
-  int persist_grid_ = 0;
-  int persist_minb_ = 5;
+  int wave_ = 0;       // tiles one launch keeps resident (SMs x CTAs per SM)
   int sms_ = 1;
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
-  bool grid_launch_ = true;  // mode 5 as one CTA per tile (column_step_grid)
-  int ws_mode_ = -1;         // OD_WS: -1 auto (less than a wave of tiles), 0 never, 1 always
-  int grid_minb_ = 5;        // OD_GRID_MINB=6: 6 CTAs/SM build (80 registers)
-  size_t grid_pad_smem_ = 0;  // OD_GRID_SMEM: unused dynamic smem per CTA (caps CTAs/SM)
   void refresh_tile_order();
+  // mode 5: the warp-specialised tile when a GPU holds less than one wave of
+  // tiles (latency-bound), the interleaved tile otherwise; mode 7 always WS
+  bool use_ws(int ntiles) const {
+    return cfg_.overlap == 7 || (cfg_.overlap == 5 && ntiles < wave_);
+  }
+  int32_t last_kernel_ = 0;  // OD_KERNEL_* of the last step kernel launched
   // cross-step overlap of the mode-5 step kernels (PDL + per-tile stamps;
   // OD_OVERLAP=0 disables): tile -> same-GPU tiles whose cells it reads (itself first),
   // pack job -> tiles holding its face cells; per-tile completed-step stamps
@@ -286,6 +312,7 @@ class Runtime {
   bool profiling_ = false;
   std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_, prof_f_;
   od_rt_stats st_{};
+  std::vector<double> step_wall_;  // by global step index (NaN until collected)
   std::vector<od_epoch_summary> history_;
 };
 
@@ -319,31 +346,31 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
       cfg.later_call_strategy < 0 || cfg.later_call_strategy > 2)
     throw ValidationError("unknown strategy");
   if (cfg.n_inner < 0) throw ValidationError("n_inner must be >= 0");
-  if (cfg.overlap != 0 && (cfg.overlap < 4 || cfg.overlap > 7))
-    throw ValidationError("unknown kernel mode (overlap): 0, 4, 5 or 6");
+  if (cfg.overlap != 0 && cfg.overlap != 4 && cfg.overlap != 5 && cfg.overlap != 7)
+    throw ValidationError("unknown kernel mode (overlap): 0 separate, 4 interleaved tiles, "
+                          "5 automatic, 7 warp-specialised tiles");
   if (cfg.measure != OD_MEASURE_EVENTS && cfg.measure != OD_MEASURE_TIMER &&
       cfg.measure != OD_MEASURE_TIMER_RAW && cfg.measure != OD_MEASURE_OPS)
     throw ValidationError("unknown measurement mode");
-  if (world != cfg.nodes)
-    throw ValidationError("one rank per node GPU: world size must equal cluster.nodes");
+  if (world < 1 || world > cfg.nodes * cfg.procs_per_node)
+    throw ValidationError("world size must be between 1 and the processor count "
+                          "(cluster.nodes x cluster.procs_per_node)");
   if (rank < 0 || rank >= world) throw ValidationError("rank out of range");
   if (world > 1 && !nccl_id) throw ValidationError("multi-rank runtime needs an NCCL id");
 
   subs_ = cfg.decomposition_kind == OD_ONE_D ? strips_1d(cfg.nx, cfg.ny, cfg.ky)
                                              : tiles_2d(cfg.nx, cfg.ny, cfg.kx, cfg.ky);
   map_ = block_mapping(K(), P());
+  // static_node0 heats the VPs initially homed on the reference's node 0
+  // (workload.hpp:160-181 via engine.hpp:141-148), whatever GPU holds them
   std::vector<Sub> node0;
   for (int32_t v = 0; v < K(); ++v)
-    if (rank_of_vp(v) == 0) node0.push_back(subs_[v]);
+    if (map_[v] / cfg.procs_per_node == 0) node0.push_back(subs_[v]);
   base_ = make_load_field(cfg.nx, cfg.ny, Pattern(cfg.pattern), cfg.heavy_value,
                           cfg.light_value, node0);
 
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
-  if (const char* mn = std::getenv("OD_SHARE_MIN_N")) {
-    const int v = std::max(1, std::atoi(mn));
-    OD_CU(cudaMemcpyToSymbol(g_share_min_n, &v, sizeof(v)));
-  }
   if (std::getenv("OD_TILELOG")) {
     slog_cap_ = 1u << 20;
     slog_step_ = std::getenv("OD_TILELOG_STEP") ? std::atol(std::getenv("OD_TILELOG_STEP")) : 19;
@@ -358,44 +385,16 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     int sms = 0;
     OD_CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device_));
     sms_ = sms;
-    // mode 5 launches one CTA per tile (column_step_grid) unless OD_GRID=0
-    // selects the persistent tile-pulling kernel (column_step_persistent)
-    grid_launch_ = !(std::getenv("OD_GRID") && std::string(std::getenv("OD_GRID")) == "0");
-    grid_minb_ = std::getenv("OD_GRID_MINB") ? std::atoi(std::getenv("OD_GRID_MINB")) : 5;
-    ws_mode_ = std::getenv("OD_WS") ? std::atoi(std::getenv("OD_WS")) : -1;
-    grid_pad_smem_ = std::getenv("OD_GRID_SMEM") ? size_t(std::atol(std::getenv("OD_GRID_SMEM"))) : 0;
-    // cross-step overlap of the mode-5 step kernels unless OD_OVERLAP=0
+    // cross-step overlap of the step kernels unless OD_OVERLAP=0 (diagnostic)
     overlap_ = !(std::getenv("OD_OVERLAP") && std::string(std::getenv("OD_OVERLAP")) == "0");
+    // P2P halos: the step kernel's first CTAs pack the strips (OD_PACK_CTAS=0:
+    // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
-    const char* e = std::getenv("OD_PHYS_CTAS_PER_SM");
-    phys_ctas_ = sms * (e ? std::max(1, std::atoi(e)) : 2);
     OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
-    // Concurrent kernels can share an SM only with the same L1/smem split:
-    // give the co-scheduled kernels one carveout so the Jacobi CTAs fit next
-    // to the persistent physics CTAs.
-    const char* cv = std::getenv("OD_SMEM_CARVEOUT");
-    const int carve = cv ? std::atoi(cv) : 100;
-    auto set_carve = [&](const void* fn) {
-      OD_CU(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    };
-    set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, true>));
-    set_carve(reinterpret_cast<const void*>(&jacobi_step<kTX, kTY, kPrefetch, false>));
     int per_sm = 0;
-    const char* pm = std::getenv("OD_PERSIST_MINB");
-    persist_minb_ = pm ? std::atoi(pm) : 5;
-    if (persist_minb_ == 6)
-      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, column_step_persistent<4, kFusedPrefetch, false, 6>, kTX * 4, 0));
-    else
-      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, column_step_persistent<4, kFusedPrefetch, false, 5>, kTX * 4, 0));
-    if (cfg.overlap == 6) {
-      kTY4 = 8;
-      OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-          &per_sm, column_step4_persistent<kFusedPrefetch, false, 4>, kTX * 4, 0));
-    }
-    if (const char* pc = std::getenv("OD_PERSIST_CTAS")) per_sm = std::min(per_sm, std::atoi(pc));
-    persist_grid_ = sms * std::max(per_sm, 1);
+    OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, column_step_grid<kFusedPrefetch, false, kGridMinBlocks>, 32 * kRowWarps, 0));
+    wave_ = sms * std::max(per_sm, 1);
   }
   if (world_ > 1) {
     ncclUniqueId id;
@@ -517,7 +516,6 @@ Runtime::~Runtime() {
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
   cudaFree(d_tiles_);
-  cudaFree(d_tiles2_);
   cudaFree(d_tiles4_);
   for (int b = 0; b < 2; ++b) {
     cudaFree(d_tiles4s_[b]);
@@ -560,7 +558,7 @@ void Runtime::set_shift(int32_t rows) {
   order_dirty_ = true;
 }
 
-// Heaviest tiles first (longest-processing-time order) for the persistent
+// Heaviest tiles first (longest-processing-time order) for the batched step
 // kernel: estimated work = physics units + Jacobi cells, from the current field.
 void Runtime::refresh_tile_order() {
   const size_t n = tiles4_.size();
@@ -570,8 +568,6 @@ void Runtime::refresh_tile_order() {
   // position (and with it every issue priority on the SM: the warp scheduler
   // favours older CTAs) and the per-chunk measurements average over them
   std::vector<std::tuple<double, int32_t, int32_t>> key(n);
-  static const bool chunk_major = std::getenv("OD_TILE_ORDER") &&
-                                  std::string(std::getenv("OD_TILE_ORDER")) == "chunk";
   const double jac = 2.0 * cfg_.nz * cfg_.fields;  // a Jacobi cell ~ 2 micro-steps
   if (tile_work_.size() != size_t(K())) {
     tile_work_.assign(K(), {});
@@ -589,8 +585,8 @@ void Runtime::refresh_tile_order() {
       const Sub& s = subs_[vp];
       for (int32_t j = 0; j < tile4_count_[td.slot]; ++j) {
         const TileDev& tj = tiles4_[tile4_begin_[td.slot] + j];
-        const int32_t x0 = s.x0 + tj.tx0, x1 = std::min(s.x1, x0 + 2 * kTX);
-        const int32_t y0 = s.y0 + tj.ty0, y1 = std::min(s.y1, y0 + kTY4);
+        const int32_t x0 = s.x0 + tj.tx0, x1 = std::min(s.x1, x0 + tj.tw);
+        const int32_t y0 = s.y0 + tj.ty0, y1 = std::min(s.y1, y0 + tj.th);
         double w = 0;
         for (int32_t y = y0; y < y1; ++y)
           for (int32_t x = x0; x < x1; ++x) {
@@ -601,49 +597,21 @@ void Runtime::refresh_tile_order() {
       }
     }
     const double w = tile_work_[vp][local];
-    key[t] = {-w, chunk_major ? 0 : int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
+    key[t] = {-w, int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
   }
   std::sort(key.begin(), key.end());
-  // diagnostic order variants (OD_ORDER): spt = lightest first; lightwave =
-  // the lightest tiles form the first wave, then heaviest first; shuffle
-  if (const char* ov = std::getenv("OD_ORDER")) {
-    const std::string o(ov);
-    if (o == "spt") {
-      std::stable_sort(key.begin(), key.end(), [](const auto& a, const auto& b) {
-        return std::get<0>(a) > std::get<0>(b);
-      });
-    } else if (o == "lightwave") {
-      const size_t g = std::min(n, size_t(persist_grid_));
-      std::rotate(key.begin(), key.end() - g, key.end());
-    } else if (o == "shuffle") {
-      uint64_t st = 12345;
-      for (size_t i = n; i > 1; --i) {
-        st = mix64(st);
-        std::swap(key[i - 1], key[st % i]);
-      }
-    }
-  }
-  static const bool boundary_last = std::getenv("OD_BOUNDARY_LAST") != nullptr;
-  // OD_FIRSTWAVE=0: plain heaviest-first (boundary tiles in the first wave
-  // pre-roll their physics until the strips land); measured 5-7 % slower at 4
-  // GPUs on cfg4 than keeping them out of the first wave
-  static const bool first_wave_interior =
-      !(std::getenv("OD_FIRSTWAVE") && std::string(std::getenv("OD_FIRSTWAVE")) == "0");
-  if (p2p_ && n_senders_ > 0 && boundary_last) {
-    std::stable_sort(key.begin(), key.end(), [&](const auto& a, const auto& b) {
-      return (tiles4_[std::get<2>(a)].pad & 1) < (tiles4_[std::get<2>(b)].pad & 1);
-    });
-  } else if (p2p_ && n_senders_ > 0 && first_wave_interior) {
+  if (p2p_ && n_senders_ > 0) {
     // with peer-memory halos the neighbours' strips of this step land while the
     // kernel runs: the first wave (one tile per CTA) takes the heaviest tiles
     // that read no remote strip; everything after it stays in heaviest-first
     // order (deferring all boundary tiles to the end would put heavy migrated
-    // chunks -- typically boundary after a rebalance -- into the tail)
+    // chunks -- typically boundary after a rebalance -- into the tail).
+    // Measured 5-7 % faster at 4 GPUs on cfg4 than plain heaviest-first.
     std::vector<std::tuple<double, int32_t, int32_t>> front, rest;
     front.reserve(n);
     rest.reserve(n);
     for (const auto& k : key)
-      (front.size() < size_t(persist_grid_) && !(tiles4_[std::get<2>(k)].pad & 1) ? front : rest)
+      (front.size() < size_t(wave_) && !(tiles4_[std::get<2>(k)].pad & 1) ? front : rest)
           .push_back(k);
     front.insert(front.end(), rest.begin(), rest.end());
     key.swap(front);
@@ -779,8 +747,8 @@ void Runtime::build_step_deps() {
   };
   auto rect = [&](const TileDev& t) {
     const Sub& s = subs_[resident_[t.slot]];
-    return Rect{s.x0 + t.tx0, std::min(s.x1, s.x0 + t.tx0 + 2 * kTX), s.y0 + t.ty0,
-                std::min(s.y1, s.y0 + t.ty0 + kTY4)};
+    return Rect{s.x0 + t.tx0, std::min(s.x1, s.x0 + t.tx0 + t.tw), s.y0 + t.ty0,
+                std::min(s.y1, s.y0 + t.ty0 + t.th)};
   };
   auto overlaps = [](const Rect& a, const Rect& b) {
     return a.x0 < b.x1 && b.x0 < a.x1 && a.y0 < b.y1 && b.y0 < a.y1;
@@ -823,9 +791,9 @@ void Runtime::build_step_deps() {
     for (int32_t j = j0; j < j1; ++j) {
       const TileDev& tj = tiles4_[j];
       const bool edge = (pj.side == kLeft && tj.tx0 == 0) ||
-                        (pj.side == kRight && tj.tx0 + 2 * kTX >= s.w()) ||
+                        (pj.side == kRight && tj.tx0 + tj.tw >= s.w()) ||
                         (pj.side == kTop && tj.ty0 == 0) ||
-                        (pj.side == kBottom && tj.ty0 + kTY4 >= s.h());
+                        (pj.side == kBottom && tj.ty0 + tj.th >= s.h());
       if (edge) jidx.push_back(j);
     }
   }
@@ -875,18 +843,6 @@ void Runtime::rebuild_tables() {
   }
   ntiles_ = int32_t(tiles.size());
   upload(d_tiles_, d_tiles_cap_, tiles);
-  std::vector<TileDev> tiles2;
-  tile2_begin_.assign(nres, 0);
-  tile2_count_.assign(nres, 0);
-  for (int32_t i = 0; i < nres; ++i) {
-    const Sub& s = subs_[resident_[i]];
-    tile2_begin_[i] = int32_t(tiles2.size());
-    for (int32_t ty = 0; ty < s.h(); ty += kTY)
-      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) tiles2.push_back(TileDev{i, tx, ty, 0});
-    tile2_count_[i] = int32_t(tiles2.size()) - tile2_begin_[i];
-  }
-  ntiles2_ = int32_t(tiles2.size());
-  upload(d_tiles2_, d_tiles2_cap_, tiles2);
   tiles4_.clear();
   tile4_begin_.assign(nres, 0);
   tile4_count_.assign(nres, 0);
@@ -899,12 +855,15 @@ void Runtime::rebuild_tables() {
       const int32_t n = nbr(v, d);
       remote[d] = n >= 0 && rank_of_vp(n) != rank_;
     }
-    for (int32_t ty = 0; ty < s.h(); ty += kTY4)
-      for (int32_t tx = 0; tx < s.w(); tx += 2 * kTX) {
-        const bool needs = (remote[kLeft] && tx == 0) || (remote[kRight] && tx + 2 * kTX >= s.w()) ||
-                           (remote[kTop] && ty == 0) || (remote[kBottom] && ty + kTY4 >= s.h());
+    const int32_t tw = tile_width(s.w(), s.h()), th = 256 / tw;
+    const int32_t lg = tw == 64 ? 5 : tw == 32 ? 4 : tw == 16 ? 3 : 2;
+    for (int32_t ty = 0; ty < s.h(); ty += th)
+      for (int32_t tx = 0; tx < s.w(); tx += tw) {
+        const bool needs = (remote[kLeft] && tx == 0) || (remote[kRight] && tx + tw >= s.w()) ||
+                           (remote[kTop] && ty == 0) || (remote[kBottom] && ty + th >= s.h());
         // pad: bit 0 = reads a remote strip, bits 1.. = canonical tile id
-        tiles4_.push_back(TileDev{i, tx, ty, (needs ? 1 : 0) | (int32_t(tiles4_.size()) << 1)});
+        tiles4_.push_back(TileDev{i, tx, ty, (needs ? 1 : 0) | (int32_t(tiles4_.size()) << 1),
+                                  tw, th, lg, 0});
       }
     tile4_count_[i] = int32_t(tiles4_.size()) - tile4_begin_[i];
   }
@@ -916,8 +875,10 @@ void Runtime::rebuild_tables() {
       if (h_tiles4s_[b]) cudaFreeHost(h_tiles4s_[b]);
     }
     size_t all = 0;
-    for (const Sub& sb : subs_)
-      all += size_t((sb.h() + kTY4 - 1) / kTY4) * size_t((sb.w() + 2 * kTX - 1) / (2 * kTX));
+    for (const Sub& sb : subs_) {
+      const int32_t tw = tile_width(sb.w(), sb.h()), th = 256 / tw;
+      all += size_t((sb.h() + th - 1) / th) * size_t((sb.w() + tw - 1) / tw);
+    }
     tiles4_cap_ = std::max<size_t>({tiles4_.size(), all, 16});
     OD_CU(cudaMalloc(&d_tiles4_, tiles4_cap_ * sizeof(TileDev)));
     for (int b = 0; b < 2; ++b) {
@@ -1148,8 +1109,7 @@ void Runtime::begin_window(bool allow_overlap) {
   window_.clear();
   ev_used_ = 0;
   ns_used_ = 0;
-  win_overlap_ = overlap_ && allow_overlap && (cfg_.overlap >= 5) &&
-                 grid_launch_ && !d_tl_ &&
+  win_overlap_ = overlap_ && allow_overlap && cfg_.overlap != 0 && !d_tl_ &&
                  (cfg_.measure == OD_MEASURE_TIMER || cfg_.measure == OD_MEASURE_TIMER_RAW);
   if (win_overlap_) {
     const int32_t S = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
@@ -1188,11 +1148,17 @@ void Runtime::begin_window(bool allow_overlap) {
   prof_x_.clear();
 }
 
-void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
+void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
+                          const double* host_field) {
   const auto t0 = std::chrono::steady_clock::now();
   StepRec r;
   r.mode = mode;
   r.epoch_step = epoch_step;
+  // per-step device slots (step stamps, pack counters, mapped field buffers)
+  // are indexed by the step's position in the window, never by the label
+  const int32_t pos = int32_t(window_.size());
+  r.pos = pos;
+  r.gstep = st_.steps;
   r.slot_vps = resident_;
   const int par = parity_;
   const int32_t nres = int32_t(resident_.size());
@@ -1201,7 +1167,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
                                                     cfg_.measure == OD_MEASURE_OPS));
   // overlapped step: launched with programmatic dependent launch right behind
   // the previous step kernel; no stream operation may sit between them
-  r.ovl = win_overlap_ && (!host_io || int32_t(d_ring_.size()) > epoch_step) &&
+  r.ovl = win_overlap_ && pos < win_cap_ && (!host_io || int32_t(d_ring_.size()) > pos) &&
           !tiles4_.empty() && (mode == kAsync || timer);
   if (r.ovl && order_dirty_) refresh_tile_order();  // (its upload breaks the chain once)
   r.ovl_chained = r.ovl && !window_.empty() && window_.back().ovl;
@@ -1209,24 +1175,27 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     r.ev_begin = new_event();
     OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
   } else if (!r.ovl_chained) {
-    stamp_time<<<1, 1, 0, s0_>>>(d_stepend_ + 2 * epoch_step);  // start of a chain
+    stamp_time<<<1, 1, 0, s0_>>>(d_stepend_ + 2 * pos);  // start of a chain
     ++st_.kernel_launches;
   }
   tl_mark(0);
 
   const double* cfield = d_cbase_;
   int32_t shift = shift_ % cfg_.ny;
+  // host-facing steps: the step's load field comes from the caller's host
+  // buffer (or, without one, the runtime's own shifted field, which the
+  // reference keeps on the host: engine.hpp:337-342)
+  const double* hsrc = host_field ? host_field : field_.c.data();
   if (host_io && r.ovl) {
-    // the reference keeps the shifted load field on the host (engine.hpp:337-342);
     // overlapped: the step kernel reads this step's mapped pinned copy over the
     // host link (8 B per column per step, no copy operation between the kernels)
-    std::memcpy(h_ring_[epoch_step], field_.c.data(), field_.c.size() * sizeof(double));
-    cfield = d_ring_[epoch_step];
+    std::memcpy(h_ring_[pos], hsrc, field_.c.size() * sizeof(double));
+    cfield = d_ring_[pos];
     shift = 0;
   } else if (host_io) {
     const int b = cstage_cur_ ^= 1;
     OD_CU(cudaEventSynchronize(cstage_ev_[b]));  // the copy two steps ago has left it
-    std::memcpy(h_cstage_[b], field_.c.data(), field_.c.size() * sizeof(double));
+    std::memcpy(h_cstage_[b], hsrc, field_.c.size() * sizeof(double));
     OD_CU(cudaMemcpyAsync(d_cstage_[b], h_cstage_[b], field_.c.size() * sizeof(double),
                           cudaMemcpyHostToDevice, s0_));
     OD_CU(cudaEventRecord(cstage_ev_[b], s0_));
@@ -1256,10 +1225,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
   }
 
   // boundaries of chunks that border another GPU
-  const bool fused_pack = p2p_ && pack_ctas_ > 0 && !tiles4_.empty() &&
-                          (cfg_.overlap == 5 || cfg_.overlap == 7 ||
-                           (cfg_.overlap == 6 && grid_launch_)) &&
-                          (mode == kAsync || timer);
+  const bool fused = cfg_.overlap != 0 && !tiles4_.empty() && (mode == kAsync || timer);
+  const bool fused_pack = p2p_ && pack_ctas_ > 0 && fused;
   if (p2p_ && (!jobs_.empty() || n_senders_ > 0)) {
     // pack straight into the neighbours' receive buffers over NVLink, publish
     // the step, then wait for the neighbours' strips of this step
@@ -1285,10 +1252,9 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       e1 = new_event();
       OD_CU(cudaEventRecord(events_[e1], s0_));
     }
-    // the persistent kernels wait inside, before the first tile that needs a
-    // remote strip; the other kernels wait here
-    const bool in_kernel = (cfg_.overlap >= 5) &&
-                           (mode == kAsync || timer);
+    // the fused step kernels wait inside, per tile that needs a remote strip
+    // (pre-rolling its physics); the separate kernels wait here
+    const bool in_kernel = fused;
     if (n_senders_ > 0 && !in_kernel) {
       wait_halo<<<1, 32, 0, s0_>>>(d_flags_, d_senders_, n_senders_, stamp,
                                    20ull * 1000 * 1000 * 1000);
@@ -1344,39 +1310,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     r.kev0 = new_event();
     OD_CU(cudaEventRecord(events_[r.kev0], s0_));
   }
-  if ((mode == kAsync || timer) && !tiles4_.empty() && cfg_.overlap == 6 && !grid_launch_) {
-    if (order_dirty_) refresh_tile_order();
-    int e0 = -1, e1 = -1;
-    if (profiling_) {
-      e0 = new_event();
-      OD_CU(cudaEventRecord(events_[e0], s0_));
-    }
-    OD_CU(cudaMemsetAsync(d_counter_, 0, sizeof(unsigned int), s0_));
-    tl_mark(2);
-    const int nt = int(tiles4_.size());
-    const int grid = std::min(nt, persist_grid_);
-    const int32_t nsend = p2p_ ? n_senders_ : 0;
-    const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
-    if (timer)
-      column_step4_persistent<kFusedPrefetch, true, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
-          d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
-          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend, stamp,
-          ns + (ns_cols_ - 1));
-    else
-      column_step4_persistent<kFusedPrefetch, false, 4><<<grid, dim3(kTX, 4), 0, s0_>>>(
-          d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,
-          cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend,
-          stamp, tl_wait());
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
-      e1 = new_event();
-      OD_CU(cudaEventRecord(events_[e1], s0_));
-      prof_f_.push_back({e0, e1});
-    }
-    st_.kernel_launches += 1;
-    st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && !tiles4_.empty() &&
-             (cfg_.overlap == 5 || cfg_.overlap == 6 || cfg_.overlap == 7)) {
+  if (fused) {
     if (order_dirty_) refresh_tile_order();
     int e0 = -1, e1 = -1;
     const bool prof_f = profiling_ && !r.ovl;
@@ -1387,170 +1321,86 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     if (!r.ovl) OD_CU(cudaMemsetAsync(d_counter_, 0, 3 * sizeof(unsigned int), s0_));
     tl_mark(2);
     const int nt = int(tiles4_.size());
-    const int grid = std::min(nt, persist_grid_);
-    const dim3 blk4(kTX, 4);
     PackArgs pk{};
     if (fused_pack && !jobs_.empty()) {
+      // pack-only CTAs ahead of the tiles
       pk.jobs = d_jobs_;
       pk.njobs = int32_t(jobs_.size());
-      pk.ctas = std::min(pack_ctas_, grid);
+      pk.ctas = std::min(pack_ctas_, int(pk.njobs) * cfg_.fields);
       pk.peer_base = d_peer_base_;
       pk.half_elems = recv_half_;
       pk.par = par;
       pk.n_notify = n_notify_;
       pk.my_rank = rank_;
-      pk.counters = r.ovl ? d_pcnt_ + 4 * epoch_step : d_counter_ + 1;
+      pk.first = 0;
+      pk.counters = r.ovl ? d_pcnt_ + 4 * pos : d_counter_ + 1;
       pk.peer_flags = d_peer_flags_;
       pk.notify = d_notify_;
     }
     const int32_t nsend = p2p_ ? n_senders_ : 0;
     const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
-#define OD_LAUNCH_PS(MB)                                                                    \
-  if (timer)                                                                                \
-    column_step_persistent<4, kFusedPrefetch, true, MB><<<grid, blk4, 0, s0_>>>(         \
-        d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
-        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns, d_flags_, d_senders_, nsend,     \
-        stamp, ns + (ns_cols_ - 1), pk);                           \
-  else                                                                                      \
-    column_step_persistent<4, kFusedPrefetch, false, MB><<<grid, blk4, 0, s0_>>>(        \
-        d_chunks_[par], d_tiles4s_[tiles4s_cur_], nt, d_counter_, cfg_.nz, cfg_.fields,    \
-        cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, nsend, \
-        stamp, tl_wait(), pk);
-    if (grid_launch_) {
-      // one CTA per tile, heaviest first; the fused pack rides on the last
-      // CTAs of the first wave (the lightest tiles of it)
-      // pack-only CTAs ahead of the tiles (column_step_grid)
-      if (pk.njobs > 0) {
-        pk.first = 0;
-        pk.ctas = std::min(pack_ctas_, int(pk.njobs) * cfg_.fields);
-      } else {
-        pk.ctas = 0;
+    StepDeps sd{};
+    if (r.ovl) {
+      sd.off = d_deps_;
+      sd.idx = d_deps_ + dep_idx_at_;
+      sd.joff = d_deps_ + dep_joff_at_;
+      sd.jidx = d_deps_ + dep_jidx_at_;
+      sd.done = d_done_;
+      sd.end_ns = d_stepend_ + 2 * pos + 1;
+      sd.step = unsigned(st_.steps);
+      sd.on = 1;
+      if (host_io && nres > 0) {
+        sd.tile_cnt = d_pcnt_ + 4 * pos + 2;
+        sd.ntiles = nt;
+        sd.res_words = 2 * nres;
+        sd.res_dst = d_loads_dst_;
       }
-      StepDeps sd{};
-      if (r.ovl) {
-        sd.off = d_deps_;
-        sd.idx = d_deps_ + dep_idx_at_;
-        sd.joff = d_deps_ + dep_joff_at_;
-        sd.jidx = d_deps_ + dep_jidx_at_;
-        sd.done = d_done_;
-        sd.end_ns = d_stepend_ + 2 * epoch_step + 1;
-        sd.step = unsigned(st_.steps);
-        sd.on = 1;
-        if (host_io && nres > 0) {
-          sd.tile_cnt = d_pcnt_ + 4 * epoch_step + 2;
-          sd.ntiles = nt;
-          sd.res_words = 2 * nres;
-          sd.res_dst = d_loads_dst_;
-        }
-      }
-      // overlapped steps: programmatic dependent launch, so this grid starts
-      // while the previous step's last tiles drain (tiles wait on per-tile stamps)
-      cudaLaunchConfig_t lc{};
-      lc.gridDim = dim3(unsigned(nt + pk.ctas));
-      lc.blockDim = blk4;
-      lc.dynamicSmemBytes = grid_pad_smem_;  // (occupancy experiments: OD_GRID_SMEM)
-      lc.stream = s0_;
-      cudaLaunchAttribute la[1];
-      la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      la[0].val.programmaticStreamSerializationAllowed = 1;
-      lc.attrs = la;
-      lc.numAttrs = r.ovl ? 1 : 0;
-      const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
-      const ChunkDev* chk = d_chunks_[par];
-      // mode 5 on a GPU holding less than one wave of tiles is latency-bound:
-      // there the warp-specialised tile (mode 7) overlaps a tile's physics with
-      // its Jacobi instead of running them back to back (OD_WS=0/1 overrides)
-      const bool ws = cfg_.overlap == 7 ||
-                      (cfg_.overlap == 5 && (ws_mode_ == 1 || (ws_mode_ < 0 && nt < persist_grid_)));
-      if (ws) {
-        // warp-specialised tiles (column_step_ws): physics and Jacobi warps
-        lc.blockDim = dim3(kTX, 8);
-        if (timer)
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<4, true, 3>, chk, tl4, cfg_.nz,
-                                   cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, ns,
-                                   (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   ns + (ns_cols_ - 1), pk, sd));
-        else
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<4, false, 3>, chk, tl4, cfg_.nz,
-                                   cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner,
-                                   (unsigned long long*)nullptr,
-                                   (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   r.ovl ? nullptr : tl_wait(), pk, sd));
-      } else if (cfg_.overlap == 6) {
-        // four chains per thread, 64x8 tiles (column_step4_grid)
-        if (timer)
-          OD_CU(cudaLaunchKernelEx(&lc, column_step4_grid<kFusedPrefetch, true, 4>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   ns + (ns_cols_ - 1), pk, sd));
-        else
-          OD_CU(cudaLaunchKernelEx(&lc, column_step4_grid<kFusedPrefetch, false, 4>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, (unsigned long long*)nullptr,
-                                   (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   r.ovl ? nullptr : tl_wait(), pk, sd));
-      } else if (grid_minb_ == 6) {
-        if (timer)
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 6>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   ns + (ns_cols_ - 1), pk, sd));
-        else
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 6>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, (unsigned long long*)nullptr,
-                                   (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
-                                   nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
-} else {
-        if (timer)
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, true, 5>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, ns, (const unsigned long long*)d_flags_,
-                                   (const int32_t*)d_senders_, nsend, stamp,
-                                   ns + (ns_cols_ - 1), pk, sd));
-        else
-          OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<4, kFusedPrefetch, false, 5>, chk, tl4,
-                                   cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
-                                   cfg_.n_inner, (unsigned long long*)nullptr,
-                                   (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,
-                                   nsend, stamp, r.ovl ? nullptr : tl_wait(), pk, sd));
-}
-    } else if (persist_minb_ == 6) { OD_LAUNCH_PS(6) } else { OD_LAUNCH_PS(5) }
-#undef OD_LAUNCH_PS
+    }
+    // overlapped steps: programmatic dependent launch, so this grid starts
+    // while the previous step's last tiles drain (tiles wait on per-tile stamps)
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(nt + pk.ctas));
+    lc.blockDim = dim3(32, kRowWarps);
+    lc.stream = s0_;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = la;
+    lc.numAttrs = r.ovl ? 1 : 0;
+    const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
+    const ChunkDev* chk = d_chunks_[par];
+    unsigned long long* nsp = timer ? ns : nullptr;
+    unsigned long long* waitp = timer ? ns + (ns_cols_ - 1) : (r.ovl ? nullptr : tl_wait());
+    if (use_ws(nt)) {
+      // warp-specialised tiles (column_step_ws): physics and Jacobi warps
+      lc.blockDim = dim3(32, 2 * kRowWarps);
+      if (timer)
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      else
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      last_kernel_ = OD_KERNEL_STEP_WS;
+    } else {
+      // interleaved tiles (column_step_grid)
+      if (timer)
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<kFusedPrefetch, true, kGridMinBlocks>,
+                                 chk, tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      else
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<kFusedPrefetch, false, kGridMinBlocks>,
+                                 chk, tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      last_kernel_ = OD_KERNEL_STEP_GRID;
+    }
     OD_CU(cudaGetLastError());
     if (prof_f) {
-      e1 = new_event();
-      OD_CU(cudaEventRecord(events_[e1], s0_));
-      prof_f_.push_back({e0, e1});
-    }
-    st_.kernel_launches += 1;
-    st_.fused_launches += 1;
-  } else if ((mode == kAsync || timer) && ntiles2_ > 0 && cfg_.overlap == 4) {
-    int e0 = -1, e1 = -1;
-    if (profiling_) {
-      e0 = new_event();
-      OD_CU(cudaEventRecord(events_[e0], s0_));
-    }
-    static const int variant3 =
-        std::getenv("OD_FUSED_MINB") ? std::atoi(std::getenv("OD_FUSED_MINB")) : 3;
-#define OD_LAUNCH_CS3(MB)                                                                  \
-  if (timer)                                                                              \
-    column_step3<kTY, kFusedPrefetch, true, MB><<<ntiles2_, blk, 0, s0_>>>(               \
-        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
-        cfg_.n_inner, ns);                                                                \
-  else                                                                                    \
-    column_step3<kTY, kFusedPrefetch, false, MB><<<ntiles2_, blk, 0, s0_>>>(              \
-        d_chunks_[par], d_tiles2_, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,  \
-        cfg_.n_inner, nullptr);
-    if (variant3 == 2) { OD_LAUNCH_CS3(2) } else { OD_LAUNCH_CS3(3) }
-#undef OD_LAUNCH_CS3
-    OD_CU(cudaGetLastError());
-    if (profiling_) {
       e1 = new_event();
       OD_CU(cudaEventRecord(events_[e1], s0_));
       prof_f_.push_back({e0, e1});
@@ -1587,6 +1437,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
       st_.kernel_launches += 2;
       st_.jacobi_launches += 1;
       st_.physics_launches += 1;
+      last_kernel_ = OD_KERNEL_SEPARATE;
       if (profiling_) {
         e2 = new_event();
         OD_CU(cudaEventRecord(events_[e2], s0_));
@@ -1601,18 +1452,15 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
     for (int32_t i = 0; i < nres; ++i) {
       const int eb = new_event(), ee = new_event();
       OD_CU(cudaEventRecord(events_[eb], s0_));
-      if (cfg_.overlap == 6) {
-        column_step4<kFusedPrefetch, false, 4><<<tile4_count_[i], dim3(kTX, 4), 0, s0_>>>(
-            d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr);
-      } else if (cfg_.overlap == 5) {
-        column_step3<4, kFusedPrefetch, false, 6><<<tile4_count_[i], dim3(kTX, 4), 0, s0_>>>(
-            d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr);
-      } else if (cfg_.overlap == 4) {
-        column_step3<kTY, kFusedPrefetch, false, 3><<<tile2_count_[i], blk, 0, s0_>>>(
-            d_chunks_[par], d_tiles2_ + tile2_begin_[i], cfg_.nz, cfg_.fields, cfield, cfg_.nx,
-            cfg_.ny, shift, cfg_.n_inner, nullptr);
+      if (cfg_.overlap != 0) {
+        // the chunk's tiles through the interleaved tile kernel (no overlap, no pack)
+        column_step_grid<kFusedPrefetch, false, kGridMinBlocks>
+            <<<tile4_count_[i], dim3(32, kRowWarps), 0, s0_>>>(
+                d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield,
+                cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, 0, 0ull,
+                nullptr, PackArgs{}, StepDeps{});
+        st_.kernel_launches += 1;
+        st_.fused_launches += 1;
       } else {
         jacobi_step<kTX, kTY, kPrefetch, false>
             <<<dim3(tile_count_[i], cfg_.fields), blk, 0, s0_>>>(
@@ -1620,12 +1468,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io) {
         physics_step<kTX, kTY, false, false><<<tile_count_[i], blk, 0, s0_>>>(
             d_chunks_[par], d_tiles_ + tile_begin_[i], cfield, cfg_.nx, cfg_.ny, shift, cfg_.nz,
             cfg_.n_inner, nullptr, nullptr);
+        st_.kernel_launches += 2;
+        st_.jacobi_launches += 1;
+        st_.physics_launches += 1;
       }
       OD_CU(cudaGetLastError());
       OD_CU(cudaEventRecord(events_[ee], s0_));
-      st_.kernel_launches += 2;
-      st_.jacobi_launches += 1;
-      st_.physics_launches += 1;
     }
   }
   if (timer && !r.ovl) {
@@ -1682,7 +1530,7 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
   for (int32_t s = 0; s < S; ++s) {
     const StepRec& r = window_[s];
     if (r.ovl) {
-      const int es = r.epoch_step;
+      const int es = r.pos;
       const unsigned long long end = stamps[2 * es + 1];
       const unsigned long long start =
           r.ovl_chained && es > 0 ? stamps[2 * (es - 1) + 1] : stamps[2 * es];
@@ -1737,9 +1585,17 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
 
   walls.assign(S, 0.0);
   samples.assign(size_t(S) * Kv, 0.0);
+  auto keep_walls = [&] {
+    for (int32_t s = 0; s < S; ++s) {
+      const size_t g = size_t(window_[s].gstep);
+      if (step_wall_.size() <= g) step_wall_.resize(g + 1, std::nan(""));
+      step_wall_[g] = walls[s];
+    }
+  };
   if (world_ == 1) {
     std::copy(local.begin(), local.begin() + size_t(S) * Kv, samples.begin());
     for (int32_t s = 0; s < S; ++s) walls[s] = local[size_t(S) * Kv + s];
+    keep_walls();
     return;
   }
   const size_t need = row * (world_ + 1);
@@ -1765,10 +1621,26 @@ void Runtime::collect(std::vector<double>& walls, std::vector<double>& samples) 
       samples[size_t(s) * Kv + v] = all[q * row + size_t(s) * Kv + v];
     }
   }
+  keep_walls();
+}
+
+void Runtime::step_walls(int64_t first, int32_t n, double* out) const {
+  if (n < 0 || first < 0) throw ValidationError("step range out of bounds");
+  for (int32_t i = 0; i < n; ++i) {
+    const size_t g = size_t(first + i);
+    out[i] = g < step_wall_.size() ? step_wall_[g] : std::nan("");
+  }
+}
+
+void Runtime::require_no_open_window(const char* who) const {
+  if (cur_step_ != 0)
+    throw RuntimeFault(std::string(who) + ": an epoch started by advance() is still open (" +
+                       std::to_string(cur_step_) + " of its steps done); finish it first");
 }
 
 void Runtime::step_api(int32_t mode, int32_t epoch_step, double* wall, od_sample* out) {
   if (mode != kSync && mode != kAsync) throw ValidationError("unknown launch mode");
+  require_no_open_window("step_time");
   begin_window();
   launch_step(mode, epoch_step, false);
   std::vector<double> walls, samples;
@@ -1825,6 +1697,7 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
 
 void Runtime::run_epoch(int32_t e, od_epoch_record* rec) {
   const int32_t S = cfg_.async_steps + cfg_.sync_steps;
+  require_no_open_window("run_epoch");
   EpochOut o;
   o.map_before = map_;
   const double tr0 = trace_on() ? now_s() : 0;
@@ -1857,8 +1730,10 @@ void Runtime::run_epoch(int32_t e, od_epoch_record* rec) {
   rec->strategy = o.strategy;
   rec->n_moves = int32_t(o.plan.size());
   if (rec->moves) {
-    if (int32_t(o.plan.size()) > rec->moves_cap) throw ValidationError("moves_cap too small");
-    for (size_t i = 0; i < o.plan.size(); ++i)
+    // snprintf convention: n_moves is the plan's size, at most moves_cap moves
+    // are written (the epoch, migration included, has been committed either way)
+    const size_t m = std::min(o.plan.size(), size_t(std::max(rec->moves_cap, 0)));
+    for (size_t i = 0; i < m; ++i)
       rec->moves[i] = od_move{o.plan[i].vp, o.plan[i].from, o.plan[i].to};
   }
   rec->migration_seconds = o.mig_s;
@@ -1920,12 +1795,7 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
                         h_loads_rows_ * row_words * sizeof(unsigned long long), cudaHostAllocMapped));
     OD_CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_loads_map_), h_loads_, 0));
   }
-  if (host_c && n_fields > 0) {
-    // the caller's load multiplier field replaces the base field
-    base_.c.assign(host_c, host_c + cells);
-    OD_CU(cudaMemcpy(d_cbase_, host_c, cells * sizeof(double), cudaMemcpyHostToDevice));
-    set_shift(shift_);
-  }
+  if (n_fields < 0 || (n_fields > 0 && !host_c)) throw ValidationError("bad host field count");
   const int32_t S = cfg_.async_steps + cfg_.sync_steps;
   // steps are launched back to back; the per-step loads land in pinned rows
   // and are read once the stream has drained (epoch ends drain it anyway)
@@ -1935,7 +1805,18 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
     advance_advection(cur_epoch_, cur_step_);
     h_loads_dst_ = h_loads_ + size_t(i) * row_words;
     d_loads_dst_ = d_loads_map_ + size_t(i) * row_words;
-    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true);
+    const double* hf = nullptr;
+    if (host_c && n_fields > 0) {
+      // the caller's field for this step drives the kernel; the host-side copy
+      // of it orders the tiles (heaviest first) when it differs from the last
+      hf = host_c + size_t(std::min(i, n_fields - 1)) * cells;
+      if (std::memcmp(field_.c.data(), hf, cells * sizeof(double)) != 0) {
+        field_.c.assign(hf, hf + cells);
+        ++field_gen_;
+        order_dirty_ = true;
+      }
+    }
+    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true, hf);
     if (host_loads) step_vps[i] = window_.back().slot_vps;
     ++global_step_;
     if (++cur_step_ == S) {
@@ -1945,6 +1826,8 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
       cur_step_ = 0;
     }
   }
+  // later steps see the runtime's own advected field again
+  if (host_c && n_fields > 0) set_shift(shift_);
   OD_CU(cudaStreamSynchronize(s0_));
   for (int32_t i = 0; host_loads && i < n; ++i) {
     double* row = host_loads + size_t(i) * K();
@@ -2088,6 +1971,7 @@ void Runtime::stats(od_rt_stats* s) {
       }
   }
   st_.physics_trips = trips;
+  st_.last_kernel = last_kernel_;
   *s = st_;
 }
 
@@ -2237,6 +2121,13 @@ int od_rt_set_profiling(od_runtime* rt, int32_t on) {
 
 int od_rt_synchronize(od_runtime* rt) {
   return guarded([&] { R(rt).sync(); });
+}
+
+int od_rt_step_walls(od_runtime* rt, int64_t first, int32_t n, double* out) {
+  return guarded([&] {
+    if (n > 0 && !out) throw ValidationError("null pointer: out");
+    R(rt).step_walls(first, n, out);
+  });
 }
 
 }  // extern "C"

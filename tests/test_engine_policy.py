@@ -86,6 +86,8 @@ def test_runtime_config_validation(mutate, match):
         od.Engine(cfg)
 
 
-def test_runtime_needs_one_rank_per_node():
+def test_runtime_needs_a_processor_per_gpu():
+    # processors are dealt to GPUs in blocks: more GPUs than processors is an
+    # input error (raised before any device or NCCL work)
     with pytest.raises(od.ValidationError, match="world"):
-        od.Engine(configs.cfg1())  # 4 nodes, 1 rank
+        od.Engine(configs.cfg2(), rank=0, world=2, nccl_id=bytes(128))  # 1 processor

@@ -25,7 +25,7 @@ def small(nx=37, ny=23, nz=6, F=3, kind=TWO_D, kx=1, ky=1, nodes=1, ppn=1, steps
 
 @pytest.mark.parametrize("kx,ky,overlap", [(1, 1, 0), (4, 3, 0), (2, 5, 0), (1, 1, 4), (4, 3, 4),
                                            (2, 5, 4), (1, 1, 5), (4, 3, 5), (2, 5, 5),
-                                           (1, 1, 6), (4, 3, 6), (2, 5, 6)])
+                                           (1, 1, 7), (4, 3, 7), (2, 5, 7)])
 def test_fields_bitwise_2d(kx, ky, overlap):
     cfg = small(kx=kx, ky=ky, overlap=overlap)
     U, A, _ = device_fields(cfg, 3)
@@ -34,11 +34,25 @@ def test_fields_bitwise_2d(kx, ky, overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 4, 5, 6])
+@pytest.mark.parametrize("overlap", [0, 4, 5, 7])
 def test_fields_bitwise_1d_strips(overlap):
     cfg = small(nx=45, ny=30, kind=ONE_D, kx=1, ky=7, overlap=overlap)
     U, A, _ = device_fields(cfg, 4)
     Uo, Ao = oracle_fields(cfg, 4)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+
+
+@pytest.mark.parametrize("mode", [4, 7])
+@pytest.mark.parametrize("nx,kx,ny,ky", [(64, 8, 48, 2), (96, 6, 40, 2), (96, 3, 44, 2),
+                                         (120, 3, 50, 2), (200, 2, 18, 2), (66, 6, 30, 5),
+                                         (256, 4, 12, 1)])
+def test_fields_tile_widths(nx, kx, ny, ky, mode):
+    # chunk widths 8, 16, 32, 40, 100, 11, 64 select 8 x 32 / 16 x 16 / 32 x 8 /
+    # 64 x 4 tiles, full and partial in both directions
+    cfg = small(nx=nx, ny=ny, nz=5, F=2, kx=kx, ky=ky, n_inner=9, overlap=mode, heavy=3.0)
+    U, A, _ = device_fields(cfg, 3)
+    Uo, Ao = oracle_fields(cfg, 3)
     assert_bitwise(U, Uo, "U")
     assert_bitwise(A, Ao, "A")
 
@@ -53,7 +67,7 @@ def test_fields_multi_tile_chunks_and_advection():
 
 
 @pytest.mark.parametrize("overlap,n_inner", [(0, 5), (4, 5), (4, 0), (4, 40), (5, 5), (5, 0),
-                                             (5, 40), (6, 5), (6, 0), (6, 40)])
+                                             (5, 40), (7, 5), (7, 0), (7, 40)])
 def test_fields_edge_shapes(overlap, n_inner):
     # nz = 1 (no vertical neighbours, physics trips 0 or 1), single field
     cfg = small(nx=33, ny=9, nz=1, F=1, kx=3, ky=2, heavy=3.0, overlap=overlap, n_inner=n_inner)
@@ -67,7 +81,7 @@ def test_fields_invariant_under_balancing_and_procs():
     # 3 processors sharing the GPU, balancing every epoch: mapping changes,
     # values must not
     cfg = small(nx=64, ny=40, kx=4, ky=4, ppn=3, threshold=1.0, steps_window=(1, 1),
-                adv=(20, 2, 2), overlap=6)
+                adv=(20, 2, 2), overlap=4)
     U, A, recs = device_fields(cfg, 6, use_epochs=True)
     assert any(r.plan.moves for r in recs)
     Uo, Ao = oracle_fields(cfg, 6)
@@ -75,7 +89,7 @@ def test_fields_invariant_under_balancing_and_procs():
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("overlap", [0, 4, 5, 6])
+@pytest.mark.parametrize("overlap", [0, 4, 5, 7])
 def test_events_measurement_mode(overlap):
     cfg = small(nx=64, ny=32, kx=4, ky=2, measure=od.MeasureMode.Events, overlap=overlap)
     with od.Engine(cfg) as eng:
@@ -90,7 +104,7 @@ def test_events_measurement_mode(overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("mode", [4, 5, 6])
+@pytest.mark.parametrize("mode", [4, 5, 7])
 @pytest.mark.parametrize("n_inner,F,nz", [(0, 2, 5), (1, 3, 7), (13, 1, 4), (200, 2, 3)])
 def test_fused_quota_edge_cases(n_inner, F, nz, mode):
     # quota rounding: recurrences longer/shorter than the Jacobi level count;
@@ -109,7 +123,7 @@ def test_device_matches_committed_golden_fields():
     import os
     gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fields.json")))
     for g in gold:
-        for mode in (0, 4, 5, 6):
+        for mode in (0, 4, 5, 7):
             cfg = small(nx=g["nx"], ny=g["ny"], nz=g["nz"], F=g["fields"], kx=g["kx"], ky=g["ky"],
                         steps_window=tuple(g["window"]), n_inner=g["n_inner"], seed=g["seed"],
                         adv=tuple(g["advection"]),
@@ -135,6 +149,69 @@ def test_host_io_path_matches_device_path():
     assert (loads > 0).all()
 
 
+def test_host_io_caller_fields_after_advection():
+    """od_rt_advance_host with caller-supplied per-step load fields, after the
+    runtime's own advection has moved the field: each step computes with the
+    caller's field; afterwards od_rt_advance continues the runtime's schedule."""
+    from oracle import fields as of
+    from tests.gpu_util import oracle_fields as ofields
+    cfg = small(nx=96, ny=40, kx=3, ky=2, adv=(9, 1, 3), n_inner=7, steps_window=(2, 1))
+    rng = np.random.default_rng(5)
+    fields = np.ascontiguousarray(1.0 + rng.integers(0, 3, size=(2, 40, 96)).astype(np.float64))
+    with od.Engine(cfg) as eng:
+        eng.advance(4)                       # epoch 1 (advecting) and one step of epoch 2
+        loads = np.zeros((3, cfg.vp_count()))
+        eng.advance_host(3, fields, loads)   # steps 4..6 use fields[0], [1], [1]
+        eng.advance(2)                       # steps 7, 8: the runtime's field again
+        U, A, _ = eng.gather_fields()
+    Uo, Ao = ofields(cfg, 4)
+    for f in (fields[0], fields[1], fields[1]):
+        of.step(Uo, Ao, f, 0, cfg.n_inner)
+    # steps 7, 8 (epoch 3): the runtime's field, fully advected (9 rows)
+    import oracle.ref as oref
+    base = oref.base_field(cfg)
+    for _ in range(2):
+        of.step(Uo, Ao, base, 9, cfg.n_inner)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+    assert (loads > 0).all()
+
+
+def test_host_io_rejects_bad_buffers():
+    cfg = small(nx=96, ny=40, kx=3, ky=2, n_inner=3)
+    with od.Engine(cfg) as eng:
+        with pytest.raises(od.ValidationError):
+            eng.advance_host(2, np.ones((40, 96), dtype=np.float32))
+        with pytest.raises(od.ValidationError):
+            eng.advance_host(2, np.ones((41, 96)))
+        with pytest.raises(od.ValidationError):
+            eng.advance_host(2, None, np.zeros((1, cfg.vp_count())))
+        with pytest.raises(od.ValidationError):
+            eng.advance_host(2, np.ones((96, 40)).T)  # not C-contiguous
+
+
+def test_step_time_labels_and_open_window():
+    """Engine.step_time accepts any epoch_step label (reference semantics): the
+    device slots are indexed by position, so large or negative labels are
+    safe; a step_time inside an epoch opened by advance() is refused."""
+    cfg = small(nx=64, ny=32, kx=4, ky=2, steps_window=(2, 2))
+    with od.Engine(cfg) as eng:
+        for lab in (12, -3, 1000):
+            wall, samples = eng.step_time(od.LaunchMode.Sync, lab)
+            assert wall > 0 and all(s.step == lab for s in samples)
+        eng.advance(1)
+        with pytest.raises(od.RuntimeFault):
+            eng.step_time(od.LaunchMode.Sync, 0)
+        with pytest.raises(od.RuntimeFault):
+            eng.run_epoch(1)
+        eng.advance(3)  # closes the epoch
+        eng.run_epoch(2)
+        U, A, _ = eng.gather_fields()
+    Uo, Ao = oracle_fields(cfg, 3 + 4 + 4)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+
+
 def test_measured_loads_track_work_and_balancing_helps():
     # per-chunk loads from the in-kernel timers rank chunks like their exact
     # work; balancing on them lowers the next epoch's measured imbalance
@@ -157,17 +234,15 @@ def test_measured_loads_track_work_and_balancing_helps():
         assert r2.imbalance_before < 1.05
 
 
-@pytest.mark.parametrize("env", [{"OD_OVERLAP": "0"}, {"OD_OVERLAP": "1"},
-                                 {"OD_GRID": "0", "OD_OVERLAP": "0"},
-                                 {"OD_FIRSTWAVE": "0"}, {"OD_OVERLAP": "1", "OD_ORDER": "spt"},
-                                 {"OD_WS": "0"}, {"OD_WS": "1"}, {"OD_WS": "1", "OD_OVERLAP": "0"}])
-def test_step_kernel_variants_bitwise(env, monkeypatch):
-    """The mode-5 launch variants (cross-step overlap on/off, one CTA per tile
-    or persistent, queue orders) compute identical fields, with multi-tile
-    chunks, advection and balancing moves across several epochs."""
+@pytest.mark.parametrize("mode", [4, 5, 7])
+@pytest.mark.parametrize("env", [{"OD_OVERLAP": "0"}, {"OD_OVERLAP": "1"}])
+def test_step_kernel_variants_bitwise(env, mode, monkeypatch):
+    """The fused launch variants (interleaved / automatic / warp-specialised
+    tiles, cross-step overlap on and off) compute identical fields, with
+    multi-tile chunks, advection and balancing moves across several epochs."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
-    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, adv=(35, 1, 3), n_inner=7, overlap=5,
+    cfg = small(nx=150, ny=70, nz=9, F=2, kx=3, ky=3, adv=(35, 1, 3), n_inner=7, overlap=mode,
                 nodes=1, ppn=3, threshold=1.0)
     U, A, _ = device_fields(cfg, 12)
     Uo, Ao = oracle_fields(cfg, 12)
@@ -188,7 +263,7 @@ def test_refine_adjacent_policy_runs_bitwise():
     assert any(r.plan.moves for r in recs)
 
 
-@pytest.mark.parametrize("overlap", [5, 6])
+@pytest.mark.parametrize("overlap", [4, 5, 7])
 @pytest.mark.parametrize("nz,F", [(2, 1), (3, 1), (2, 2), (5, 1)])
 def test_fields_few_levels(overlap, nz, F):
     # fewer plane levels (F * nz) than the cp.async ring's prefetch depth

@@ -22,7 +22,8 @@ def ngpus():
 
 @pytest.mark.skipif(ngpus() < 2, reason="needs 2 GPUs")
 @pytest.mark.parametrize("mode,halo,extra", [(5, "p2p", {}), (5, "nccl", {}), (0, "p2p", {}),
-                                             (6, "p2p", {}), (5, "p2p", {"OD_OVERLAP": "0"}),
+                                             (4, "p2p", {}), (7, "p2p", {}),
+                                             (5, "p2p", {"OD_OVERLAP": "0"}),
                                              (5, "p2p", {"OD_PACK_CTAS": "0"})])
 def test_two_gpus_fields_and_plans(mode, halo, extra):
     s = socket.socket()

@@ -6,7 +6,17 @@ from paper_1310_4218_b200 import configs
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg4"
 kw = dict(a.split("=") for a in sys.argv[2:])
 kw = {k: int(v) for k, v in kw.items()}
-cfg = configs.CONFIGS[name](**kw)
+SLICES = {
+    # 256x256 slices of the cfg4 / cfg3 geometry on one GPU (4 processors)
+    "cfg4s": lambda **k: configs.cfg4(nodes=1, **k).replace(
+        cluster=od.ClusterSpec(1, 4), domain=od.Domain(256, 256, 64, 50),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 4, 4)),
+    "cfg3s": lambda **k: configs.cfg3(nodes=1, **k).replace(
+        cluster=od.ClusterSpec(1, 4), domain=od.Domain(256, 256, 64, 50),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 8, 8),
+        advection=od.AdvectionSchedule(128, 2, 10)),
+}
+cfg = (SLICES.get(name) or configs.CONFIGS[name])(**kw)
 with od.Engine(cfg) as eng:
     eng.set_profiling(True)
     for e in range(1, 4):
