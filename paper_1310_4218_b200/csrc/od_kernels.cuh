@@ -124,6 +124,29 @@ __device__ __noinline__ double sm_share_update(int delta, int tag) {
   return v;
 }
 
+// A fused tile's share-clock account in shared memory: the tile is charged
+// only while it can work.  A tile whose physics is exhausted and which blocks
+// on a neighbour (peer strip, or a same-GPU tile still finishing the previous
+// step under cross-step overlap) pauses its account and leaves the SM's
+// resident count, so idling for a neighbour is charged to nobody and the
+// other tiles on the SM get the SM.
+struct ShareAcct {
+  double t0, acc;
+};
+__device__ __forceinline__ void share_begin(ShareAcct& a, int tag) {
+  a.acc = 0.0;
+  a.t0 = sm_share_update(1, tag);
+}
+__device__ __forceinline__ void share_pause(ShareAcct& a, int tag) {
+  a.acc += sm_share_update(-1, tag) - a.t0;
+}
+__device__ __forceinline__ void share_resume(ShareAcct& a, int tag) {
+  a.t0 = sm_share_update(1, tag);
+}
+__device__ __forceinline__ double share_end(ShareAcct& a, int tag) {
+  return a.acc + (sm_share_update(-1, tag) - a.t0);
+}
+
 // Executed FP64 pipe instructions, the work measure that apportions a GPU's
 // measured busy time among its chunks (TIMER): one physics trip is 2*n_inner+3
 // (two FMAs per unit, the trip's y and eb), one Jacobi cell 8 (6 add, mul, fma).
@@ -652,8 +675,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
                                           const HaloWait hw) {
   constexpr int R = kRingSlots;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  double t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
+  __shared__ ShareAcct s_acct;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) share_begin(s_acct, share_tag(tile));
 
   const ChunkDev& c = chunks[tile.slot];
   const TileGeom g = tile_geom(tile, threadIdx.y, threadIdx.x);
@@ -819,10 +842,12 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       if (lead) {
         if (done >= need) {
           // physics exhausted before the strips came: block (traps on a dead
-          // peer); the longest such idle is kept out of the load measurement
+          // peer) with the tile's account paused (idling is charged to nobody)
+          if (TIMED) share_pause(s_acct, share_tag(tile));
           const uint64_t w0 = globaltimer_ns();
           wait_ready(hw, 20ull * 1000 * 1000 * 1000);
           if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+          if (TIMED) share_resume(s_acct, share_tag(tile));
           lead_ready = true;
         } else {
           lead_ready = stamps_ready(hw);
@@ -881,7 +906,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     charge_ops(chunk_ns, tile.slot, ops);
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(share_end(s_acct, share_tag(tile))));
   }
 }
 
@@ -1091,8 +1116,12 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
                                              const HaloWait hw) {
   constexpr int R = kRingSlots;
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
-  double t_start = 0;
-  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) t_start = sm_share_update(1, share_tag(tile));
+  __shared__ ShareAcct s_acct;
+  __shared__ int s_phys_left;  // physics warps still running (TIMED: pause when idle)
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    s_phys_left = kRowWarps;
+    if (TIMED) share_begin(s_acct, share_tag(tile));
+  }
 
   const ChunkDev& c = chunks[tile.slot];
   // warp roles: threadIdx.y < 4 physics, >= 4 Jacobi, both over row warp y % 4
@@ -1211,12 +1240,25 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       if (ncell >= 1) physics_advance(s0, 0x7fffffff);
       if (ncell == 2) physics_advance(s1, 0x7fffffff);
     }
+    __syncwarp();
+    if (threadIdx.x == 0) atomicSub(&s_phys_left, 1);
   } else {
     // Jacobi warps: wait for remote strips / neighbour tiles, then stream the ring
     if (hw.n > 0 || hw.ndeps > 0) {
       if (bar_lead) {
+        // wait while the physics warps work; once they are done and the
+        // neighbours still are not, the tile idles: pause its account
         const uint64_t w0 = globaltimer_ns();
-        wait_ready(hw, 20ull * 1000 * 1000 * 1000);
+        bool paused = false;
+        while (!stamps_ready(hw)) {
+          if (TIMED && !paused && *(volatile int*)&s_phys_left == 0) {
+            share_pause(s_acct, share_tag(tile));
+            paused = true;
+          }
+          if (globaltimer_ns() - w0 > 20ull * 1000 * 1000 * 1000) __trap();
+          __nanosleep(64);
+        }
+        if (TIMED && paused) share_resume(s_acct, share_tag(tile));
         if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
       }
       asm volatile("bar.sync 1, %0;" ::"r"(32 * kRowWarps) : "memory");
@@ -1259,7 +1301,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
     charge_ops(chunk_ns, tile.slot, ops);
     __syncthreads();
     if (threadIdx.x == 0 && threadIdx.y == 0)
-      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(sm_share_update(-1, share_tag(tile)) - t_start));
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(share_end(s_acct, share_tag(tile))));
   }
 }
 
