@@ -266,6 +266,10 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------ GPU leg --
 
+DFMA_LATENCY_CYCLES = 8.32  # dependent DFMA, profiles/r1_dfma_latency.txt
+SM_MAX_MHZ = 1965
+
+
 def physics_flops_per_trip(n_inner):
     # f: 1 mul + 2 fma (setup) + n_inner x 2 fma  (kernels: column_f)
     return 5 + 4 * n_inner
@@ -405,10 +409,27 @@ def main():
     kflops = phys_flops + jac_flops
     kms = wall_ms if wall_ms else step_ms
     k_tf = kflops / (kms * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "kernel": kname, "achieved": k_tf, "peak": fp64_peak,
-                "unit": "TFLOP/s", "frac": k_tf / fp64_peak, "traffic": traffic,
-                "peak_source": "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)"
+    # the step is bounded by the FP64 pipe (all GPUs' flops at the measured
+    # peak) or, on grids too small to fill a B200, by the longest column's
+    # dependent chain: T_max trips x (2 n_inner + 3) DFMAs at the measured
+    # dependent-DFMA latency (profiles/r1_dfma_latency.txt: 8.32 cycles) at the
+    # maximum SM clock
+    t_max = float(np.maximum(np.floor(d.nz * lf) - 1, 0).max())
+    chain_s = t_max * (2 * cfg.n_inner + 3) * DFMA_LATENCY_CYCLES / (SM_MAX_MHZ * 1e6)
+    t_fp64 = kflops / (fp64_peak * 1e12)
+    latency_bound = chain_s > t_fp64
+    peak = kflops / chain_s / 1e12 if latency_bound else fp64_peak
+    roofline = {"bound": "latency" if latency_bound else "fp64", "kernel": kname,
+                "achieved": k_tf, "peak": peak, "unit": "TFLOP/s", "frac": k_tf / peak,
+                "traffic": traffic,
+                "peak_source": (f"dependent-chain latency: {t_max:.0f} trips x "
+                                f"{2 * cfg.n_inner + 3} DFMA x {DFMA_LATENCY_CYCLES} cycles "
+                                f"at {SM_MAX_MHZ} MHz = {chain_s * 1e3:.3f} ms per step "
+                                "(the grid cannot fill the FP64 pipe)")
+                               if latency_bound else
+                               "measured FP64 FMA microbenchmark (profiles/peaks_fp64.json)"
                                + (f" x {world} GPUs" if world > 1 else ""),
+                "fp64_frac": k_tf / fp64_peak,
                 "avg_ms": kms, "share_of_step": kms / step_ms,
                 "avg_ms_def": "mean device wall of exactly the timed steps (step-kernel "
                               "interval on the device clock; epoch-boundary host work "
@@ -496,6 +517,10 @@ def main():
         if world > 1:
             dist.destroy_process_group()
         return
+    state_b = float(cols) * d.nz * (2 * d.fields + 1) * 8
+    l2_note = (f"state {state_b / 1e9:.1f} GB >> 126 MB L2 (no flush needed)" if state_b > 1e9
+               else f"state {state_b / 1e6:.0f} MB: fits the 126 MB L2 partly or fully; no "
+                    "flush (the step is bound by the dependent-chain latency, see roofline)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -508,7 +533,7 @@ def main():
                              f"@{cfg.policy.trigger_threshold}",
                    "n_inner": cfg.n_inner, "measure": cfg.measure.name, "lb": "on",
                    "kernel_mode": cfg.overlap,
-                   "l2": "state 54 GB >> 126 MB L2 (no flush needed)"},
+                   "l2": l2_note},
         "roofline": roofline,
         "roofline_hbm": roofline_hbm,
         "clocks": clk.summary(),

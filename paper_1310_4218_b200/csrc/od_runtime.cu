@@ -221,6 +221,15 @@ class Runtime {
   int tiles4s_cur_ = 0;
   bool order_dirty_ = true;
   int wave_ = 0;       // tiles one launch keeps resident (SMs x CTAs per SM)
+  // equal-work tiles are dealt round-robin over the chunks in bands of band_
+  // consecutive tiles of a chunk: y-neighbours start ~one CTA retirement apart,
+  // so the halo rows they share are read within microseconds and hit L2.
+  // cfg4 at N=1 (profiles/r2_tile_band_sweep.json): DRAM traffic per step
+  // 68.3 GB (band 1) -> 62.6 (2) -> 59.7 (4) -> 59.0 GB (16) against 54.8 GB
+  // algorithmic, step time unchanged (FP64-bound); the per-chunk load spread
+  // among identical chunks grows 0.6 -> 1.0 -> 1.6 -> 12 % (CV): band 4.
+  // OD_TILE_BAND overrides (diagnostic)
+  int band_ = 4;
   int sms_ = 1;
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
   void refresh_tile_order();
@@ -390,6 +399,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // P2P halos: the step kernel's first CTAs pack the strips (OD_PACK_CTAS=0:
     // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
+    if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
     OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
     int per_sm = 0;
     OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -597,7 +607,7 @@ void Runtime::refresh_tile_order() {
       }
     }
     const double w = tile_work_[vp][local];
-    key[t] = {-w, int32_t(t) - tile4_begin_[td.slot], int32_t(t)};
+    key[t] = {-w, (int32_t(t) - tile4_begin_[td.slot]) / band_, int32_t(t)};
   }
   std::sort(key.begin(), key.end());
   if (p2p_ && n_senders_ > 0) {
