@@ -168,6 +168,26 @@ int od_greedy_lb(const double* loads, int32_t n_loads, const int32_t* map,
 int od_refine_swap_lb(const double* loads, int32_t n_loads, const int32_t* map,
                       int32_t vp_count, int32_t proc_count, double tolerance,
                       od_move* out, int32_t cap, int32_t* n_out);
+/* B200 extension, off-parity (no reference counterpart): capacity-aware
+   greedy_lb / refine_swap_lb (balancer.hpp:36-152 ignore memory).
+   Processors are grouped into bins (the GPUs holding them, bin_of_proc[P]);
+   no plan takes a bin's resident chunk bytes (vp_bytes[K]) past
+   bin_capacity[n_bins] when the bins fit before it (moves out of an
+   over-full bin stay allowed).  Same order, ties and acceptance tests as the
+   plain planners, which they equal exactly when no capacity binds; greedy
+   places each chunk on the least-loaded processor with room, and if its pass
+   still overfills a bin, chunks that moved in return home, lightest first.
+   cap >= K (greedy) / 2*K*P (refine). */
+int od_greedy_lb_capacity(const double* loads, int32_t n_loads, const int32_t* map,
+                          int32_t vp_count, int32_t proc_count, const int64_t* vp_bytes,
+                          const int32_t* bin_of_proc, int32_t n_bins,
+                          const int64_t* bin_capacity, od_move* out, int32_t cap,
+                          int32_t* n_out);
+int od_refine_swap_lb_capacity(const double* loads, int32_t n_loads, const int32_t* map,
+                               int32_t vp_count, int32_t proc_count, double tolerance,
+                               const int64_t* vp_bytes, const int32_t* bin_of_proc,
+                               int32_t n_bins, const int64_t* bin_capacity, od_move* out,
+                               int32_t cap, int32_t* n_out);
 /* B200 extension, off-parity (no reference counterpart; Strategy 2): refine_swap_lb's
    rounds, thresholds and acceptance tests, choosing among admissible moves/swaps the
    one adding the fewest chunk faces between processors (balance score breaks ties);
@@ -248,7 +268,11 @@ typedef struct od_config {
                            GPU up, column_step_ws below; 7 warp-specialised tiles
                            (column_step_ws).  Fused modes overlap consecutive step
                            kernels (programmatic dependent launch) */
-  int32_t reserved_[5];
+  int32_t capacity_mib;  /* per-GPU cap on resident chunk data (MiB, B200 extension):
+                            > 0 makes the epoch's Greedy / RefineSwap calls
+                            capacity-aware (od_*_lb_capacity, one bin per GPU);
+                            0 = unlimited, the reference's behaviour */
+  int32_t reserved_[4];
 } od_config;
 
 /* EpochRecord (engine.hpp:85-97); arrays are caller-allocated */

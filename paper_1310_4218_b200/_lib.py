@@ -56,7 +56,7 @@ class od_config(C.Structure):
         ("trigger_threshold", C.c_double), ("refine_tolerance", C.c_double),
         ("seed", C.c_uint64),
         ("n_inner", C.c_int32), ("measure", C.c_int32), ("overlap", C.c_int32),
-        ("reserved_", C.c_int32 * 5),
+        ("capacity_mib", C.c_int32), ("reserved_", C.c_int32 * 4),
     ]
 
 
@@ -134,6 +134,10 @@ PROTOTYPES = {
     "od_should_balance": [_P(_D), _I32, _D, _P(_I32)],
     "od_greedy_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _P(od_move), _I32, _P(_I32)],
     "od_refine_swap_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _P(od_move), _I32, _P(_I32)],
+    "od_greedy_lb_capacity": [_P(_D), _I32, _P(_I32), _I32, _I32, _P(C.c_int64), _P(_I32), _I32,
+                              _P(C.c_int64), _P(od_move), _I32, _P(_I32)],
+    "od_refine_swap_lb_capacity": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _P(C.c_int64),
+                                   _P(_I32), _I32, _P(C.c_int64), _P(od_move), _I32, _P(_I32)],
     "od_refine_adjacent_lb": [_P(_D), _I32, _P(_I32), _I32, _I32, _D, _I32, _I32, _I32,
                               _P(od_move), _I32, _P(_I32)],
     "od_kernel_time_sync": [_P(od_kernel_work), _P(od_gpu_model), _P(_D)],

@@ -35,7 +35,8 @@ __all__ = [
     "decompose_1d", "decompose_2d", "init_load_field", "advect_load_field", "physics_work",
     "jacobi_work", "halo_bytes", "subdomain_bytes", "Move", "MigrationPlan", "Mapping",
     "initial_block_mapping", "apply_plan", "proc_loads", "imbalance_ratio", "BalancePolicy",
-    "should_balance", "greedy_lb", "refine_swap_lb", "refine_adjacent_lb", "StepSample",
+    "should_balance", "greedy_lb", "refine_swap_lb", "refine_adjacent_lb", "greedy_lb_capacity",
+    "refine_swap_lb_capacity", "StepSample",
     "MeasurementWindow", "LoadDB", "record_step", "epoch_loads", "ClusterSpec", "Decomposition",
     "AdvectionSchedule", "ExperimentConfig", "EpochRecord", "Timeline", "Engine",
     "run_experiment", "nccl_unique_id", "epoch_decision", "EpochDecision", "chunk_neighbor",
@@ -408,6 +409,48 @@ def refine_adjacent_lb(loads: Sequence[float], mapping: Mapping, decomposition: 
     return _plan_from(out, n.value, Strategy.RefineAdjacent)
 
 
+def _capacity_args(mapping: Mapping, vp_bytes, bin_of_proc, bin_capacity):
+    vb = np.ascontiguousarray(vp_bytes, dtype=np.int64)
+    bp = np.ascontiguousarray(bin_of_proc, dtype=np.int32)
+    bc = np.ascontiguousarray(bin_capacity, dtype=np.int64)
+    if vb.size != mapping.vp_count() or bp.size != mapping.proc_count():
+        raise ValidationError("capacity: vp_bytes / bin_of_proc length mismatch")
+    return (vb, bp, bc), (vb.ctypes.data_as(C.POINTER(C.c_int64)),
+                          bp.ctypes.data_as(C.POINTER(C.c_int32)), int(bc.size),
+                          bc.ctypes.data_as(C.POINTER(C.c_int64)))
+
+
+def greedy_lb_capacity(loads: Sequence[float], mapping: Mapping, vp_bytes: Sequence[int],
+                       bin_of_proc: Sequence[int], bin_capacity: Sequence[int]) -> MigrationPlan:
+    """B200 extension (off-parity): greedy_lb that never moves a chunk into a bin
+    (GPU) whose resident chunk bytes would exceed its capacity; equals greedy_lb
+    when no capacity binds."""
+    l = np.ascontiguousarray(loads, dtype=np.float64)
+    keep, args = _capacity_args(mapping, vp_bytes, bin_of_proc, bin_capacity)
+    cap = max(mapping.vp_count(), 1)
+    out = (od_move * cap)()
+    n = C.c_int32()
+    check(lib.od_greedy_lb_capacity(_dptr(l), int(l.size), _iptr(mapping._a), mapping.vp_count(),
+                                    mapping.proc_count(), *args, out, cap, C.byref(n)))
+    return _plan_from(out, n.value, Strategy.Greedy)
+
+
+def refine_swap_lb_capacity(loads: Sequence[float], mapping: Mapping, vp_bytes: Sequence[int],
+                            bin_of_proc: Sequence[int], bin_capacity: Sequence[int],
+                            tolerance: float = 0.02) -> MigrationPlan:
+    """B200 extension (off-parity): refine_swap_lb under per-bin (GPU) capacity;
+    equals refine_swap_lb when no capacity binds."""
+    l = np.ascontiguousarray(loads, dtype=np.float64)
+    keep, args = _capacity_args(mapping, vp_bytes, bin_of_proc, bin_capacity)
+    cap = max(2 * mapping.vp_count() * max(mapping.proc_count(), 1), 1)
+    out = (od_move * cap)()
+    n = C.c_int32()
+    check(lib.od_refine_swap_lb_capacity(_dptr(l), int(l.size), _iptr(mapping._a),
+                                         mapping.vp_count(), mapping.proc_count(),
+                                         float(tolerance), *args, out, cap, C.byref(n)))
+    return _plan_from(out, n.value, Strategy.RefineSwap)
+
+
 @dataclass
 class EpochDecision:
     strategy: Optional[Strategy]
@@ -758,6 +801,9 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     # columns (tw = 64/32/16/8 by chunk width), heaviest first, consecutive
     # step kernels overlapped.
     overlap: int = 5
+    # B200 extension: per-GPU cap on resident chunk data in MiB (0 = unlimited,
+    # the reference); > 0 makes Greedy/RefineSwap calls capacity-aware
+    capacity_mib: int = 0
 
     def vp_count(self) -> int:
         return self.decomposition.vp_count()
@@ -785,6 +831,7 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
         c.trigger_threshold, c.refine_tolerance = float(p.trigger_threshold), float(p.refine_tolerance)
         c.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
         c.n_inner, c.measure, c.overlap = int(self.n_inner), int(self.measure), int(self.overlap)
+        c.capacity_mib = int(self.capacity_mib)
         return c
 
     def replace(self, **kw) -> "ExperimentConfig":

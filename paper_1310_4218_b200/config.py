@@ -130,10 +130,11 @@ def config_from_json(doc: Dict[str, Any]) -> ExperimentConfig:  # config.hpp:101
         if k in doc:
             _reject_unknown(doc[k], k, allowed)
     seed = _get(doc, "seed", int, c.seed)
-    n_inner, measure, mode = c.n_inner, c.measure, c.overlap
+    n_inner, measure, mode, capacity = c.n_inner, c.measure, c.overlap, c.capacity_mib
     if "b200" in doc:
         o = doc["b200"]
-        _reject_unknown(o, "b200", {"n_inner", "measure", "kernel_mode"})
+        _reject_unknown(o, "b200", {"n_inner", "measure", "kernel_mode", "capacity_mib"})
+        capacity = _get(o, "capacity_mib", int, capacity)
         n_inner = _get(o, "n_inner", int, n_inner)
         if "measure" in o:
             try:
@@ -144,7 +145,8 @@ def config_from_json(doc: Dict[str, Any]) -> ExperimentConfig:  # config.hpp:101
         mode = _get(o, "kernel_mode", int, mode)
     out = ExperimentConfig(cluster=cl, domain=dm, decomposition=de, window=wi, epochs=epochs,
                            pattern=pattern, heavy_value=heavy, light_value=light, advection=adv,
-                           policy=pol, seed=seed, n_inner=n_inner, measure=measure, overlap=mode)
+                           policy=pol, seed=seed, n_inner=n_inner, measure=measure, overlap=mode,
+                           capacity_mib=capacity)
     _validate(out)
     return out
 
@@ -193,7 +195,7 @@ def config_to_json(c: ExperimentConfig) -> Dict[str, Any]:  # config.hpp:55-99
                    "refine_tolerance": c.policy.refine_tolerance},
         "seed": c.seed,
         "b200": {"n_inner": c.n_inner, "measure": c.measure.name.lower() if c.measure != 2
-                 else "timer_raw", "kernel_mode": c.overlap},
+                 else "timer_raw", "kernel_mode": c.overlap, "capacity_mib": c.capacity_mib},
     }
 
 

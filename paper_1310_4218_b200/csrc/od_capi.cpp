@@ -259,6 +259,49 @@ int od_refine_adjacent_lb(const double* loads, int32_t n_loads, const int32_t* m
   });
 }
 
+static Capacity capacity_of(const int64_t* vp_bytes, int32_t vp_count,
+                            const int32_t* bin_of_proc, int32_t proc_count, int32_t n_bins,
+                            const int64_t* bin_capacity) {
+  if (n_bins < 1) throw ValidationError("capacity: need at least one bin");
+  need(vp_bytes, "vp_bytes");
+  need(bin_of_proc, "bin_of_proc");
+  need(bin_capacity, "bin_capacity");
+  Capacity c;
+  c.vp_bytes.assign(vp_bytes, vp_bytes + vp_count);
+  c.bin_of_proc.assign(bin_of_proc, bin_of_proc + proc_count);
+  c.bin_cap.assign(bin_capacity, bin_capacity + n_bins);
+  c.validate(vp_count, proc_count);
+  return c;
+}
+
+int od_greedy_lb_capacity(const double* loads, int32_t n_loads, const int32_t* map,
+                          int32_t vp_count, int32_t proc_count, const int64_t* vp_bytes,
+                          const int32_t* bin_of_proc, int32_t n_bins,
+                          const int64_t* bin_capacity, od_move* out, int32_t cap,
+                          int32_t* n_out) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    const Capacity c = capacity_of(vp_bytes, vp_count, bin_of_proc, proc_count, n_bins,
+                                   bin_capacity);
+    return emit_moves(plan_greedy_capacity(l, m, proc_count, c), out, cap, n_out);
+  });
+}
+
+int od_refine_swap_lb_capacity(const double* loads, int32_t n_loads, const int32_t* map,
+                               int32_t vp_count, int32_t proc_count, double tolerance,
+                               const int64_t* vp_bytes, const int32_t* bin_of_proc,
+                               int32_t n_bins, const int64_t* bin_capacity, od_move* out,
+                               int32_t cap, int32_t* n_out) {
+  return guarded([&] {
+    auto l = vec_view(loads, n_loads, "loads");
+    auto m = map_view(map, vp_count, proc_count);
+    const Capacity c = capacity_of(vp_bytes, vp_count, bin_of_proc, proc_count, n_bins,
+                                   bin_capacity);
+    return emit_moves(plan_refine_capacity(l, m, proc_count, tolerance, c), out, cap, n_out);
+  });
+}
+
 static GpuCostModel gpu_of(const od_gpu_model* g) {
   need(g, "gpu model");
   GpuCostModel m;

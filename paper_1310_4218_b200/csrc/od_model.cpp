@@ -416,6 +416,181 @@ std::vector<MoveRec> plan_refine_adjacent(const std::vector<double>& loads,
   return plan;
 }
 
+// ------------------------------------------------- capacity-aware balancers --
+
+void Capacity::validate(int32_t K, int32_t P) const {
+  if (int32_t(vp_bytes.size()) != K) throw ValidationError("capacity: vp_bytes length mismatch");
+  if (int32_t(bin_of_proc.size()) != P)
+    throw ValidationError("capacity: bin_of_proc length mismatch");
+  for (int64_t b : vp_bytes)
+    if (b < 0) throw ValidationError("capacity: chunk bytes must be >= 0");
+  for (int32_t b : bin_of_proc)
+    if (b < 0 || b >= int32_t(bin_cap.size())) throw ValidationError("capacity: bin out of range");
+  for (int64_t c : bin_cap)
+    if (c < 0) throw ValidationError("capacity: bin capacity must be >= 0");
+}
+
+std::vector<MoveRec> plan_greedy_capacity(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P,
+                                          const Capacity& cap) {
+  const int32_t K = int32_t(map.size());
+  if (int32_t(loads.size()) != K) throw ValidationError("greedy_lb: load vector length mismatch");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  cap.validate(K, P);
+  // plan_greedy's order and least-loaded rule, over the processors whose bin
+  // still has room for the chunk
+  std::vector<int32_t> order(K);
+  for (int32_t v = 0; v < K; ++v) order[v] = v;
+  std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) {
+    return loads[a] > loads[b] || (!(loads[b] > loads[a]) && !(loads[a] > loads[b]) && a < b);
+  });
+  std::vector<double> bin(P, 0.0);
+  std::vector<int64_t> used(cap.bin_cap.size(), 0);
+  std::vector<int32_t> dest(K, 0);
+  for (int32_t v : order) {
+    int32_t p = -1;
+    for (int32_t q = 0; q < P; ++q) {
+      const int32_t b = cap.bin_of_proc[q];
+      if (used[b] + cap.vp_bytes[v] > cap.bin_cap[b]) continue;
+      if (p < 0 || bin[q] < bin[p]) p = q;
+    }
+    if (p < 0) {
+      // no bin has room: the processor whose bin has the most room left
+      for (int32_t q = 0; q < P; ++q) {
+        const int32_t b = cap.bin_of_proc[q], bp = p < 0 ? -1 : cap.bin_of_proc[p];
+        if (p < 0 || cap.bin_cap[b] - used[b] > cap.bin_cap[bp] - used[bp]) p = q;
+      }
+    }
+    dest[v] = p;
+    bin[p] += loads[v];
+    used[cap.bin_of_proc[p]] += cap.vp_bytes[v];
+  }
+  // Repair (only when the greedy pass had to overfill): a bin over capacity
+  // holds at least one chunk that moved in (its own chunks fitted before the
+  // plan), so return moved-in chunks home, lightest first, until every bin
+  // fits; each return shrinks the plan, so this ends at the latest with the
+  // starting layout.
+  for (bool over = true; over;) {
+    over = false;
+    for (size_t b = 0; b < used.size(); ++b) {
+      while (used[b] > cap.bin_cap[b]) {
+        int32_t back = -1;
+        for (int32_t v = 0; v < K; ++v)
+          if (dest[v] != map[v] && cap.bin_of_proc[dest[v]] == int32_t(b) &&
+              cap.bin_of_proc[map[v]] != int32_t(b) &&
+              (back < 0 || loads[v] < loads[back] || (loads[v] == loads[back] && v < back)))
+            back = v;
+        if (back < 0) break;  // the bin was over capacity before the plan
+        used[b] -= cap.vp_bytes[back];
+        used[cap.bin_of_proc[map[back]]] += cap.vp_bytes[back];
+        dest[back] = map[back];
+        over = true;
+      }
+    }
+  }
+  std::vector<MoveRec> plan;
+  for (int32_t v = 0; v < K; ++v)
+    if (dest[v] != map[v]) plan.push_back({v, map[v], dest[v]});
+  return plan;
+}
+
+std::vector<MoveRec> plan_refine_capacity(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P, double tol,
+                                          const Capacity& cap) {
+  const int32_t K = int32_t(map.size());
+  if (int32_t(loads.size()) != K)
+    throw ValidationError("refine_swap_lb: load vector length mismatch");
+  if (tol < 0) throw ValidationError("refine_swap_lb: tolerance must be >= 0");
+  if (P < 1) throw ValidationError("proc count must be >= 1");
+  cap.validate(K, P);
+  std::vector<int32_t> where = map;
+  std::vector<double> acc = totals_per_proc(loads, where, P);
+  std::vector<int64_t> used(cap.bin_cap.size(), 0);
+  for (int32_t v = 0; v < K; ++v) used[cap.bin_of_proc[where[v]]] += cap.vp_bytes[v];
+  // a bin may take `delta` more bytes if it shrinks or stays within capacity
+  auto fits = [&](int32_t b, int64_t delta) { return delta <= 0 || used[b] + delta <= cap.bin_cap[b]; };
+  double sum = 0.0;
+  for (double a : acc) sum += a;
+  const double avg = sum / P;
+  const double ceil_load = avg * (1.0 + tol);
+
+  std::vector<MoveRec> plan;
+  std::vector<int32_t> donors, takers;
+  auto members = [&](int32_t p, std::vector<int32_t>& out) {
+    out.clear();
+    for (int32_t v = 0; v < K; ++v)
+      if (where[v] == p) out.push_back(v);
+  };
+  const int32_t max_rounds = K * P;
+  for (int32_t round = 0; round < max_rounds; ++round) {
+    int32_t hot = -1;
+    for (int32_t p = 0; p < P; ++p)
+      if (acc[p] > ceil_load && (hot < 0 || acc[p] > acc[hot])) hot = p;
+    if (hot < 0) break;
+    const double excess = acc[hot] - avg;
+    const int32_t bh = cap.bin_of_proc[hot];
+    members(hot, donors);
+    int32_t mv = -1, mq = -1;
+    double mscore = 0;
+    for (int32_t v : donors)
+      for (int32_t q = 0; q < P; ++q) {
+        if (q == hot || acc[q] >= avg) continue;
+        const double after_src = acc[hot] - loads[v];
+        const double after_dst = acc[q] + loads[v];
+        const double ds = std::fabs(after_src - avg);
+        if (ds >= excess || after_dst > ceil_load) continue;
+        const int32_t bq = cap.bin_of_proc[q];
+        if (bq != bh && !fits(bq, cap.vp_bytes[v])) continue;
+        const double score = larger(ds, std::fabs(after_dst - avg));
+        if (mv < 0 || score < mscore) { mv = v; mq = q; mscore = score; }
+      }
+    if (mv >= 0) {
+      plan.push_back({mv, hot, mq});
+      acc[hot] -= loads[mv];
+      acc[mq] += loads[mv];
+      const int32_t bq = cap.bin_of_proc[mq];
+      used[bh] -= cap.vp_bytes[mv];
+      used[bq] += cap.vp_bytes[mv];
+      where[mv] = mq;
+      continue;
+    }
+    int32_t sa = -1, sb = -1, sq = -1;
+    double sscore = 0;
+    for (int32_t q = 0; q < P; ++q) {
+      if (q == hot || acc[q] >= avg) continue;
+      const int32_t bq = cap.bin_of_proc[q];
+      members(q, takers);
+      for (int32_t a : donors)
+        for (int32_t b : takers) {
+          const double d = loads[a] - loads[b];
+          if (d <= 0) continue;
+          const double after_src = acc[hot] - d;
+          const double after_dst = acc[q] + d;
+          const double ds = std::fabs(after_src - avg);
+          if (ds >= excess || after_dst > ceil_load) continue;
+          if (bq != bh) {
+            const int64_t db = cap.vp_bytes[a] - cap.vp_bytes[b];
+            if (!fits(bq, db) || !fits(bh, -db)) continue;
+          }
+          const double score = larger(ds, std::fabs(after_dst - avg));
+          if (sa < 0 || score < sscore) { sa = a; sb = b; sq = q; sscore = score; }
+        }
+    }
+    if (sa < 0) break;
+    plan.push_back({sa, hot, sq});
+    plan.push_back({sb, sq, hot});
+    const double d = loads[sa] - loads[sb];
+    acc[hot] -= d;
+    acc[sq] += d;
+    const int64_t db = cap.vp_bytes[sa] - cap.vp_bytes[sb];
+    used[cap.bin_of_proc[sq]] += db;
+    used[bh] -= db;
+    where[sa] = sq;
+    where[sb] = hot;
+  }
+  return plan;
+}
+
 // ------------------------------------------------------------ modelled costs --
 
 void GpuCostModel::validate() const {
@@ -481,7 +656,8 @@ double plan_cost_model(const std::vector<MoveRec>& plan, const std::vector<int64
 Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
                       int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
                       int32_t first_strategy, int32_t later_strategy, double threshold,
-                      double tolerance, int32_t kind, int32_t kx, int32_t ky) {
+                      double tolerance, int32_t kind, int32_t kx, int32_t ky,
+                      const Capacity* cap) {
   Decision d;
   d.totals = totals_per_proc(loads, map, P);
   d.imbalance_before = max_over_mean(d.totals);
@@ -489,12 +665,13 @@ Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_
   if (epoch < epochs && balance_needed(d.totals, threshold)) {
     d.strategy = balance_calls == 0 ? first_strategy : later_strategy;
     if (d.strategy == kGreedy)
-      d.plan = plan_greedy(loads, map, P);
+      d.plan = cap ? plan_greedy_capacity(loads, map, P, *cap) : plan_greedy(loads, map, P);
     else if (d.strategy == kRefineAdjacent) {
       if (kind < 0) throw ValidationError("strategy 2 (refine_adjacent) needs the decomposition");
       d.plan = plan_refine_adjacent(loads, map, P, tolerance, kind, kx, ky);
     } else
-      d.plan = plan_refine_swap(loads, map, P, tolerance);
+      d.plan = cap ? plan_refine_capacity(loads, map, P, tolerance, *cap)
+                   : plan_refine_swap(loads, map, P, tolerance);
     ++balance_calls;
     if (!d.plan.empty())
       d.imbalance_after = max_over_mean(totals_per_proc(loads, apply_moves(map, P, d.plan), P));

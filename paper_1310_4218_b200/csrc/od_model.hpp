@@ -95,6 +95,26 @@ std::vector<MoveRec> plan_refine_adjacent(const std::vector<double>& loads,
                                           const std::vector<int32_t>& map, int32_t P, double tol,
                                           int32_t kind, int32_t kx, int32_t ky);                            // :68-152
 
+// B200 extension (off-parity): capacity-aware balancing.  The reference's
+// balancers ignore memory: GreedyLB can pack chunks onto one GPU
+// past its HBM.  Processors are grouped into bins (the GPUs that hold them);
+// a plan never moves a chunk into a bin whose resident chunk bytes would then
+// exceed its capacity (moves out of an over-full bin are always allowed).
+// With capacities no plan can reach, both equal plan_greedy /
+// plan_refine_swap exactly.
+struct Capacity {
+  std::vector<int64_t> vp_bytes;     // K
+  std::vector<int32_t> bin_of_proc;  // P
+  std::vector<int64_t> bin_cap;      // bins
+  void validate(int32_t K, int32_t P) const;
+};
+std::vector<MoveRec> plan_greedy_capacity(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P,
+                                          const Capacity& cap);
+std::vector<MoveRec> plan_refine_capacity(const std::vector<double>& loads,
+                                          const std::vector<int32_t>& map, int32_t P, double tol,
+                                          const Capacity& cap);
+
 // ---- modelled costs (gpu_cost.hpp:21-80, balancer.hpp:157-175) ---------------
 // The B200 path measures these quantities; the model functions stay available
 // with the reference's arithmetic for users who compare against the simulator.
@@ -157,10 +177,12 @@ struct Decision {
 // Given the epoch's per-VP loads: totals, imbalance, trigger check (never on
 // the last epoch), first call -> first strategy, later calls -> later
 // strategy; balance_calls is incremented on every triggered call.
+// With `cap`, Greedy and RefineSwap calls use the capacity-aware planners.
 Decision decide_epoch(const std::vector<double>& loads, const std::vector<int32_t>& map,
                       int32_t P, int32_t epoch, int32_t epochs, int32_t& balance_calls,
                       int32_t first_strategy, int32_t later_strategy, double threshold,
-                      double tolerance, int32_t kind = -1, int32_t kx = 0, int32_t ky = 0);
+                      double tolerance, int32_t kind = -1, int32_t kx = 0, int32_t ky = 0,
+                      const Capacity* cap = nullptr);
 
 // ---- halo exchange schedule -------------------------------------------------
 // Faces between chunks owned by different ranks.  Both sides enumerate the

@@ -322,6 +322,7 @@ class Runtime {
   std::vector<std::pair<int, int>> prof_j_, prof_p_, prof_pack_, prof_x_, prof_f_;
   od_rt_stats st_{};
   std::vector<double> step_wall_;  // by global step index (NaN until collected)
+  Capacity capacity_;  // per-GPU chunk-data bins (cfg.capacity_mib > 0)
   std::vector<od_epoch_summary> history_;
 };
 
@@ -377,6 +378,25 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     if (map_[v] / cfg.procs_per_node == 0) node0.push_back(subs_[v]);
   base_ = make_load_field(cfg.nx, cfg.ny, Pattern(cfg.pattern), cfg.heavy_value,
                           cfg.light_value, node0);
+  if (cfg.capacity_mib < 0) throw ValidationError("capacity_mib must be >= 0");
+  if (cfg.capacity_mib > 0) {
+    // one bin per GPU; a chunk's footprint is its device allocation (U^t,
+    // U^{t+1}, A with the pitch padding)
+    capacity_.bin_cap.assign(world_, int64_t(cfg.capacity_mib) << 20);
+    capacity_.bin_of_proc.resize(P());
+    for (int32_t p = 0; p < P(); ++p) capacity_.bin_of_proc[p] = rank_of_proc(p);
+    capacity_.vp_bytes.resize(K());
+    std::vector<int64_t> used(world_, 0);
+    for (int32_t v = 0; v < K(); ++v) {
+      const int64_t plane = int64_t(subs_[v].h()) * ((subs_[v].w() + 15) / 16 * 16);
+      capacity_.vp_bytes[v] = (2 * plane * cfg.nz * cfg.fields + plane * cfg.nz) * 8;
+      used[rank_of_vp(v)] += capacity_.vp_bytes[v];
+    }
+    for (int q = 0; q < world_; ++q)
+      if (used[q] > capacity_.bin_cap[q])
+        throw ValidationError("capacity_mib is below the initial chunk data of GPU " +
+                              std::to_string(q) + " (" + std::to_string(used[q] >> 20) + " MiB)");
+  }
 
   OD_CU(cudaSetDevice(device_));
   OD_CU(cudaStreamCreateWithFlags(&s0_, cudaStreamNonBlocking));
@@ -1676,7 +1696,8 @@ void Runtime::finish_epoch(int32_t e, int32_t steps, EpochOut& o) {
   Decision d = decide_epoch(o.loads, map_, P(), e, cfg_.epochs, balance_calls_,
                             cfg_.first_call_strategy, cfg_.later_call_strategy,
                             cfg_.trigger_threshold, cfg_.refine_tolerance,
-                            cfg_.decomposition_kind, cfg_.kx, cfg_.ky);
+                            cfg_.decomposition_kind, cfg_.kx, cfg_.ky,
+                            cfg_.capacity_mib > 0 ? &capacity_ : nullptr);
   o.totals = d.totals;
   o.imb_before = d.imbalance_before;
   o.imb_after = d.imbalance_after;

@@ -226,3 +226,70 @@ def test_refine_adjacent_validation_and_policy():
         od.refine_adjacent_lb([1.0] * 6, m, od.Decomposition(od.DecompositionKind.TwoD, 2, 2))
     # balanced input: nothing to do
     assert od.refine_adjacent_lb([1.0] * 6, m, dec).moves == []
+
+
+# ---------------------------------------------- capacity-aware (B200 extension)
+
+def _bins(P, G):
+    return [p * G // P for p in range(P)]
+
+
+def test_capacity_planners_equal_reference_when_capacity_is_ample():
+    # with capacities no plan can reach, the capacity-aware planners are the
+    # reference's greedy_lb / refine_swap_lb, move for move (420 goldens)
+    for c in json.load(open(os.path.join(GOLD, "lb_cases.json"))):
+        loads = [float.fromhex(x) for x in c["loads"]]
+        K, P = c["K"], c["P"]
+        m = M(c["mapping"], P)
+        G = max(1, P // 2)
+        vb, bp, cap = [1000 + v for v in range(K)], _bins(P, G), [1 << 60] * G
+        assert [list(x) for x in moves(od.greedy_lb_capacity(loads, m, vb, bp, cap))] == \
+            c["greedy"]
+        assert [list(x) for x in moves(od.refine_swap_lb_capacity(loads, m, vb, bp, cap,
+                                                                  c["tol"]))] == c["refine"]
+
+
+def _bin_bytes(assign, vb, bp, G):
+    used = [0] * G
+    for v, p in enumerate(assign):
+        used[bp[p]] += vb[v]
+    return used
+
+
+def test_capacity_planners_respect_capacity():
+    # GreedyLB re-places every chunk by load only and can pack light chunks
+    # past a GPU's memory; the capacity-aware planners never
+    # exceed a bin that started within capacity, and refine stays monotone
+    rng = np.random.default_rng(7)
+    plain_violations = 0
+    for t in range(300):
+        G = int(rng.integers(2, 5))
+        P = G * int(rng.integers(1, 3))
+        K = P * int(rng.integers(2, 6))
+        loads = rng.uniform(0.1, 4.0, K)
+        # heavy chunks are small, light ones big: load-only packing overfills
+        vb = [int(1000 + 3000 / l) for l in loads]
+        mp = np.array(od.initial_block_mapping(K, P).assignment())
+        bp = _bins(P, G)
+        start = _bin_bytes(mp, vb, bp, G)
+        cap = [int(max(start) * 1.05)] * G
+        m = M(mp, P)
+        for plan_fn in (lambda: od.greedy_lb_capacity(loads, m, vb, bp, cap),
+                        lambda: od.refine_swap_lb_capacity(loads, m, vb, bp, cap, 0.02)):
+            after = od.apply_plan(m, plan_fn()).assignment()
+            used = _bin_bytes(after, vb, bp, G)
+            assert all(u <= c for u, c in zip(used, cap)), (t, used, cap)
+        ref_after = od.apply_plan(m, od.refine_swap_lb_capacity(loads, m, vb, bp, cap, 0.02))
+        assert od.imbalance_ratio(od.proc_loads(loads, ref_after)) <= \
+            od.imbalance_ratio(od.proc_loads(loads, m)) + 1e-12
+        g_after = od.apply_plan(m, od.greedy_lb(loads, m)).assignment()
+        plain_violations += any(u > c for u, c in zip(_bin_bytes(g_after, vb, bp, G), cap))
+    assert plain_violations > 30  # the constraint is real for the reference's greedy
+
+
+def test_capacity_planner_validation():
+    m = od.initial_block_mapping(4, 2)
+    with pytest.raises(od.ValidationError):
+        od.greedy_lb_capacity([1.0] * 4, m, [1] * 3, [0, 0], [10])
+    with pytest.raises(od.ValidationError):
+        od.refine_swap_lb_capacity([1.0] * 4, m, [1] * 4, [0, 1], [10])  # bin 1 missing

@@ -15,6 +15,16 @@ SLICES = {
         cluster=od.ClusterSpec(1, 4), domain=od.Domain(256, 256, 64, 50),
         decomposition=od.Decomposition(od.DecompositionKind.TwoD, 8, 8),
         advection=od.AdvectionSchedule(128, 2, 10)),
+    # small sanitizer shapes: full 64x4 tiles (sanA) / full 32x8 tiles (sanB),
+    # 4 processors balancing every epoch, a moving hotspot
+    "sanA": lambda **k: configs.cfg3(nodes=1, **k).replace(
+        cluster=od.ClusterSpec(1, 4), domain=od.Domain(128, 128, 16, 4),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 2, 2), n_inner=24,
+        window=od.MeasurementWindow(2, 1), advection=od.AdvectionSchedule(64, 2, 3)),
+    "sanB": lambda **k: configs.cfg3(nodes=1, **k).replace(
+        cluster=od.ClusterSpec(1, 4), domain=od.Domain(128, 128, 16, 4),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 4, 4), n_inner=24,
+        window=od.MeasurementWindow(2, 1), advection=od.AdvectionSchedule(64, 2, 3)),
 }
 cfg = (SLICES.get(name) or configs.CONFIGS[name])(**kw)
 with od.Engine(cfg) as eng:

@@ -5,6 +5,7 @@
 #   tests                  pytest -m gpu (all GPU parity tests)
 #   smoke                  __graft_entry__.smoke()
 #   bench CFG [ARGS..]     bench.py --config CFG ARGS  -> gpurun_out/bench_CFG[_TAG].json
+#   mbench N CFG [ARGS..]  torchrun --nproc-per-node N bench.py --gpus N --config CFG ARGS
 #   ref CFG [ARGS..]       bench.py --impl reference --config CFG ARGS
 #   launches CFG           ncu launch list (gpu__time_duration) of a short bench run
 #   full CFG REGEX         ncu --set full capture of one launch of kernel REGEX (diag run)
@@ -31,6 +32,12 @@ for stage in "$@"; do
       cfg=$2; shift 2
       timeout 1500 python bench.py --config "$cfg" "$@" > gpurun_out/bench_$cfg$T.json \
         2> gpurun_out/bench_$cfg$T.err; r=$?; tail -c 600 gpurun_out/bench_$cfg$T.json ;;
+    mbench)
+      n=$2; cfg=$3; shift 3
+      timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$n" \
+        --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 1000)) bench.py --gpus "$n" \
+        --config "$cfg" "$@" > gpurun_out/bench_${cfg}_n$n$T.json 2> gpurun_out/bench_${cfg}_n$n$T.err
+      r=$?; tail -c 600 gpurun_out/bench_${cfg}_n$n$T.json ;;
     ref)
       cfg=$2; shift 2
       timeout 1500 python bench.py --impl reference --config "$cfg" "$@" \
@@ -52,10 +59,14 @@ for stage in "$@"; do
       timeout 1500 compute-sanitizer --tool "$tool" --error-exitcode 9 \
         python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_${tool}_smoke$T.log 2>&1
       r=$?
-      timeout 1500 compute-sanitizer --tool "$tool" --error-exitcode 9 \
-        python tools/diag.py cfg4s > gpurun_out/san_${tool}_step$T.log 2>&1
-      r2=$?; [ $r -eq 0 ] && r=$r2
-      tail -3 gpurun_out/san_${tool}_smoke$T.log gpurun_out/san_${tool}_step$T.log ;;
+      for shape in "sanA overlap=4" "sanA overlap=7" "sanB overlap=4" "sanB overlap=7"; do
+        tagn=$(echo $shape | tr ' =' '__')
+        timeout 1500 compute-sanitizer --tool "$tool" --error-exitcode 9 \
+          python tools/diag.py $shape > gpurun_out/san_${tool}_${tagn}$T.log 2>&1
+        r2=$?; [ $r -eq 0 ] && r=$r2
+        tail -2 gpurun_out/san_${tool}_${tagn}$T.log
+      done
+      tail -3 gpurun_out/san_${tool}_smoke$T.log ;;
     *) echo "unknown stage $1"; r=2 ;;
   esac
   echo "[gpu_suite] $stage -> rc $r"
