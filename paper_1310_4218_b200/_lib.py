@@ -10,7 +10,12 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libod_b200.so")
+# OD_LIB_VARIANT=checked loads the test-only checked build (device bounds
+# checks and injected sleeps at the synchronisation points; make builds both)
+_VARIANT = os.environ.get("OD_LIB_VARIANT", "")
+if _VARIANT not in ("", "checked"):
+    raise ImportError(f"unknown OD_LIB_VARIANT {_VARIANT!r} (expected 'checked' or unset)")
+LIB_PATH = os.path.join(_HERE, "libod_b200_checked.so" if _VARIANT else "libod_b200.so")
 
 OD_OK, OD_EVALIDATION, OD_ERUNTIME = 0, 2, 3
 

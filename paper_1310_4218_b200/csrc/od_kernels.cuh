@@ -30,6 +30,8 @@ enum Face : int32_t { kLeft = 0, kRight = 1, kTop = 2, kBottom = 3 };
 struct FaceDev {
   const double* p;     // element (f=0, k=0, e=0) of the strip
   int64_t fs, ks, es;  // strides (elements) for field, level, position along the face
+  const double* lo;    // the allocation the strip lies in: [lo, hi) (checked builds)
+  const double* hi;
 };
 
 struct ChunkDev {
@@ -74,6 +76,38 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Checked build (libod_b200_checked.so, -DOD_CHECKED; compute-sanitizer is not
+// available on the GPU pool): every walker's first and last global address is
+// checked against its allocation, every shared-memory ring offset against the
+// plane, and random sleeps are injected at the cross-CTA synchronisation
+// points (tile step stamps, pack counters, halo flags) and inside the ring
+// hand-off, so ordering bugs that a lucky schedule hides surface as wrong
+// fields in the bitwise stress tests (tests/test_gpu_stress.py).
+#ifdef OD_CHECKED
+#define OD_CHECK(cond, what)                                                              \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("od checked: %s failed (block %d, thread %d,%d)\n", what, int(blockIdx.x),   \
+             int(threadIdx.x), int(threadIdx.y));                                         \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+__device__ __forceinline__ uint64_t dmix64(uint64_t x);
+__device__ __forceinline__ void od_jitter(unsigned salt) {
+  const uint64_t h = dmix64(globaltimer_ns() ^ (uint64_t(blockIdx.x) << 32) ^
+                            (uint64_t(threadIdx.y * 32 + threadIdx.x) << 20) ^ salt);
+  if ((h & 7) == 0) __nanosleep(unsigned(h >> 40) & 8191);
+}
+#else
+#define OD_CHECK(cond, what) \
+  do {                       \
+  } while (0)
+__device__ __forceinline__ void od_jitter(unsigned) {}
+#endif
+__device__ __forceinline__ bool od_in(const double* p, const double* lo, const double* hi) {
+  return p >= lo && p < hi;
 }
 
 // Per-SM processor-sharing clock for the per-chunk load measurement.  The
@@ -505,9 +539,12 @@ __device__ __forceinline__ void physics_init(ColumnState& s, const ChunkDev& c, 
                                              int32_t n_inner) {
   int row = c.y0 + y - shift;
   if (row < 0) row += ny;
+  OD_CHECK(row >= 0 && row < ny && c.x0 + x >= 0 && c.x0 + x < nx, "physics: load field index");
   const double cm = __ldg(cfield + int64_t(row) * nx + c.x0 + x);
   int T = int(floor(__dmul_rn(double(nz), cm))) - 1;
   s.T = T < 0 ? 0 : T;
+  OD_CHECK(c.a + int64_t(y) * c.pitch + x + int64_t(nz - 1) * c.kstride < c.a + int64_t(nz) * c.kstride,
+           "physics: A range");
   s.ks = c.kstride;
   s.B = c.in + int64_t(y) * c.pitch + x;
   s.A = c.a + int64_t(y) * c.pitch + x;
@@ -698,6 +735,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   const double* py = nullptr;
   int64_t xstep = 0, ystep = 0;
   int ox = 0, oy = 0, ny_cells = 0;
+  const double* const in_hi = c.in + int64_t(F) * c.fstride;
+  const double *xlo = c.in, *xhi = in_hi, *ylo = c.in, *yhi = in_hi;  // walker allocations
   if (ly < hv && (lx == 0 || lx == tpr - 1)) {
     // x-halo duty: the row's first thread loads the left, its last the right
     // halo cell (a one-thread row, tw = 2, never occurs: tw >= 8)
@@ -711,6 +750,8 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       const FaceDev& fd = c.face[left ? kLeft : kRight];
       px = fd.p + int64_t(y) * fd.es;
       xstep = fd.ks;
+      xlo = fd.lo;
+      xhi = fd.hi;
     }
   }
   if (pair > 0 && (ly == 0 || ly == g.th - 1)) {
@@ -725,10 +766,35 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
       const FaceDev& fd = c.face[top ? kTop : kBottom];
       py = fd.p + int64_t(x) * fd.es;
       ystep = fd.ks;
+      ylo = fd.lo;
+      yhi = fd.hi;
     }
   }
   const int oc = (ly + 1) * PW + 2 + 2 * lx;
   const int levels = F * nz;
+#ifdef OD_CHECKED
+  {
+    const int64_t span = int64_t(levels - 1) * ks;
+    if (ncell > 0) {
+      OD_CHECK(od_in(pc, c.in, in_hi) && od_in(pc + span + ncell - 1, c.in, in_hi),
+               "tile: U^t read range");
+      OD_CHECK(od_in(c.out + own, c.out, c.out + int64_t(F) * c.fstride) &&
+                   od_in(c.out + own + span + ncell - 1, c.out, c.out + int64_t(F) * c.fstride),
+               "tile: U^{t+1} write range");
+      OD_CHECK(oc >= PW && oc + 2 <= (g.th + 1) * PW && oc + 2 <= kPlaneMax, "tile: ring offset");
+    }
+    if (px) {
+      OD_CHECK(od_in(px, xlo, xhi) && od_in(px + int64_t(levels - 1) * xstep, xlo, xhi),
+               "tile: x-halo read range");
+      OD_CHECK(ox >= 0 && ox < kPlaneMax, "tile: x-halo ring offset");
+    }
+    if (py) {
+      OD_CHECK(od_in(py, ylo, yhi) && od_in(py + int64_t(levels - 1) * ystep + ny_cells - 1, ylo, yhi),
+               "tile: y-halo read range");
+      OD_CHECK(oy >= 0 && oy + ny_cells <= kPlaneMax, "tile: y-halo ring offset");
+    }
+  }
+#endif
 
   auto issue = [&](int L) {
     if (L < levels) {
@@ -886,6 +952,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     level(L + 1, k);
     if (++k == nz) k = 0;
     cp_async_wait<S - 3>();  // this thread's planes <= L+4 landed
+    od_jitter(4u + unsigned(L));
     mbar_arrive(&s_ring_bar);
     physics(2 * q0, 2 * q1);
   }
@@ -987,6 +1054,10 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
                   int64_t(f) * nz * j.lenp;
     // (level, position) flattened; 8 independent loads in flight per thread
     const int n = nz * j.len;
+    OD_CHECK(j.rdst >= 0 && j.rdst + (int64_t(f) + 1) * nz * j.lenp <= pk.half_elems,
+             "pack: peer strip range");
+    OD_CHECK(off + int64_t(nz - 1) * c.kstride + int64_t(j.len - 1) * es < c.fstride,
+             "pack: face read range");
     constexpr int U = 8;
     for (int i0 = tid; i0 < n; i0 += U * nthr) {
       double v[U];
@@ -1009,6 +1080,7 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
     }
     __threadfence_system();
     __syncthreads();
+    od_jitter(3u);
     if (lead && atomicAdd(&pk.counters[1], 1u) == unsigned(total - 1)) {
       __threadfence_system();
       for (int i = 0; i < pk.n_notify; ++i)
@@ -1022,6 +1094,7 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
 // pre-roll poll.
 __device__ __forceinline__ void tile_deps(const StepDeps& sd, int self, HaloWait& hw) {
   if (!sd.on) return;
+  od_jitter(1u);
   if (threadIdx.x == 0 && threadIdx.y == 0) {
     const uint64_t t0 = globaltimer_ns();
     while (ld_acquire_gpu_u32(sd.done + self) < sd.step) {
@@ -1044,6 +1117,7 @@ __device__ __forceinline__ void tile_publish(const StepDeps& sd, int self,
   __syncthreads();  // every thread's U^{t+1} stores issued
   __shared__ int s_last;
   if (threadIdx.x == 0 && threadIdx.y == 0) {
+    od_jitter(2u);
     __threadfence();
     st_release_gpu_u32(sd.done + self, sd.step + 1);
     if (sd.end_ns) atomicMax(sd.end_ns, (unsigned long long)globaltimer_ns());
@@ -1144,6 +1218,8 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   const double* py = nullptr;
   int64_t xstep = 0, ystep = 0;
   int ox = 0, oy = 0, ny_cells = 0;
+  const double* const in_hi = c.in + int64_t(F) * c.fstride;
+  const double *xlo = c.in, *xhi = in_hi, *ylo = c.in, *yhi = in_hi;  // walker allocations
   if (!phys && ly < hv && (lx == 0 || lx == tpr - 1)) {
     const bool left = lx == 0;
     const int xs = left ? tile.tx0 - 1 : tile.tx0 + wv;
@@ -1155,6 +1231,8 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       const FaceDev& fd = c.face[left ? kLeft : kRight];
       px = fd.p + int64_t(y) * fd.es;
       xstep = fd.ks;
+      xlo = fd.lo;
+      xhi = fd.hi;
     }
   }
   if (!phys && pair > 0 && (ly == 0 || ly == g.th - 1)) {
@@ -1169,10 +1247,35 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       const FaceDev& fd = c.face[top ? kTop : kBottom];
       py = fd.p + int64_t(x) * fd.es;
       ystep = fd.ks;
+      ylo = fd.lo;
+      yhi = fd.hi;
     }
   }
   const int oc = (ly + 1) * PW + 2 + 2 * lx;
   const int levels = F * nz;
+#ifdef OD_CHECKED
+  {
+    const int64_t span = int64_t(levels - 1) * ks;
+    if (ncell > 0) {
+      OD_CHECK(od_in(pc, c.in, in_hi) && od_in(pc + span + ncell - 1, c.in, in_hi),
+               "tile: U^t read range");
+      OD_CHECK(od_in(c.out + own, c.out, c.out + int64_t(F) * c.fstride) &&
+                   od_in(c.out + own + span + ncell - 1, c.out, c.out + int64_t(F) * c.fstride),
+               "tile: U^{t+1} write range");
+      OD_CHECK(oc >= PW && oc + 2 <= (g.th + 1) * PW && oc + 2 <= kPlaneMax, "tile: ring offset");
+    }
+    if (px) {
+      OD_CHECK(od_in(px, xlo, xhi) && od_in(px + int64_t(levels - 1) * xstep, xlo, xhi),
+               "tile: x-halo read range");
+      OD_CHECK(ox >= 0 && ox < kPlaneMax, "tile: x-halo ring offset");
+    }
+    if (py) {
+      OD_CHECK(od_in(py, ylo, yhi) && od_in(py + int64_t(levels - 1) * ystep + ny_cells - 1, ylo, yhi),
+               "tile: y-halo read range");
+      OD_CHECK(oy >= 0 && oy + ny_cells <= kPlaneMax, "tile: y-halo ring offset");
+    }
+  }
+#endif
 
   auto issue = [&](int L) {
     if (L < levels) {
@@ -1279,6 +1382,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       level(L + 1, k);
       if (++k == nz) k = 0;
       cp_async_wait<S - 3>();
+      od_jitter(4u + unsigned(L));
       mbar_arrive(&s_ring_bar);
     }
     if (L < levels) {

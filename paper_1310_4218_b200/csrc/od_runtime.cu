@@ -746,6 +746,8 @@ void Runtime::release_chunk(ChunkMem& m) {
 FaceDev Runtime::edge_of(const ChunkMem& s, int side, int par) const {
   FaceDev f;
   const double* b = s.u[par];
+  f.lo = b;
+  f.hi = b + s.kstride() * cfg_.nz * cfg_.fields;
   f.fs = s.kstride() * cfg_.nz;
   f.ks = s.kstride();
   switch (side) {
@@ -1026,6 +1028,8 @@ void Runtime::rebuild_tables() {
         } else {
           const int32_t len = (d == kLeft || d == kRight) ? c.h : c.w;
           c.face[d].p = d_recv_ + par * recv_half_ + recv_face_off_[i][d];
+          c.face[d].lo = d_recv_ + par * recv_half_;
+          c.face[d].hi = d_recv_ + par * recv_half_ + int64_t(recv_cap_);
           const int32_t lenp = (len + 1) & ~1;
           c.face[d].fs = int64_t(cfg_.nz) * lenp;
           c.face[d].ks = lenp;
