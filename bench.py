@@ -465,6 +465,15 @@ def main():
                    "measured_next_epoch": nxt[0]["imbalance_before"] if nxt else None,
                    "before": last["imbalance_before"], "moves": last["n_moves"]}
     eng_imb = [h["imbalance_before"] for h in full]  # every epoch so far, warm-up included
+    if post_lb is not None and world > 1:
+        # the per-GPU view beside the load view: max/avg over GPUs of each
+        # GPU's own mean step-kernel interval in the timed steps.  Under
+        # cross-step overlap and P2P halos a light GPU's wall includes waiting
+        # for its neighbours' strips, so this ratio understates the work
+        # imbalance; the loads (share clock, idling charged to nobody) are what
+        # the balancer is given
+        kt = [r["kernel_avg_ms"] for r in per_rank]
+        post_lb["gpu_wall_max_over_avg"] = max(kt) / (sum(kt) / len(kt))
 
     # end to end through the host-facing C ABI call: per step H2D of the
     # step's load multiplier field (pinned) and D2H of per-chunk loads

@@ -18,15 +18,31 @@ import paper_1310_4218_b200 as od  # noqa: E402
 from oracle import ref as oref  # noqa: E402
 from paper_1310_4218_b200 import configs  # noqa: E402
 
+rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+local = int(os.environ.get("LOCAL_RANK", "0"))
+if world > 1:  # torchrun: one rank per GPU, the presets' processors dealt to the GPUs
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 names = sys.argv[1:] or ["expA", "expB", "expC", "cfg1"]
 out = {}
 for name in names:
     cfg = configs.CONFIGS[name]()
+    if cfg.proc_count() < world:
+        continue
+    nid = None
+    if world > 1:
+        obj = [od.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
     t0 = time.perf_counter()
-    with od.Engine(cfg) as eng:
+    with od.Engine(cfg, rank, world, local, nid) as eng:
         tl = eng.run()
     wall = time.perf_counter() - t0
-    row = {"config": od.config_to_json(cfg), "gpus": 1, "host_wall_s": wall,
+    if rank != 0:
+        continue
+    row = {"config": od.config_to_json(cfg), "gpus": world, "host_wall_s": wall,
            "csv": od.render_report(tl, "csv"),
            "epochs": [{"epoch": e.epoch, "vp_loads": e.vp_loads, "proc_loads": e.proc_loads,
                        "moves": [tuple(m) for m in e.plan.moves],
@@ -44,8 +60,11 @@ for name in names:
         row["reference_csv"] = oref.run_json(j)["csv"]
         row["reference_note"] = "config through run_experiment with the default cost model"
     out[name] = row
-    print(f"== {name} (B200, measured)\n{row['csv']}== {name} (reference simulator)\n"
+    print(f"== {name} (B200 x{world}, measured)\n{row['csv']}== {name} (reference simulator)\n"
           f"{row['reference_csv']}", flush=True)
-os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-with open(os.path.join(ROOT, "gpurun_out", "paper_presets.json"), "w") as f:
-    json.dump(out, f, indent=1)
+if rank == 0:
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", f"paper_presets_n{world}.json"), "w") as f:
+        json.dump(out, f, indent=1)
+if world > 1:
+    dist.destroy_process_group()
