@@ -333,6 +333,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   } while (!done);
 }
 
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(done)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+// experiment switch (OD_SPIN): run physics while the ring phase is incomplete
+__device__ int g_spin = 0;
+// experiment switch (OD_PHASE): a per-CTA physics head start of a pseudo-random
+// fraction of one level pair's quota, so that CTAs with identical tiles do not
+// run their Jacobi phases in lockstep
+__device__ int g_phase = 0;
+constexpr int kSpinUnits = 32;
+
 // f(b, a) of Fig. 1 / Fig. 4: mix a and b, then n micro-steps of the
 // perturbed logistic map.  Every operation is a correctly rounded add/mul/fma.
 __device__ __forceinline__ double column_f(double b, double a, int n) {
@@ -703,14 +721,14 @@ __device__ __forceinline__ TileGeom tile_geom(const TileDev& t, int wr, int lane
 // keeps the two chains on the branch-free interleaved loop between trip
 // boundaries.  FULL: the tile lies inside the chunk (compile-time two cells
 // per thread, no partial-tile predicates).  Same arithmetic as every path.
-template <int S, bool TIMED, bool FULL>
+template <int S, bool TIMED, bool FULL, int R = kRingSlots>
 __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileDev tile,
                                           const ChunkDev* __restrict__ chunks, int32_t nz,
                                           int32_t F, const double* __restrict__ cfield,
                                           int32_t nx, int32_t ny, int32_t shift, int32_t n_inner,
                                           unsigned long long* __restrict__ chunk_ns,
                                           const HaloWait hw) {
-  constexpr int R = kRingSlots;
+  static_assert((R & (R - 1)) == 0, "ring slots: power of two");
   static_assert(S + 2 <= R && S >= 3, "prefetch depth");
   __shared__ ShareAcct s_acct;
   if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) share_begin(s_acct, share_tag(tile));
@@ -926,6 +944,17 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     fast = 0;  // the level loop's budgets differ from the pre-roll's
   }
 
+  if (g_phase && q0 > 0) {
+    const int slots = (2 * q0) / 16;
+    const int off = slots > 0 ? int(dmix64(uint64_t(blockIdx.x) * 0x9E37u + 7u) % uint64_t(slots + 1)) * 16
+                              : 0;
+    if (off > 0) {
+      fast = 0;
+      physics(off, off);
+      fast = 0;
+    }
+  }
+
   // ring hand-off: an mbarrier phase per level pair.  A thread arrives once its
   // reads of the pair's planes are done and its copies for the next pair have
   // landed, then runs its physics quota while the other warps catch up; the
@@ -942,7 +971,18 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 
   uint32_t parity = 0;
   int k = 0, L = 0;
+  const int spin = g_spin;
   for (; L + 1 < levels; L += 2) {
+    if (spin && !mbar_test(&s_ring_bar, parity)) {
+      // the phase is not complete yet: keep this warp's chains on the FP64
+      // pipe instead of idling (the chains' split into budgets does not
+      // change their operations)
+      fast = 0;
+      do {
+        physics(kSpinUnits, kSpinUnits);
+      } while (!mbar_test(&s_ring_bar, parity));
+      fast = 0;
+    }
     mbar_wait(&s_ring_bar, parity);  // everyone: planes <= L+2 landed, planes L-2, L-1 read
     parity ^= 1;
     issue(L + S);
@@ -980,7 +1020,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 // Partial tiles (chunk edges narrower or shorter than the tile) take an
 // out-of-line path so their predicates do not cost registers in the common
 // full-tile code.
-template <int S, bool TIMED>
+template <int S, bool TIMED, int R = kRingSlots>
 __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const TileDev tile,
                                                const ChunkDev* __restrict__ chunks, int32_t nz,
                                                int32_t F, const double* __restrict__ cfield,
@@ -988,8 +1028,8 @@ __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const 
                                                int32_t n_inner,
                                                unsigned long long* __restrict__ chunk_ns,
                                                const HaloWait hw) {
-  tile_step<S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
-                             hw);
+  tile_step<S, TIMED, false, R>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                chunk_ns, hw);
 }
 
 __device__ __forceinline__ bool tile_full(const TileDev& t, const ChunkDev& c) {
@@ -1142,7 +1182,7 @@ __device__ __forceinline__ void tile_publish(const StepDeps& sd, int self,
 // the first pk.ctas CTAs only pack this step's boundary strips into the peers'
 // buffers and exit; with sd.on the grid is launched with programmatic
 // dependent launch behind the previous step's (cross-step overlap).
-template <int S, bool TIMED, int MINB>
+template <int S, bool TIMED, int MINB, int R = kRingSlots>
 __global__ void __launch_bounds__(32 * kRowWarps, MINB)
     column_step_grid(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
                      int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
@@ -1152,7 +1192,10 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
                      const int32_t* __restrict__ senders, int32_t n_senders,
                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                      const PackArgs pk, const StepDeps sd) {
-  __shared__ __align__(16) double ring[kRingSlots * kPlaneMax];
+  // rings deeper than 8 slots exceed the 48 KB static limit: dynamic smem
+  __shared__ __align__(16) double ring_s[R <= 8 ? R * kPlaneMax : 2];
+  extern __shared__ __align__(16) double ring_d[];
+  double* const ring = R <= 8 ? ring_s : ring_d;
   // cross-step overlap: let the next step's grid launch as soon as every CTA of
   // this one has started; its tiles wait on per-tile stamps, not on this grid
   if (sd.on) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1167,10 +1210,11 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
               nullptr, nullptr, 0, 0};
   tile_deps(sd, self, hw);
   if (tile_full(t, c))
-    tile_step<S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
+    tile_step<S, TIMED, true, R>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
+                                 hw);
   else
-    tile_step_partial<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
-                                hw);
+    tile_step_partial<S, TIMED, R>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                   chunk_ns, hw);
   tile_publish(sd, self, chunk_ns);
 }
 
