@@ -343,13 +343,6 @@ __device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
       : "memory");
   return done != 0;
 }
-// experiment switch (OD_SPIN): run physics while the ring phase is incomplete
-__device__ int g_spin = 0;
-// experiment switch (OD_PHASE): a per-CTA physics head start of a pseudo-random
-// fraction of one level pair's quota, so that CTAs with identical tiles do not
-// run their Jacobi phases in lockstep
-__device__ int g_phase = 0;
-constexpr int kSpinUnits = 32;
 
 // f(b, a) of Fig. 1 / Fig. 4: mix a and b, then n micro-steps of the
 // perturbed logistic map.  Every operation is a correctly rounded add/mul/fma.
@@ -944,17 +937,6 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     fast = 0;  // the level loop's budgets differ from the pre-roll's
   }
 
-  if (g_phase && q0 > 0) {
-    const int slots = (2 * q0) / 16;
-    const int off = slots > 0 ? int(dmix64(uint64_t(blockIdx.x) * 0x9E37u + 7u) % uint64_t(slots + 1)) * 16
-                              : 0;
-    if (off > 0) {
-      fast = 0;
-      physics(off, off);
-      fast = 0;
-    }
-  }
-
   // ring hand-off: an mbarrier phase per level pair.  A thread arrives once its
   // reads of the pair's planes are done and its copies for the next pair have
   // landed, then runs its physics quota while the other warps catch up; the
@@ -971,18 +953,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 
   uint32_t parity = 0;
   int k = 0, L = 0;
-  const int spin = g_spin;
   for (; L + 1 < levels; L += 2) {
-    if (spin && !mbar_test(&s_ring_bar, parity)) {
-      // the phase is not complete yet: keep this warp's chains on the FP64
-      // pipe instead of idling (the chains' split into budgets does not
-      // change their operations)
-      fast = 0;
-      do {
-        physics(kSpinUnits, kSpinUnits);
-      } while (!mbar_test(&s_ring_bar, parity));
-      fast = 0;
-    }
     mbar_wait(&s_ring_bar, parity);  // everyone: planes <= L+2 landed, planes L-2, L-1 read
     parity ^= 1;
     issue(L + S);

@@ -420,14 +420,6 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
-    if (const char* sp = std::getenv("OD_SPIN")) {
-      const int v = std::atoi(sp);
-      OD_CU(cudaMemcpyToSymbol(g_spin, &v, sizeof(v)));
-    }
-    if (const char* ph = std::getenv("OD_PHASE")) {
-      const int v = std::atoi(ph);
-      OD_CU(cudaMemcpyToSymbol(g_phase, &v, sizeof(v)));
-    }
     OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
     int per_sm = 0;
     OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -1429,36 +1421,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
       last_kernel_ = OD_KERNEL_STEP_WS;
     } else {
       // interleaved tiles (column_step_grid)
-      static const int ring_exp = std::getenv("OD_RING") ? std::atoi(std::getenv("OD_RING")) : 0;
-      if (ring_exp == 16 || ring_exp == 166) {
-        // experiment: a 16-slot ring (S = 14 planes ahead; 166: S = 6 as control)
-        lc.dynamicSmemBytes = 16 * kPlaneMax * sizeof(double);
-        static bool attr = false;
-        if (!attr) {
-          OD_CU(cudaFuncSetAttribute(column_step_grid<14, true, 4, 16>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kPlaneMax * 8));
-          OD_CU(cudaFuncSetAttribute(column_step_grid<14, false, 4, 16>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kPlaneMax * 8));
-          OD_CU(cudaFuncSetAttribute(column_step_grid<6, true, 4, 16>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kPlaneMax * 8));
-          OD_CU(cudaFuncSetAttribute(column_step_grid<6, false, 4, 16>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kPlaneMax * 8));
-          attr = true;
-        }
-#define OD_RING_LAUNCH(SS)                                                                     \
-  if (timer)                                                                                   \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<SS, true, 4, 16>, chk, tl4, cfg_.nz,         \
-                             cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nsp,   \
-                             (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,   \
-                             nsend, stamp, waitp, pk, sd));                                     \
-  else                                                                                         \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<SS, false, 4, 16>, chk, tl4, cfg_.nz,        \
-                             cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nsp,   \
-                             (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,   \
-                             nsend, stamp, waitp, pk, sd));
-        if (ring_exp == 16) { OD_RING_LAUNCH(14) } else { OD_RING_LAUNCH(6) }
-#undef OD_RING_LAUNCH
-      } else if (timer)
+      if (timer)
         OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<kFusedPrefetch, true, kGridMinBlocks>,
                                  chk, tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
                                  cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
