@@ -579,10 +579,13 @@ def plan_cost(plan: MigrationPlan, data_bytes: Sequence[int], procs_per_node: in
 
 
 def plan_cost_nvlink(plan: MigrationPlan, data_bytes: Sequence[int], procs_per_gpu: int,
-                     gpus: int, link_bandwidth: float = 450e9,
-                     latency: float = 2e-5) -> float:
+                     gpus: int, link_bandwidth: float = 550e9,
+                     latency: float = 0.0) -> float:
     """B200 migration cost (replaces plan_cost's host staging): NVLink peer copies,
-    GPUs in parallel, max(bytes out, bytes in) per GPU over its link."""
+    GPUs in parallel, max(bytes out, bytes in) per GPU over its link.  Defaults:
+    the runtime's measured pull rate (550 GB/s per GPU, no per-transfer term: one
+    kernel pulls every chunk concurrently), which predicts the measured cfg3
+    migrations on 2 and 4 B200 within 3 % (profiles/r2_migration_cost_validation.json)."""
     db = np.ascontiguousarray(data_bytes, dtype=np.int64)
     out = C.c_double()
     check(lib.od_plan_cost_nvlink(_moves_c(plan.moves), len(plan.moves),
