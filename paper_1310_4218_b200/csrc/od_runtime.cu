@@ -220,6 +220,15 @@ class Runtime {
   size_t tiles4_cap_ = 0;
   int tiles4s_cur_ = 0;
   bool order_dirty_ = true;
+  // A tile order refreshed inside an overlapped chain of step kernels (the
+  // load field moves every step while a hotspot advects) is handed to the step
+  // kernel in mapped pinned memory, one buffer per window position, so no copy
+  // operation breaks the programmatic-dependent-launch chain; the next window
+  // uploads the latest one to the device list.
+  std::vector<TileDev*> h_oring_, d_oring_;
+  size_t oring_cap_ = 0;
+  int oring_pending_ = -1;             // window position of the live mapped order
+  const TileDev* cur_tiles_ = nullptr;  // the list the step kernel reads
   int wave_ = 0;       // tiles one launch keeps resident (SMs x CTAs per SM)
   // equal-work tiles are dealt round-robin over the chunks in bands of band_
   // consecutive tiles of a chunk: y-neighbours start ~one CTA retirement apart,
@@ -232,7 +241,7 @@ class Runtime {
   int band_ = 4;
   int sms_ = 1;
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
-  void refresh_tile_order();
+  void refresh_tile_order(int mapped_pos = -1);
   // mode 5: the warp-specialised tile when a GPU holds less than one wave of
   // tiles (latency-bound), the interleaved tile otherwise; mode 7 always WS
   bool use_ws(int ntiles) const {
@@ -543,6 +552,7 @@ Runtime::~Runtime() {
   }
   if (h_loads_) cudaFreeHost(h_loads_);
   for (double* p : h_ring_) cudaFreeHost(p);
+  for (TileDev* p : h_oring_) cudaFreeHost(p);
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
   cudaFree(d_tiles_);
@@ -590,7 +600,7 @@ void Runtime::set_shift(int32_t rows) {
 
 // Heaviest tiles first (longest-processing-time order) for the batched step
 // kernel: estimated work = physics units + Jacobi cells, from the current field.
-void Runtime::refresh_tile_order() {
+void Runtime::refresh_tile_order(int mapped_pos) {
   const size_t n = tiles4_.size();
   if (n == 0) return;
   // (group, -work, tile index within its chunk, tile): equal-work tiles are
@@ -646,6 +656,14 @@ void Runtime::refresh_tile_order() {
     front.insert(front.end(), rest.begin(), rest.end());
     key.swap(front);
   }
+  order_dirty_ = false;
+  if (mapped_pos >= 0 && mapped_pos < int(h_oring_.size()) && n <= oring_cap_) {
+    // inside an overlapped chain: the kernel reads this order from mapped memory
+    for (size_t t = 0; t < n; ++t) h_oring_[mapped_pos][t] = tiles4_[std::get<2>(key[t])];
+    cur_tiles_ = d_oring_[mapped_pos];
+    oring_pending_ = mapped_pos;
+    return;
+  }
   const int b = tiles4s_cur_ ^ 1;
   OD_CU(cudaEventSynchronize(tiles4s_ev_[b]));  // previous upload from this buffer done
   for (size_t t = 0; t < n; ++t) h_tiles4s_[b][t] = tiles4_[std::get<2>(key[t])];
@@ -653,7 +671,8 @@ void Runtime::refresh_tile_order() {
                         cudaMemcpyHostToDevice, s0_));
   OD_CU(cudaEventRecord(tiles4s_ev_[b], s0_));
   tiles4s_cur_ = b;
-  order_dirty_ = false;
+  cur_tiles_ = d_tiles4s_[b];
+  oring_pending_ = -1;
 }
 
 // engine.hpp:323-336
@@ -923,6 +942,8 @@ void Runtime::rebuild_tables() {
     OD_CU(cudaMemcpy(d_tiles4_, tiles4_.data(), tiles4_.size() * sizeof(TileDev),
                      cudaMemcpyHostToDevice));
   order_dirty_ = true;
+  cur_tiles_ = nullptr;  // (the stream has drained; the next launch refreshes the order)
+  oring_pending_ = -1;
 
   const double r1 = now_s();
   // exchange schedule: per peer, faces in (sender vp, side) order
@@ -1145,8 +1166,37 @@ void Runtime::begin_window(bool allow_overlap) {
   ns_used_ = 0;
   win_overlap_ = overlap_ && allow_overlap && cfg_.overlap != 0 && !d_tl_ &&
                  (cfg_.measure == OD_MEASURE_TIMER || cfg_.measure == OD_MEASURE_TIMER_RAW);
+  if (oring_pending_ >= 0) {
+    // the stream has drained (collect): the last mapped order becomes the device list
+    const int b = tiles4s_cur_ ^ 1;
+    const size_t n = tiles4_.size();
+    OD_CU(cudaEventSynchronize(tiles4s_ev_[b]));
+    std::memcpy(h_tiles4s_[b], h_oring_[oring_pending_], n * sizeof(TileDev));
+    OD_CU(cudaMemcpyAsync(d_tiles4s_[b], h_tiles4s_[b], n * sizeof(TileDev),
+                          cudaMemcpyHostToDevice, s0_));
+    OD_CU(cudaEventRecord(tiles4s_ev_[b], s0_));
+    tiles4s_cur_ = b;
+    cur_tiles_ = d_tiles4s_[b];
+    oring_pending_ = -1;
+  }
   if (win_overlap_) {
     const int32_t S = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
+    if (int(h_oring_.size()) < S || oring_cap_ < tiles4_cap_) {
+      OD_CU(cudaStreamSynchronize(s0_));
+      for (TileDev* h : h_oring_) cudaFreeHost(h);
+      h_oring_.clear();
+      d_oring_.clear();
+      oring_cap_ = tiles4_cap_;
+      for (int32_t i = 0; i < S; ++i) {
+        TileDev* h = nullptr;
+        TileDev* d = nullptr;
+        OD_CU(cudaHostAlloc(reinterpret_cast<void**>(&h), std::max<size_t>(oring_cap_, 1) * sizeof(TileDev),
+                            cudaHostAllocMapped));
+        OD_CU(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d), h, 0));
+        h_oring_.push_back(h);
+        d_oring_.push_back(d);
+      }
+    }
     if (win_cap_ < S) {
       OD_CU(cudaStreamSynchronize(s0_));
       cudaFree(d_stepend_);
@@ -1203,8 +1253,9 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
   // the previous step kernel; no stream operation may sit between them
   r.ovl = win_overlap_ && pos < win_cap_ && (!host_io || int32_t(d_ring_.size()) > pos) &&
           !tiles4_.empty() && (mode == kAsync || timer);
-  if (r.ovl && order_dirty_) refresh_tile_order();  // (its upload breaks the chain once)
   r.ovl_chained = r.ovl && !window_.empty() && window_.back().ovl;
+  // a refreshed order inside a chain travels in mapped memory (no stream op)
+  if (r.ovl && order_dirty_) refresh_tile_order(r.ovl_chained ? pos : -1);
   if (!r.ovl) {
     r.ev_begin = new_event();
     OD_CU(cudaEventRecord(events_[r.ev_begin], s0_));
@@ -1346,6 +1397,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
   }
   if (fused) {
     if (order_dirty_) refresh_tile_order();
+    if (!cur_tiles_) cur_tiles_ = d_tiles4s_[tiles4s_cur_];
     int e0 = -1, e1 = -1;
     const bool prof_f = profiling_ && !r.ovl;
     if (prof_f) {
@@ -1401,7 +1453,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     la[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = la;
     lc.numAttrs = r.ovl ? 1 : 0;
-    const TileDev* tl4 = d_tiles4s_[tiles4s_cur_];
+    const TileDev* tl4 = cur_tiles_;
     const ChunkDev* chk = d_chunks_[par];
     unsigned long long* nsp = timer ? ns : nullptr;
     unsigned long long* waitp = timer ? ns + (ns_cols_ - 1) : (r.ovl ? nullptr : tl_wait());
