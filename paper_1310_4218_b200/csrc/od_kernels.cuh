@@ -32,6 +32,10 @@ struct FaceDev {
   int64_t fs, ks, es;  // strides (elements) for field, level, position along the face
   const double* lo;    // the allocation the strip lies in: [lo, hi) (checked builds)
   const double* hi;
+  // TMA source of a top/bottom face row (full tiles): a chunk row map (tkind 0,
+  // coordinates (x, trow, plane)) or a received strip's map (tkind 1, (x, plane))
+  const void* tm;
+  int32_t trow, tkind;
 };
 
 struct ChunkDev {
@@ -42,6 +46,10 @@ struct ChunkDev {
   int64_t kstride;   // h * pitch
   int32_t w, h, pitch, x0, y0, vp, pad0, pad1;
   FaceDev face[4];
+  // TMA tensor maps of U^t for full tiles (null: the chunk has no full tile or
+  // TMA staging is off): box tw x th x 1 (main) and tw x 1 x 1 (row)
+  const void* tm_main;
+  const void* tm_row;
 };
 
 struct TileDev {
@@ -686,7 +694,7 @@ __device__ __forceinline__ int fast_calls(const ColumnState& s, int budget) {
 // most 408 doubles for every shape.
 // ---------------------------------------------------------------------------
 constexpr int kRingSlots = 8;
-constexpr int kPlaneMax = 408;  // (th + 2) * (tw + 4) over the four shapes
+constexpr int kPlaneMax = 416;  // >= (th + 2) * (tw + 4) over the four shapes; 128-byte multiple (TMA)
 constexpr int kRowWarps = 4;
 
 struct TileGeom {
@@ -1003,6 +1011,288 @@ __device__ __noinline__ void tile_step_partial(double* __restrict__ ring, const 
                                 chunk_ns, hw);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged full tile (mode 4/5 interleaved kernel, tiles that lie inside
+// their chunk).  Same tile shape, Jacobi arithmetic and physics interleave as
+// tile_step, but each (field, level) plane of the tile lands in shared memory
+// through the tensor memory accelerator: one elected thread issues, per
+// plane, a tw x th box of the chunk's own U^t plus the two halo rows (from
+// the chunk itself, the neighbour chunk's map, or the received strip's map),
+// all completing on the plane slot's "full" mbarrier with expect-tx; the
+// threads owning a row's first/last column pair copy the two x-halo cells
+// (8 B each, not a TMA box) with cp.async and arrive on the same barrier
+// (noinc).  Slot layout (doubles, 128-byte aligned regions):
+//   [top row: tw (>= 16)] [tile: th x tw] [bottom row: tw (>= 16)] [x-halo: th x 2]
+// The ring hand-off (slots refilled only after every thread has read them)
+// is tile_step's mbarrier phase per level pair.
+// ---------------------------------------------------------------------------
+constexpr int kTmaSlot = kPlaneMax;  // doubles per slot (>= 392, every shape's TMA layout)
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int x, int y, int z,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensormap_acquire(const void* tmap) {
+  asm volatile("fence.proxy.tensormap::generic.acquire.gpu [%0], 128;\n" ::"l"(tmap) : "memory");
+}
+
+template <int S, bool TIMED>
+__device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const TileDev tile,
+                                              const ChunkDev* __restrict__ chunks, int32_t nz,
+                                              int32_t F, const double* __restrict__ cfield,
+                                              int32_t nx, int32_t ny, int32_t shift,
+                                              int32_t n_inner,
+                                              unsigned long long* __restrict__ chunk_ns,
+                                              const HaloWait hw) {
+  constexpr int R = kRingSlots;
+  static_assert(S + 2 <= R && S >= 3, "prefetch depth");
+  __shared__ ShareAcct s_acct;
+  if (TIMED && threadIdx.x == 0 && threadIdx.y == 0) share_begin(s_acct, share_tag(tile));
+
+  const ChunkDev& c = chunks[tile.slot];
+  const TileGeom g = tile_geom(tile, threadIdx.y, threadIdx.x);
+  const int tw = g.tw, th = g.th;
+  const int lx = g.lx, ly = g.ly;
+  const int pitch = c.pitch;
+  const int64_t ks = c.kstride;
+  const int x = tile.tx0 + 2 * lx, y = tile.ty0 + ly;
+  const int64_t own = int64_t(y) * pitch + x;
+  const int tpr = tw >> 1;
+  const int levels = F * nz;
+
+  // slot layout
+  const int row_len = tw < 16 ? 16 : tw;
+  const int o_top = 0, o_main = row_len, o_bot = row_len + th * tw, o_xh = o_bot + row_len;
+  const int oc = o_main + ly * tw + 2 * lx;
+  const int o_ym = ly == 0 ? o_top + 2 * lx : oc - tw;
+  const int o_yp = ly == th - 1 ? o_bot + 2 * lx : oc + tw;
+  const int o_xl = lx == 0 ? o_xh + 2 * ly : oc - 1;
+  const int o_xr = lx == tpr - 1 ? o_xh + 2 * ly + 1 : oc + 2;
+
+  // x-halo duty: the row's first and last thread copy one cell each per plane
+  const double* px = nullptr;
+  int64_t xstep = 0;
+  int oxh = 0;
+  if (lx == 0 || lx == tpr - 1) {
+    const bool left = lx == 0;
+    const int xs = left ? tile.tx0 - 1 : tile.tx0 + tw;
+    oxh = o_xh + 2 * ly + (left ? 0 : 1);
+    if (xs >= 0 && xs < c.w) {
+      px = c.in + int64_t(y) * pitch + xs;
+      xstep = ks;
+    } else {
+      const FaceDev& fd = c.face[left ? kLeft : kRight];
+      px = fd.p + int64_t(y) * fd.es;
+      xstep = fd.ks;
+    }
+  }
+  // halo rows: sources resolved once (uniform over the CTA)
+  const FaceDev& ft = c.face[kTop];
+  const FaceDev& fb = c.face[kBottom];
+  const bool top_in = tile.ty0 > 0, bot_in = tile.ty0 + th < c.h;
+  const void* tm_top = top_in ? c.tm_row : ft.tm;
+  const void* tm_bot = bot_in ? c.tm_row : fb.tm;
+  const int top_y = top_in ? tile.ty0 - 1 : ft.trow;
+  const int bot_y = bot_in ? tile.ty0 + th : fb.trow;
+  const bool top_2d = !top_in && ft.tkind == 1, bot_2d = !bot_in && fb.tkind == 1;
+  const uint32_t tx_bytes = uint32_t((th + 2) * tw) * 8u;
+
+  __shared__ __align__(8) uint64_t s_full[R];
+  __shared__ uint64_t s_ring_bar;
+  const bool lead = threadIdx.x == 0 && threadIdx.y == 0;
+  if (lead) {
+    for (int i = 0; i < R; ++i) mbar_init(&s_full[i], 1 + 2 * th);
+    mbar_init(&s_ring_bar, blockDim.x * blockDim.y);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    tensormap_acquire(c.tm_main);
+    tensormap_acquire(c.tm_row);
+    tensormap_acquire(tm_top);
+    tensormap_acquire(tm_bot);
+  }
+
+  auto issue = [&](int L) {
+    if (L >= levels) return;
+    double* slot = ring + (L & (R - 1)) * kTmaSlot;
+    uint64_t* full = &s_full[L & (R - 1)];
+    if (lead) {
+      mbar_expect_tx(full, tx_bytes);
+      tma_load_3d(slot + o_main, c.tm_main, tile.tx0, tile.ty0, L, full);
+      if (top_2d) tma_load_2d(slot + o_top, tm_top, tile.tx0, L, full);
+      else tma_load_3d(slot + o_top, tm_top, tile.tx0, top_y, L, full);
+      if (bot_2d) tma_load_2d(slot + o_bot, tm_bot, tile.tx0, L, full);
+      else tma_load_3d(slot + o_bot, tm_bot, tile.tx0, bot_y, L, full);
+    }
+    if (px) {
+      cp_async8(slot + oxh, px);
+      cp_async_mbar_arrive_noinc(full);
+      px += xstep;
+    }
+  };
+  auto wait_plane = [&](int L) {
+    if (L < levels) mbar_wait(&s_full[L & (R - 1)], uint32_t((L / R) & 1));
+  };
+
+  ColumnState s0, s1;
+  physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
+  physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
+  int q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
+  q0 = (q0 + 7) & ~7;
+  int q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
+  q1 = (q1 + 7) & ~7;
+  int fast = 0;
+  auto physics = [&](int b0, int b1) {
+    if (fast > 0) {
+      double y0 = s0.y, y1 = s1.y;
+      const double e0 = s0.eb, e1 = s1.eb;
+      for (int j = 0; j < b0; j += 16) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const double u0 = __fma_rn(-y0, y0, y0);
+          const double u1 = __fma_rn(-y1, y1, y1);
+          y0 = __fma_rn(kR, u0, e0);
+          y1 = __fma_rn(kR, u1, e1);
+        }
+      }
+      s0.y = y0;
+      s1.y = y1;
+      s0.i += b0;
+      s1.i += b0;
+      --fast;
+      return;
+    }
+    if (b0 == b1 && s0.T == s1.T) {
+      physics_advance_pair(s0, s1, b0);
+      fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
+      return;
+    }
+    physics_advance(s0, b0);
+    physics_advance(s1, b1);
+    if (b0 == b1) fast = min(fast_calls(s0, b0), fast_calls(s1, b1));
+  };
+
+  double zm0 = 0.0, zm1 = 0.0;
+  double* pout = c.out + own;
+  auto level = [&](int L, int k) {
+    const double* pl = ring + (L & (R - 1)) * kTmaSlot;
+    const double2 uc = *reinterpret_cast<const double2*>(pl + oc);
+    const double xl = pl[o_xl], xr = pl[o_xr];
+    const double2 ym = *reinterpret_cast<const double2*>(pl + o_ym);
+    const double2 yp = *reinterpret_cast<const double2*>(pl + o_yp);
+    double2 zu = uc;
+    if (k + 1 < nz)
+      zu = *reinterpret_cast<const double2*>(ring + ((L + 1) & (R - 1)) * kTmaSlot + oc);
+    const double zd0 = k > 0 ? zm0 : uc.x, zd1 = k > 0 ? zm1 : uc.y;
+    const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                __dadd_rn(zd0, zu.x));
+    const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                __dadd_rn(zd1, zu.y));
+    double2 o;
+    o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+    o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+    __stcs(reinterpret_cast<double2*>(pout), o);
+    zm0 = uc.x;
+    zm1 = uc.y;
+    pout += ks;
+  };
+
+  if (hw.n > 0 || hw.ndeps > 0) {
+    // pre-roll the physics until the remote strips / neighbour tiles are there
+    const int64_t need = int64_t(max(s0.T, s1.T)) * (n_inner + 1);
+    int64_t done = 0;
+    bool lead_ready = false;
+    for (;;) {
+      if (lead) {
+        if (done >= need) {
+          if (TIMED) share_pause(s_acct, share_tag(tile));
+          const uint64_t w0 = globaltimer_ns();
+          wait_ready(hw, 20ull * 1000 * 1000 * 1000);
+          if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
+          if (TIMED) share_resume(s_acct, share_tag(tile));
+          lead_ready = true;
+        } else {
+          lead_ready = stamps_ready(hw);
+        }
+      }
+      if (__syncthreads_or(lead && lead_ready)) break;
+      physics(kPreroll, kPreroll);
+      done += kPreroll;
+    }
+    fast = 0;
+  }
+  // U^t and the received strips were written through the generic proxy (the
+  // previous step's tiles, the peers' pack CTAs) and acquired through the step
+  // stamps / halo flags; order those writes before this tile's TMA reads
+  if (lead) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  __syncthreads();  // barriers initialised (and the pre-roll's stamps acquired) before any TMA
+
+#pragma unroll
+  for (int L = 0; L < S; ++L) issue(L);
+  mbar_arrive(&s_ring_bar);
+
+  uint32_t parity = 0;
+  int k = 0, L = 0;
+  for (; L + 1 < levels; L += 2) {
+    mbar_wait(&s_ring_bar, parity);  // everyone has read planes <= L-1: their slots are free
+    parity ^= 1;
+    issue(L + S);
+    issue(L + S + 1);
+    wait_plane(L);
+    wait_plane(L + 1);
+    wait_plane(L + 2);
+    level(L, k);
+    if (++k == nz) k = 0;
+    level(L + 1, k);
+    if (++k == nz) k = 0;
+    od_jitter(4u + unsigned(L));
+    mbar_arrive(&s_ring_bar);
+    physics(2 * q0, 2 * q1);
+  }
+  if (L < levels) {
+    mbar_wait(&s_ring_bar, parity);
+    wait_plane(L);
+    level(L, k);
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  if (lead) {
+    for (int i = 0; i < R; ++i) mbar_inval(&s_full[i]);
+    mbar_inval(&s_ring_bar);
+  }
+  physics_advance(s0, 0x7fffffff);
+  physics_advance(s1, 0x7fffffff);
+
+  if (TIMED) {
+    unsigned long long ops = 2ull * nz * F * kJacobiOps;
+    ops += (unsigned long long)s0.T * trip_ops(n_inner);
+    ops += (unsigned long long)s1.T * trip_ops(n_inner);
+    charge_ops(chunk_ns, tile.slot, ops);
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0)
+      atomicAdd(&chunk_ns[2 * tile.slot], (unsigned long long)llrint(share_end(s_acct, share_tag(tile))));
+  }
+}
+
 __device__ __forceinline__ bool tile_full(const TileDev& t, const ChunkDev& c) {
   return t.tx0 + t.tw <= c.w && t.ty0 + t.th <= c.h;
 }
@@ -1164,8 +1454,8 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                      const PackArgs pk, const StepDeps sd) {
   // rings deeper than 8 slots exceed the 48 KB static limit: dynamic smem
-  __shared__ __align__(16) double ring_s[R <= 8 ? R * kPlaneMax : 2];
-  extern __shared__ __align__(16) double ring_d[];
+  __shared__ __align__(128) double ring_s[R <= 8 ? R * kPlaneMax : 2];
+  extern __shared__ __align__(128) double ring_d[];
   double* const ring = R <= 8 ? ring_s : ring_d;
   // cross-step overlap: let the next step's grid launch as soon as every CTA of
   // this one has started; its tiles wait on per-tile stamps, not on this grid
@@ -1180,7 +1470,9 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
   HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
               nullptr, nullptr, 0, 0};
   tile_deps(sd, self, hw);
-  if (tile_full(t, c))
+  if (tile_full(t, c) && c.tm_main && R == kRingSlots)
+    tile_step_tma<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
+  else if (tile_full(t, c))
     tile_step<S, TIMED, true, R>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
                                  hw);
   else

@@ -15,6 +15,8 @@
 // Neighbouring chunks on the same GPU read each other's boundary cells
 // directly through per-face descriptors, so there is no halo copy at all
 // inside a GPU; only faces that border another rank are packed and exchanged.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -270,6 +272,13 @@ class Runtime {
   mutable std::vector<int32_t> classes_;
   mutable uint64_t classes_gen_ = ~0ull;
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
+  // TMA tensor maps of the full tiles' planes, per parity and slot: [main box,
+  // own row, top-face row source, bottom-face row source] (OD_TMA=0: off)
+  bool tma_on_ = true;
+  PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_ = nullptr;
+  CUtensorMap* d_tmaps_ = nullptr;
+  size_t d_tmaps_cap_ = 0;
+  void build_tensor_maps(std::vector<ChunkDev>& tab, int par, const std::vector<int32_t>& slot_of);
   size_t d_chunks_cap_[2] = {0, 0};
   TileDev* d_tiles_ = nullptr;
   size_t d_tiles_cap_ = 0;
@@ -429,6 +438,15 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
+    tma_on_ = !(std::getenv("OD_TMA") && std::string(std::getenv("OD_TMA")) == "0");
+    if (tma_on_) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+              cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+        throw RuntimeFault("cuTensorMapEncodeTiled unavailable (set OD_TMA=0 to stage with cp.async)");
+      encode_tiled_ = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
     OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
     int per_sm = 0;
     OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -555,6 +573,7 @@ Runtime::~Runtime() {
   for (TileDev* p : h_oring_) cudaFreeHost(p);
   cudaFree(d_chunks_[0]);
   cudaFree(d_chunks_[1]);
+  cudaFree(d_tmaps_);
   cudaFree(d_tiles_);
   cudaFree(d_tiles4_);
   for (int b = 0; b < 2; ++b) {
@@ -1058,6 +1077,7 @@ void Runtime::rebuild_tables() {
         }
       }
     }
+    if (tma_on_) build_tensor_maps(tab, par, slot_of);
     upload(d_chunks_[par], d_chunks_cap_[par], tab);
   }
   if (!d_trips_ || ns_cols_ < 2 * nres + 1) {
@@ -1075,6 +1095,82 @@ void Runtime::rebuild_tables() {
   if (trace_on())
     fprintf(stderr, "[od rank %d] rebuild: tiles %.2f ms, exchange %.2f ms, chunk tables %.2f ms\n",
             rank_, (r1 - r0) * 1e3, (r2 - r1) * 1e3, (now_s() - r2) * 1e3);
+}
+
+// TMA maps for the full tiles of every resident chunk (parity par): the
+// chunk's U^t as a 3-D tensor {w, h, F*nz} (row stride pitch, plane stride
+// h*pitch) with a tw x th box and a tw x 1 box, and per top/bottom face the
+// tensor its halo row comes from with a tw x 1 box: the neighbour chunk on this
+// GPU (row h-1 above, 0 below), the chunk itself (zero-flux edge) or the
+// received strip (2-D {lenp, F*nz}).  A chunk without a full tile gets none
+// and its tiles keep the cp.async ring.
+void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
+                                const std::vector<int32_t>& slot_of) {
+  const int32_t nres = int32_t(tab.size());
+  const size_t need = size_t(2) * std::max(nres, 1) * 4;
+  if (need > d_tmaps_cap_) {
+    OD_CU(cudaStreamSynchronize(s0_));
+    cudaFree(d_tmaps_);
+    d_tmaps_cap_ = std::max(need, size_t(2) * std::max<size_t>(slab_slots_, 1) * 4);
+    OD_CU(cudaMalloc(&d_tmaps_, d_tmaps_cap_ * sizeof(CUtensorMap)));
+  }
+  std::vector<CUtensorMap> maps(size_t(nres) * 4);
+  const cuuint64_t planes = cuuint64_t(cfg_.nz) * cfg_.fields;
+  auto chunk_map = [&](CUtensorMap* out, const ChunkMem& m, int tw, int rows) {
+    const cuuint64_t dims[3] = {cuuint64_t(m.sub.w()), cuuint64_t(m.sub.h()), planes};
+    const cuuint64_t strides[2] = {cuuint64_t(m.pitch) * 8, cuuint64_t(m.kstride()) * 8};
+    const cuuint32_t box[3] = {cuuint32_t(tw), cuuint32_t(rows), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (encode_tiled_(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, m.u[par], dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      throw RuntimeFault("cuTensorMapEncodeTiled failed for a chunk");
+  };
+  CUtensorMap* dev = d_tmaps_ + size_t(par) * (d_tmaps_cap_ / 2);
+  for (int32_t i = 0; i < nres; ++i) {
+    ChunkDev& c = tab[i];
+    const ChunkMem& m = chunks_[resident_[i]];
+    const int tw = tile_width(c.w, c.h), th = 256 / tw;
+    c.tm_main = c.tm_row = nullptr;
+    if (c.w < tw || c.h < th) continue;  // no full tile
+    chunk_map(&maps[size_t(i) * 4 + 0], m, tw, th);
+    chunk_map(&maps[size_t(i) * 4 + 1], m, tw, 1);
+    for (int side = kTop; side <= kBottom; ++side) {
+      CUtensorMap* mp = &maps[size_t(i) * 4 + 2 + (side - kTop)];
+      FaceDev& f = c.face[side];
+      const int32_t n = nbr(m.vp, side);
+      if (n < 0) {  // zero-flux: the chunk's own edge row
+        chunk_map(mp, m, tw, 1);
+        f.trow = side == kTop ? 0 : c.h - 1;
+        f.tkind = 0;
+      } else if (rank_of_vp(n) == rank_) {
+        const ChunkMem& nm = chunks_[n];
+        chunk_map(mp, nm, tw, 1);
+        f.trow = side == kTop ? nm.sub.h() - 1 : 0;
+        f.tkind = 0;
+      } else {  // received strip [f][k][e], e along x
+        const cuuint64_t lenp = cuuint64_t((c.w + 1) & ~1);
+        const cuuint64_t dims[2] = {cuuint64_t(c.w), planes};
+        const cuuint64_t strides[1] = {lenp * 8};
+        const cuuint32_t box[2] = {cuuint32_t(tw), 1};
+        const cuuint32_t es[2] = {1, 1};
+        if (encode_tiled_(mp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(f.p), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          throw RuntimeFault("cuTensorMapEncodeTiled failed for a received strip");
+        f.trow = 0;
+        f.tkind = 1;
+      }
+      f.tm = dev + size_t(i) * 4 + 2 + (side - kTop);
+    }
+    c.tm_main = dev + size_t(i) * 4 + 0;
+    c.tm_row = dev + size_t(i) * 4 + 1;
+  }
+  (void)slot_of;
+  if (nres > 0)
+    OD_CU(cudaMemcpy(dev, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
 }
 
 // Worst case for this rank: every face of every chunk slot borders another GPU.
