@@ -1125,17 +1125,22 @@ __device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const T
     for (int i = 0; i < R; ++i) mbar_init(&s_full[i], 1 + 2 * th);
     mbar_init(&s_ring_bar, blockDim.x * blockDim.y);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x == 0) {  // the issuing lanes
     tensormap_acquire(c.tm_main);
     tensormap_acquire(c.tm_row);
     tensormap_acquire(tm_top);
     tensormap_acquire(tm_bot);
   }
 
+  // the issuing thread rotates over the four warps' first lanes, so no warp
+  // carries the TMA issue of every plane
+  const int wid = threadIdx.y;
   auto issue = [&](int L) {
     if (L >= levels) return;
     double* slot = ring + (L & (R - 1)) * kTmaSlot;
     uint64_t* full = &s_full[L & (R - 1)];
-    if (lead) {
+    if (threadIdx.x == 0 && wid == ((L >> 1) & (kRowWarps - 1))) {
       mbar_expect_tx(full, tx_bytes);
       tma_load_3d(slot + o_main, c.tm_main, tile.tx0, tile.ty0, L, full);
       if (top_2d) tma_load_2d(slot + o_top, tm_top, tile.tx0, L, full);
@@ -1243,7 +1248,8 @@ __device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const T
   // U^t and the received strips were written through the generic proxy (the
   // previous step's tiles, the peers' pack CTAs) and acquired through the step
   // stamps / halo flags; order those writes before this tile's TMA reads
-  if (lead) asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;\n" ::: "memory");
   __syncthreads();  // barriers initialised (and the pre-roll's stamps acquired) before any TMA
 
 #pragma unroll
@@ -1257,7 +1263,7 @@ __device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const T
     parity ^= 1;
     issue(L + S);
     issue(L + S + 1);
-    wait_plane(L);
+    if (L == 0) wait_plane(L);  // (later: plane L was waited for as L+2 one phase ago)
     wait_plane(L + 1);
     wait_plane(L + 2);
     level(L, k);

@@ -273,8 +273,12 @@ class Runtime {
   mutable uint64_t classes_gen_ = ~0ull;
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
   // TMA tensor maps of the full tiles' planes, per parity and slot: [main box,
-  // own row, top-face row source, bottom-face row source] (OD_TMA=0: off)
+  // own row, top-face row source, bottom-face row source].  Default: 64-wide
+  // tiles (cfg4/cfg5; measured on par with the cp.async ring at lower power);
+  // narrower tiles keep the cp.async ring (TMA measured 1.5 % slower at 32 x 8,
+  // profiles/r2_tma_vs_cpasync.json).  OD_TMA=0: off, OD_TMA=2: every width.
   bool tma_on_ = true;
+  int tma_min_width_ = 64;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_ = nullptr;
   CUtensorMap* d_tmaps_ = nullptr;
   size_t d_tmaps_cap_ = 0;
@@ -439,6 +443,7 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
     tma_on_ = !(std::getenv("OD_TMA") && std::string(std::getenv("OD_TMA")) == "0");
+    if (std::getenv("OD_TMA") && std::string(std::getenv("OD_TMA")) == "2") tma_min_width_ = 8;
     if (tma_on_) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q{};
@@ -1133,7 +1138,7 @@ void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
     const ChunkMem& m = chunks_[resident_[i]];
     const int tw = tile_width(c.w, c.h), th = 256 / tw;
     c.tm_main = c.tm_row = nullptr;
-    if (c.w < tw || c.h < th) continue;  // no full tile
+    if (c.w < tw || c.h < th || tw < tma_min_width_) continue;  // no full tile / cp.async width
     chunk_map(&maps[size_t(i) * 4 + 0], m, tw, th);
     chunk_map(&maps[size_t(i) * 4 + 1], m, tw, 1);
     for (int side = kTop; side <= kBottom; ++side) {

@@ -43,13 +43,15 @@ def test_fields_bitwise_1d_strips(overlap):
     assert_bitwise(A, Ao, "A")
 
 
-@pytest.mark.parametrize("mode", [4, 7])
+@pytest.mark.parametrize("mode,tma", [(4, "2"), (4, "0"), (7, "1")])
 @pytest.mark.parametrize("nx,kx,ny,ky", [(64, 8, 48, 2), (96, 6, 40, 2), (96, 3, 44, 2),
                                          (120, 3, 50, 2), (200, 2, 18, 2), (66, 6, 30, 5),
                                          (256, 4, 12, 1)])
-def test_fields_tile_widths(nx, kx, ny, ky, mode):
+def test_fields_tile_widths(nx, kx, ny, ky, mode, tma, monkeypatch):
     # chunk widths 8, 16, 32, 40, 100, 11, 64 select 8 x 32 / 16 x 16 / 32 x 8 /
-    # 64 x 4 tiles, full and partial in both directions
+    # 64 x 4 tiles, full and partial in both directions; full tiles staged by TMA
+    # at every width (OD_TMA=2) or by the cp.async ring (OD_TMA=0)
+    monkeypatch.setenv("OD_TMA", tma)
     cfg = small(nx=nx, ny=ny, nz=5, F=2, kx=kx, ky=ky, n_inner=9, overlap=mode, heavy=3.0)
     U, A, _ = device_fields(cfg, 3)
     Uo, Ao = oracle_fields(cfg, 3)

@@ -67,15 +67,18 @@ def test_cfg1_as_configured_with_balancing(mode):
     assert recs[0].imbalance_before > 1.05 and recs[0].plan.moves, recs[0]
 
 
-@pytest.mark.parametrize("mode", [4, 5, 7])
-def test_cfg4_geometry_slice(mode):
-    # 16 chunks x 16 full 64x4 tiles; mode 4 forces the interleaved tile,
-    # 5 picks the warp-specialised one here (less than a wave of tiles), 7 forces it
+@pytest.mark.parametrize("mode,tma", [(4, "1"), (4, "0"), (5, "1"), (7, "1")])
+def test_cfg4_geometry_slice(mode, tma, monkeypatch):
+    # 16 chunks x 16 full 64x4 tiles; mode 4 forces the interleaved tile (TMA-staged
+    # planes by default for 64-wide tiles, OD_TMA=0: the cp.async ring), 5 picks the
+    # warp-specialised one here (less than a wave of tiles), 7 forces it
+    monkeypatch.setenv("OD_TMA", tma)
     _check("cfg4s", cfg4_slice(mode), 10, use_epochs=True)
 
 
-@pytest.mark.parametrize("mode", [4, 7])
-def test_cfg3_geometry_slice_moving_hotspot_greedy(mode):
+@pytest.mark.parametrize("mode,tma", [(4, "1"), (4, "2"), (7, "1")])
+def test_cfg3_geometry_slice_moving_hotspot_greedy(mode, tma, monkeypatch):
+    monkeypatch.setenv("OD_TMA", tma)  # 2: TMA staging for the 32-wide tiles too
     # 64 chunks of 32x32 (full 32x8 tiles), the hotspot moves half the grid in
     # epoch 2 and GreedyLB rebalances every epoch
     recs = _check("cfg3s", cfg3_slice(mode), 20, use_epochs=True)

@@ -26,7 +26,10 @@ def ngpus():
                                              (5, "p2p", {"OD_OVERLAP": "0"}),
                                              (5, "p2p", {"OD_PACK_CTAS": "0"}),
                                              (5, "p2p", {"OD_LIB_VARIANT": "checked"}),
-                                             (4, "p2p", {"OD_LIB_VARIANT": "checked"})])
+                                             (4, "p2p", {"OD_LIB_VARIANT": "checked"}),
+                                             (4, "p2p", {"OD_TMA": "2"}),
+                                             (4, "p2p", {"OD_TMA": "2",
+                                                         "OD_LIB_VARIANT": "checked"})])
 def test_two_gpus_fields_and_plans(mode, halo, extra):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

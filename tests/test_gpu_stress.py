@@ -45,15 +45,16 @@ print(json.dumps(out))
 """
 
 
+@pytest.mark.parametrize("tma", ["1", "2"])
 @pytest.mark.parametrize("cases", [
     [(4, 2, 2, 128, 32), (4, 4, 4, 128, 64), (4, 8, 8, 64, 64)],   # 64x4 / 32x8 / 8x32 tiles
     [(7, 2, 2, 128, 32), (7, 4, 4, 128, 64), (5, 5, 3, 90, 40)],   # warp-specialised, partial
 ])
-def test_checked_build_stress_bitwise(cases):
+def test_checked_build_stress_bitwise(cases, tma):
     lib = os.path.join(ROOT, "paper_1310_4218_b200", "libod_b200_checked.so")
     if not os.path.exists(lib):
         pytest.fail("libod_b200_checked.so missing: build with make -C paper_1310_4218_b200/csrc")
-    env = dict(os.environ, OD_LIB_VARIANT="checked")
+    env = dict(os.environ, OD_LIB_VARIANT="checked", OD_TMA=tma)
     code = CHILD.format(root=ROOT, cases=cases)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
                        cwd=ROOT, timeout=900)
