@@ -9,7 +9,7 @@ timeout 900 $TR --master-port 29611 tools/migration_cost_check.py cfg3 \
 timeout 900 $TR --master-port 29612 tools/paper_presets.py expA expB expC cfg1 \
   > gpurun_out/paper_presets_n$N.log 2>&1; echo "presets rc=$?"
 if [ "${2:-}" = sweep ]; then
-  timeout 2400 $TR --master-port 29613 tools/sweep_cfg5.py 1,2,4,8,16,32 5,10,20,40 20 \
+  timeout 3000 $TR --master-port 29613 tools/sweep_cfg5.py 1,4,16,32 5,10,20,40 80 \
     > gpurun_out/cfg5_sweep_n$N.jsonl 2> gpurun_out/cfg5_sweep_n$N.err; echo "sweep rc=$?"
 fi
 echo campaign done
