@@ -3,7 +3,7 @@ vs problem size on one GPU, all columns heavy (C=2), for the kernel modes."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1310_4218_b200 as od
-modes = [int(m) for m in sys.argv[1].split(",")] if len(sys.argv) > 1 else [4, 5, 6]
+modes = [int(m) for m in sys.argv[1].split(",")] if len(sys.argv) > 1 else [4, 7]
 for ny in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["64","128","256","384","512","768","1024"])]:
     row = {"columns": 1024 * ny}
     for mode in modes:
