@@ -273,11 +273,13 @@ class Runtime {
   mutable uint64_t classes_gen_ = ~0ull;
   ChunkDev* d_chunks_[2] = {nullptr, nullptr};
   // TMA tensor maps of the full tiles' planes, per parity and slot: [main box,
-  // own row, top-face row source, bottom-face row source].  Default: 64-wide
-  // tiles (cfg4/cfg5; measured on par with the cp.async ring at lower power);
-  // narrower tiles keep the cp.async ring (TMA measured 1.5 % slower at 32 x 8,
-  // profiles/r2_tma_vs_cpasync.json).  OD_TMA=0: off, OD_TMA=2: every width.
-  bool tma_on_ = true;
+  // own row, top-face row source, bottom-face row source].  Opt-in: OD_TMA=1
+  // stages 64-wide full tiles through TMA, OD_TMA=2 every width.  Default off:
+  // at cfg4 the TMA-staged kernel reads 10 % more DRAM (L2 hit rate 12.5 % vs
+  // 43 %, independent of the L2 promotion) and takes 3.8 % more cycles than the
+  // cp.async ring; at free clocks it runs at higher SM clocks for the same step
+  // time (profiles/r2_tma_vs_cpasync.json).  OD_TMA_L2: promotion experiment.
+  bool tma_on_ = false;
   int tma_min_width_ = 64;
   PFN_cuTensorMapEncodeTiled_v12000 encode_tiled_ = nullptr;
   CUtensorMap* d_tmaps_ = nullptr;
@@ -442,14 +444,16 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
-    tma_on_ = !(std::getenv("OD_TMA") && std::string(std::getenv("OD_TMA")) == "0");
-    if (std::getenv("OD_TMA") && std::string(std::getenv("OD_TMA")) == "2") tma_min_width_ = 8;
+    if (const char* t = std::getenv("OD_TMA")) {
+      tma_on_ = std::atoi(t) > 0;
+      if (std::atoi(t) == 2) tma_min_width_ = 8;
+    }
     if (tma_on_) {
       void* fn = nullptr;
       cudaDriverEntryPointQueryResult q{};
       if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
               cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
-        throw RuntimeFault("cuTensorMapEncodeTiled unavailable (set OD_TMA=0 to stage with cp.async)");
+        throw RuntimeFault("cuTensorMapEncodeTiled unavailable (unset OD_TMA to stage with cp.async)");
       encode_tiled_ = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
     OD_CU(cudaMalloc(&d_counter_, 4 * sizeof(unsigned int)));  // [tiles, pack next, pack done]
@@ -1120,6 +1124,11 @@ void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
     OD_CU(cudaMalloc(&d_tmaps_, d_tmaps_cap_ * sizeof(CUtensorMap)));
   }
   std::vector<CUtensorMap> maps(size_t(nres) * 4);
+  static const int promo_env = std::getenv("OD_TMA_L2") ? std::atoi(std::getenv("OD_TMA_L2")) : 128;
+  const CUtensorMapL2promotion promo = promo_env == 0     ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : promo_env == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : promo_env == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
   const cuuint64_t planes = cuuint64_t(cfg_.nz) * cfg_.fields;
   auto chunk_map = [&](CUtensorMap* out, const ChunkMem& m, int tw, int rows) {
     const cuuint64_t dims[3] = {cuuint64_t(m.sub.w()), cuuint64_t(m.sub.h()), planes};
@@ -1127,8 +1136,7 @@ void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
     const cuuint32_t box[3] = {cuuint32_t(tw), cuuint32_t(rows), 1};
     const cuuint32_t es[3] = {1, 1, 1};
     if (encode_tiled_(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, m.u[par], dims, strides, box, es,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       throw RuntimeFault("cuTensorMapEncodeTiled failed for a chunk");
   };
@@ -1162,7 +1170,7 @@ void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
         const cuuint32_t es[2] = {1, 1};
         if (encode_tiled_(mp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(f.p), dims,
                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, promo,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
           throw RuntimeFault("cuTensorMapEncodeTiled failed for a received strip");
         f.trow = 0;

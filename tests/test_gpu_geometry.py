@@ -69,8 +69,8 @@ def test_cfg1_as_configured_with_balancing(mode):
 
 @pytest.mark.parametrize("mode,tma", [(4, "1"), (4, "0"), (5, "1"), (7, "1")])
 def test_cfg4_geometry_slice(mode, tma, monkeypatch):
-    # 16 chunks x 16 full 64x4 tiles; mode 4 forces the interleaved tile (TMA-staged
-    # planes by default for 64-wide tiles, OD_TMA=0: the cp.async ring), 5 picks the
+    # 16 chunks x 16 full 64x4 tiles; mode 4 forces the interleaved tile (planes
+    # staged by the cp.async ring by default, OD_TMA=1: by TMA), 5 picks the
     # warp-specialised one here (less than a wave of tiles), 7 forces it
     monkeypatch.setenv("OD_TMA", tma)
     _check("cfg4s", cfg4_slice(mode), 10, use_epochs=True)
