@@ -158,7 +158,7 @@ class Runtime {
   int new_event();
   void begin_window(bool allow_overlap = true);
   void launch_step(int32_t mode, int32_t epoch_step, bool host_io,
-                   const double* host_field = nullptr);
+                   const double* host_field = nullptr, int staged_slot = -1);
   // waits for the window, gathers per-step walls and the K x S sample matrix
   void collect(std::vector<double>& walls, std::vector<double>& samples);
   struct EpochOut {
@@ -1342,7 +1342,7 @@ void Runtime::begin_window(bool allow_overlap) {
 }
 
 void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
-                          const double* host_field) {
+                          const double* host_field, int staged_slot) {
   const auto t0 = std::chrono::steady_clock::now();
   StepRec r;
   r.mode = mode;
@@ -1360,7 +1360,8 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
                                                     cfg_.measure == OD_MEASURE_OPS));
   // overlapped step: launched with programmatic dependent launch right behind
   // the previous step kernel; no stream operation may sit between them
-  r.ovl = win_overlap_ && pos < win_cap_ && (!host_io || int32_t(d_ring_.size()) > pos) &&
+  r.ovl = win_overlap_ && pos < win_cap_ &&
+          (!host_io || staged_slot >= 0 || int32_t(d_ring_.size()) > pos) &&
           !tiles4_.empty() && (mode == kAsync || timer);
   r.ovl_chained = r.ovl && !window_.empty() && window_.back().ovl;
   // a refreshed order inside a chain travels in mapped memory (no stream op)
@@ -1380,7 +1381,11 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
   // buffer (or, without one, the runtime's own shifted field, which the
   // reference keeps on the host: engine.hpp:337-342)
   const double* hsrc = host_field ? host_field : field_.c.data();
-  if (host_io && r.ovl) {
+  if (host_io && r.ovl && staged_slot >= 0) {
+    // the caller's field for this step was staged while the previous step ran
+    cfield = d_ring_[staged_slot];
+    shift = 0;
+  } else if (host_io && r.ovl) {
     // overlapped: the step kernel reads this step's mapped pinned copy over the
     // host link (8 B per column per step, no copy operation between the kernels)
     std::memcpy(h_ring_[pos], hsrc, field_.c.size() * sizeof(double));
@@ -1967,7 +1972,11 @@ void Runtime::advance(int32_t n, int32_t* epochs_done) {
 void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, double* host_loads) {
   if (n < 0) throw ValidationError("negative step count");
   const size_t cells = size_t(cfg_.nx) * cfg_.ny;
-  const int32_t Sw = std::max(cfg_.async_steps + cfg_.sync_steps, 1);
+  // one mapped slot per window position + 1: a caller's field is staged into
+  // slot (global step % (S + 1)) while the previous step runs, so no slot is
+  // rewritten while a step kernel that may still be in flight reads it (the
+  // host runs at most one epoch ahead: epoch ends drain the stream)
+  const int32_t Sw = std::max(cfg_.async_steps + cfg_.sync_steps, 1) + 1;
   if (int32_t(h_ring_.size()) < Sw) {
     OD_CU(cudaStreamSynchronize(s0_));
     while (int32_t(h_ring_.size()) < Sw) {
@@ -2000,23 +2009,46 @@ void Runtime::advance_host(int32_t n, const double* host_c, int32_t n_fields, do
   // steps are launched back to back; the per-step loads land in pinned rows
   // and are read once the stream has drained (epoch ends drain it anyway)
   std::vector<std::vector<int32_t>> step_vps(host_loads ? n : 0);
+  const bool caller = host_c && n_fields > 0;
+  auto field_of = [&](int32_t i) { return host_c + size_t(std::min(i, n_fields - 1)) * cells; };
+  const size_t ring_n = h_ring_.size();
+  // staging of caller fields, one step ahead: the copy into the mapped slot and
+  // the change test (for the tile order) run while the GPU works on the
+  // previous step -- also across epoch ends, where the stream drains
+  std::vector<char> changed(caller ? n : 0, 0);
+  const size_t base_g = size_t(global_step_);  // step i is global step base_g + i
+  auto stage = [&](int32_t i) {
+    const double* f = field_of(i);
+    std::memcpy(h_ring_[(base_g + size_t(i)) % ring_n], f, cells * sizeof(double));
+    if (i == 0)
+      changed[i] = std::memcmp(field_.c.data(), f, cells * sizeof(double)) != 0;
+    else
+      changed[i] = f != field_of(i - 1) &&
+                   std::memcmp(field_of(i - 1), f, cells * sizeof(double)) != 0;
+  };
+  if (caller && n > 0) stage(0);
   for (int32_t i = 0; i < n; ++i) {
     if (cur_step_ == 0) begin_window();
-    advance_advection(cur_epoch_, cur_step_);
+    const uint64_t gen0 = field_gen_;
+    advance_advection(cur_epoch_, cur_step_);  // (may reset field_ to the runtime's own)
+    const bool reset = field_gen_ != gen0;
     h_loads_dst_ = h_loads_ + size_t(i) * row_words;
     d_loads_dst_ = d_loads_map_ + size_t(i) * row_words;
     const double* hf = nullptr;
-    if (host_c && n_fields > 0) {
+    int slot = -1;
+    if (caller) {
       // the caller's field for this step drives the kernel; the host-side copy
       // of it orders the tiles (heaviest first) when it differs from the last
-      hf = host_c + size_t(std::min(i, n_fields - 1)) * cells;
-      if (std::memcmp(field_.c.data(), hf, cells * sizeof(double)) != 0) {
+      hf = field_of(i);
+      slot = int((base_g + size_t(i)) % ring_n);
+      if (changed[i] || reset) {
         field_.c.assign(hf, hf + cells);
         ++field_gen_;
         order_dirty_ = true;
       }
     }
-    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true, hf);
+    launch_step(cur_step_ < cfg_.async_steps ? kAsync : kSync, cur_step_, true, hf, slot);
+    if (caller && i + 1 < n) stage(i + 1);
     if (host_loads) step_vps[i] = window_.back().slot_vps;
     ++global_step_;
     if (++cur_step_ == S) {
