@@ -1574,20 +1574,16 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     if (use_ws(nt)) {
       // warp-specialised tiles (column_step_ws): physics and Jacobi warps
       lc.blockDim = dim3(32, 2 * kRowWarps);
-      static const int ws_minb = std::getenv("OD_WS_MINB") ? std::atoi(std::getenv("OD_WS_MINB")) : 3;
-#define OD_WS_LAUNCH(MB)                                                                       \
-  if (timer)                                                                                   \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, MB>, chk, tl4, cfg_.nz,  \
-                             cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nsp,   \
-                             (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,   \
-                             nsend, stamp, waitp, pk, sd));                                     \
-  else                                                                                         \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, MB>, chk, tl4, cfg_.nz, \
-                             cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nsp,   \
-                             (const unsigned long long*)d_flags_, (const int32_t*)d_senders_,   \
-                             nsend, stamp, waitp, pk, sd));
-      if (ws_minb == 4) { OD_WS_LAUNCH(4) } else { OD_WS_LAUNCH(kWsMinBlocks) }
-#undef OD_WS_LAUNCH
+      if (timer)
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      else
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
       last_kernel_ = OD_KERNEL_STEP_WS;
     } else {
       // interleaved tiles (column_step_grid)
