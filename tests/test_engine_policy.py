@@ -91,3 +91,17 @@ def test_runtime_needs_a_processor_per_gpu():
     # input error (raised before any device or NCCL work)
     with pytest.raises(od.ValidationError, match="world"):
         od.Engine(configs.cfg2(), rank=0, world=2, nccl_id=bytes(128))  # 1 processor
+
+
+def test_runtime_capacity_below_initial_chunks_is_rejected():
+    # capacity_mib (B200 extension): a per-GPU cap below the chunks a GPU holds
+    # from the start is an input error, raised before any device work
+    with pytest.raises(od.ValidationError, match="capacity"):
+        od.Engine(configs.cfg2(capacity_mib=1))
+    with pytest.raises(od.ValidationError, match="capacity"):
+        od.Engine(configs.cfg2(capacity_mib=-5))
+
+
+def test_capacity_round_trips_through_json_config():
+    c = configs.cfg4(capacity_mib=90000)
+    assert od.config_from_json(od.config_to_json(c)).capacity_mib == 90000
