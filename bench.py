@@ -485,12 +485,18 @@ def main():
         loads = np.zeros((args.steps, K))
         field = np.ascontiguousarray(eng.load_field().as_array())
         eng.advance_host(1, field, loads[:1])
+        he0 = len(eng.epoch_history())
         ms_e2e = timed(lambda: eng.advance_host(args.steps, field, loads))
+        e2e_epochs = [{k: (round(v, 6) if isinstance(v, float) else v) for k, v in h.items()
+                       if k in ("epoch", "n_moves", "imbalance_before", "imbalance_after",
+                                "compute_total", "migration_seconds")}
+                      for h in eng.epoch_history()[he0:]]
         e2e = {"value": cols * args.steps / (ms_e2e * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": cols * 8,
                "d2h_bytes_per_step": int(st1["resident_chunks"]) * 16,
                "path": "od_rt_advance_host: the caller's (ny, nx) float64 load field is read "
-                       "from host memory every step, per-chunk loads written back every step"}
+                       "from host memory every step, per-chunk loads written back every step",
+               "epochs": e2e_epochs}
     eng.close()
     del eng
 
