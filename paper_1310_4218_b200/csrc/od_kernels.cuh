@@ -1140,7 +1140,7 @@ __device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const T
     if (L >= levels) return;
     double* slot = ring + (L & (R - 1)) * kTmaSlot;
     uint64_t* full = &s_full[L & (R - 1)];
-    if (threadIdx.x == 0 && wid == int((L >> 1) % blockDim.y)) {
+    if (threadIdx.x == 0 && wid == ((L >> 1) & (kRowWarps - 1))) {
       mbar_expect_tx(full, tx_bytes);
       tma_load_3d(slot + o_main, c.tm_main, tile.tx0, tile.ty0, L, full);
       if (top_2d) tma_load_2d(slot + o_top, tm_top, tile.tx0, L, full);
@@ -1493,7 +1493,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
 // back, no ring, no barrier) while warps 4..7 stream the Jacobi planes of the
 // same rows.  A tile lasts max(physics, Jacobi) instead of their sum, which is
 // what counts when the GPU holds few tiles (latency-bound sizes).
-template <int S, bool TIMED, bool FULL, int RW>
+template <int S, bool TIMED, bool FULL>
 __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const TileDev tile,
                                              const ChunkDev* __restrict__ chunks, int32_t nz,
                                              int32_t F, const double* __restrict__ cfield,
@@ -1506,14 +1506,14 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   __shared__ ShareAcct s_acct;
   __shared__ int s_phys_left;  // physics warps still running (TIMED: pause when idle)
   if (threadIdx.x == 0 && threadIdx.y == 0) {
-    s_phys_left = RW;
+    s_phys_left = kRowWarps;
     if (TIMED) share_begin(s_acct, share_tag(tile));
   }
 
   const ChunkDev& c = chunks[tile.slot];
   // warp roles: threadIdx.y < 4 physics, >= 4 Jacobi, both over row warp y % 4
-  const bool phys = threadIdx.y < RW;
-  const TileGeom g = tile_geom(tile, threadIdx.y % RW, threadIdx.x);
+  const bool phys = threadIdx.y < kRowWarps;
+  const TileGeom g = tile_geom(tile, threadIdx.y % kRowWarps, threadIdx.x);
   const int PW = g.pw;
   const int lx = g.lx, ly = g.ly;
   const int w = c.w, h = c.h, pitch = c.pitch;
@@ -1645,8 +1645,8 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   };
 
   __shared__ uint64_t s_ring_bar;
-  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == RW;  // first Jacobi thread
-  if (bar_lead) mbar_init(&s_ring_bar, 32 * RW);
+  const bool bar_lead = threadIdx.x == 0 && threadIdx.y == kRowWarps;  // first Jacobi thread
+  if (bar_lead) mbar_init(&s_ring_bar, 32 * kRowWarps);
   __syncthreads();
   if (phys) {
     // physics warps: both chains to the end, nothing else
@@ -1677,7 +1677,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
         if (TIMED && paused) share_resume(s_acct, share_tag(tile));
         if (hw.wait_ns) atomicMax(hw.wait_ns, (unsigned long long)(globaltimer_ns() - w0));
       }
-      asm volatile("bar.sync 1, %0;" ::"r"(32 * RW) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kRowWarps) : "memory");
     }
 #pragma unroll
     for (int L = 0; L < S; ++L) issue(L);
@@ -1722,7 +1722,7 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
   }
 }
 
-template <int S, bool TIMED, int RW>
+template <int S, bool TIMED>
 __device__ __noinline__ void tile_step_ws_partial(double* __restrict__ ring, const TileDev tile,
                                                   const ChunkDev* __restrict__ chunks, int32_t nz,
                                                   int32_t F, const double* __restrict__ cfield,
@@ -1730,12 +1730,12 @@ __device__ __noinline__ void tile_step_ws_partial(double* __restrict__ ring, con
                                                   int32_t n_inner,
                                                   unsigned long long* __restrict__ chunk_ns,
                                                   const HaloWait hw) {
-  tile_step_ws<S, TIMED, false, RW>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                    chunk_ns, hw);
+  tile_step_ws<S, TIMED, false>(ring, tile, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                chunk_ns, hw);
 }
 
-template <int S, bool TIMED, int MINB, int RW = kRowWarps>
-__global__ void __launch_bounds__(64 * RW, MINB)
+template <int S, bool TIMED, int MINB>
+__global__ void __launch_bounds__(64 * kRowWarps, MINB)
     column_step_ws(const ChunkDev* __restrict__ chunks, const TileDev* __restrict__ tiles,
                    int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
                    int32_t ny, int32_t shift, int32_t n_inner,
@@ -1757,11 +1757,11 @@ __global__ void __launch_bounds__(64 * RW, MINB)
               nullptr, nullptr, 0, 0};
   tile_deps(sd, self, hw);
   if (tile_full(t, c))
-    tile_step_ws<S, TIMED, true, RW>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                     chunk_ns, hw);
+    tile_step_ws<S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
+                                 hw);
   else
-    tile_step_ws_partial<S, TIMED, RW>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
-                                       chunk_ns, hw);
+    tile_step_ws_partial<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner,
+                                   chunk_ns, hw);
   tile_publish(sd, self, chunk_ns);
 }
 

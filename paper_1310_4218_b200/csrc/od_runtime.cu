@@ -245,13 +245,10 @@ class Runtime {
   int pack_ctas_ = 0;  // CTAs of the step kernel that pack P2P halos (0: separate kernel)
   void refresh_tile_order(int mapped_pos = -1);
   // mode 5: the warp-specialised tile when a GPU holds less than one wave of
-  // 4-row-warp tiles (latency-bound), the interleaved tile otherwise; mode 7
-  // always WS.  Decided per tile set (rebuild_tables).  rows_: row warps per
-  // tile (4; OD_WS_ROWS=2 halves the warp-specialised tiles: twice the tiles,
-  // 6 CTAs/SM, finer balance over the SMs in the latency-bound regime)
-  bool ws_ = false;
-  int rows_ = kRowWarps;
-  int ws_rows_env_ = kRowWarps;
+  // tiles (latency-bound), the interleaved tile otherwise; mode 7 always WS
+  bool use_ws(int ntiles) const {
+    return cfg_.overlap == 7 || (cfg_.overlap == 5 && ntiles < wave_);
+  }
   int32_t last_kernel_ = 0;  // OD_KERNEL_* of the last step kernel launched
   // cross-step overlap of the mode-5 step kernels (PDL + per-tile stamps;
   // OD_OVERLAP=0 disables): tile -> same-GPU tiles whose cells it reads (itself first),
@@ -447,7 +444,6 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     // a separate pack kernel ahead of the step kernel)
     pack_ctas_ = std::getenv("OD_PACK_CTAS") ? std::atoi(std::getenv("OD_PACK_CTAS")) : sms;
     if (const char* b = std::getenv("OD_TILE_BAND")) band_ = std::max(1, std::atoi(b));
-    if (const char* wr = std::getenv("OD_WS_ROWS")) ws_rows_env_ = std::atoi(wr) == 2 ? 2 : kRowWarps;
     if (const char* t = std::getenv("OD_TMA")) {
       tma_on_ = std::atoi(t) > 0;
       if (std::atoi(t) == 2) tma_min_width_ = 8;
@@ -926,17 +922,6 @@ void Runtime::rebuild_tables() {
   }
   ntiles_ = int32_t(tiles.size());
   upload(d_tiles_, d_tiles_cap_, tiles);
-  {
-    // the step kernel for this tile set (tile counts at four row warps)
-    size_t nt4 = 0;
-    for (int32_t i = 0; i < nres; ++i) {
-      const Sub& s = subs_[resident_[i]];
-      const int32_t tw = tile_width(s.w(), s.h()), th = 256 / tw;
-      nt4 += size_t((s.h() + th - 1) / th) * size_t((s.w() + tw - 1) / tw);
-    }
-    ws_ = cfg_.overlap == 7 || (cfg_.overlap == 5 && nt4 < size_t(wave_));
-    rows_ = ws_ ? ws_rows_env_ : kRowWarps;
-  }
   tiles4_.clear();
   tile4_begin_.assign(nres, 0);
   tile4_count_.assign(nres, 0);
@@ -949,7 +934,7 @@ void Runtime::rebuild_tables() {
       const int32_t n = nbr(v, d);
       remote[d] = n >= 0 && rank_of_vp(n) != rank_;
     }
-    const int32_t tw = tile_width(s.w(), s.h()), th = rows_ * 64 / tw;
+    const int32_t tw = tile_width(s.w(), s.h()), th = 256 / tw;
     const int32_t lg = tw == 64 ? 5 : tw == 32 ? 4 : tw == 16 ? 3 : 2;
     for (int32_t ty = 0; ty < s.h(); ty += th)
       for (int32_t tx = 0; tx < s.w(); tx += tw) {
@@ -969,8 +954,8 @@ void Runtime::rebuild_tables() {
       if (h_tiles4s_[b]) cudaFreeHost(h_tiles4s_[b]);
     }
     size_t all = 0;
-    for (const Sub& sb : subs_) {  // (at the smallest tile height a tile set can use)
-      const int32_t tw = tile_width(sb.w(), sb.h()), th = 128 / tw;
+    for (const Sub& sb : subs_) {
+      const int32_t tw = tile_width(sb.w(), sb.h()), th = 256 / tw;
       all += size_t((sb.h() + th - 1) / th) * size_t((sb.w() + tw - 1) / tw);
     }
     tiles4_cap_ = std::max<size_t>({tiles4_.size(), all, 16});
@@ -1159,7 +1144,7 @@ void Runtime::build_tensor_maps(std::vector<ChunkDev>& tab, int par,
   for (int32_t i = 0; i < nres; ++i) {
     ChunkDev& c = tab[i];
     const ChunkMem& m = chunks_[resident_[i]];
-    const int tw = tile_width(c.w, c.h), th = rows_ * 64 / tw;
+    const int tw = tile_width(c.w, c.h), th = 256 / tw;
     c.tm_main = c.tm_row = nullptr;
     if (c.w < tw || c.h < th || tw < tma_min_width_) continue;  // no full tile / cp.async width
     chunk_map(&maps[size_t(i) * 4 + 0], m, tw, th);
@@ -1575,7 +1560,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     // while the previous step's last tiles drain (tiles wait on per-tile stamps)
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(unsigned(nt + pk.ctas));
-    lc.blockDim = dim3(32, rows_);
+    lc.blockDim = dim3(32, kRowWarps);
     lc.stream = s0_;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1586,23 +1571,19 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     const ChunkDev* chk = d_chunks_[par];
     unsigned long long* nsp = timer ? ns : nullptr;
     unsigned long long* waitp = timer ? ns + (ns_cols_ - 1) : (r.ovl ? nullptr : tl_wait());
-    (void)nt;
-    if (ws_) {
+    if (use_ws(nt)) {
       // warp-specialised tiles (column_step_ws): physics and Jacobi warps
-      lc.blockDim = dim3(32, 2 * rows_);
-#define OD_WS_LAUNCH(MB, RWS)                                                                   \
-  if (timer)                                                                                    \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, MB, RWS>, chk, tl4,       \
-                             cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, \
-                             nsp, (const unsigned long long*)d_flags_,                           \
-                             (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));          \
-  else                                                                                          \
-    OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, MB, RWS>, chk, tl4,      \
-                             cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift, cfg_.n_inner, \
-                             nsp, (const unsigned long long*)d_flags_,                           \
-                             (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
-      if (rows_ == 2) { OD_WS_LAUNCH(2 * kWsMinBlocks, 2) } else { OD_WS_LAUNCH(kWsMinBlocks, kRowWarps) }
-#undef OD_WS_LAUNCH
+      lc.blockDim = dim3(32, 2 * kRowWarps);
+      if (timer)
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+      else
+        OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, kWsMinBlocks>, chk,
+                                 tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
+                                 cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
+                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
       last_kernel_ = OD_KERNEL_STEP_WS;
     } else {
       // interleaved tiles (column_step_grid)
@@ -1674,7 +1655,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
       if (cfg_.overlap != 0) {
         // the chunk's tiles through the interleaved tile kernel (no overlap, no pack)
         column_step_grid<kFusedPrefetch, false, kGridMinBlocks>
-            <<<tile4_count_[i], dim3(32, rows_), 0, s0_>>>(
+            <<<tile4_count_[i], dim3(32, kRowWarps), 0, s0_>>>(
                 d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield,
                 cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, 0, 0ull,
                 nullptr, PackArgs{}, StepDeps{});
