@@ -610,7 +610,7 @@ __device__ __forceinline__ void physics_advance(ColumnState& s, int budget) {
     const int m = min(budget, s.n_inner + 1 - s.i);
     double y = s.y;
     const double eb = s.eb;
-#pragma unroll 4
+#pragma unroll 16
     for (int j = 0; j < m; ++j) {
       const double u = __fma_rn(-y, y, y);
       y = __fma_rn(kR, u, eb);
@@ -653,7 +653,7 @@ __device__ __forceinline__ void physics_advance_pair(ColumnState& s0, ColumnStat
     const int m = min(budget, s0.n_inner + 1 - s0.i);
     double y0 = s0.y, y1 = s1.y;
     const double e0 = s0.eb, e1 = s1.eb;
-#pragma unroll 4
+#pragma unroll 16
     for (int j = 0; j < m; ++j) {
       const double u0 = __fma_rn(-y0, y0, y0);
       const double u1 = __fma_rn(-y1, y1, y1);
@@ -835,22 +835,22 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   if (ncell >= 1) {
     physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
     q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
-    q0 = (q0 + 7) & ~7;
+    q0 = (q0 + 15) & ~15;
   }
   if (ncell == 2) {
     physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
     q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
-    q1 = (q1 + 7) & ~7;
+    q1 = (q1 + 15) & ~15;
   }
   int fast = 0;  // interleaved iterations left before a trip boundary
   auto physics = [&](int b0, int b1) {
     if (fast > 0) {
       double y0 = s0.y, y1 = s1.y;
       const double e0 = s0.eb, e1 = s1.eb;
-      // b0 is a multiple of 16 (quota rounded to 8, two levels per call)
-      for (int j = 0; j < b0; j += 16) {
+      // b0 is a multiple of 32 (quota rounded to 16, two levels per call)
+      for (int j = 0; j < b0; j += 32) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < 32; ++q) {
           const double u0 = __fma_rn(-y0, y0, y0);
           const double u1 = __fma_rn(-y1, y1, y1);
           y0 = __fma_rn(kR, u0, e0);
@@ -1162,17 +1162,17 @@ __device__ __forceinline__ void tile_step_tma(double* __restrict__ ring, const T
   physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
   physics_init(s1, c, x + 1, y, cfield, nx, ny, shift, nz, n_inner);
   int q0 = int((int64_t(s0.T) * (n_inner + 1) + levels - 1) / levels);
-  q0 = (q0 + 7) & ~7;
+  q0 = (q0 + 15) & ~15;
   int q1 = int((int64_t(s1.T) * (n_inner + 1) + levels - 1) / levels);
-  q1 = (q1 + 7) & ~7;
+  q1 = (q1 + 15) & ~15;
   int fast = 0;
   auto physics = [&](int b0, int b1) {
     if (fast > 0) {
       double y0 = s0.y, y1 = s1.y;
       const double e0 = s0.eb, e1 = s1.eb;
-      for (int j = 0; j < b0; j += 16) {
+      for (int j = 0; j < b0; j += 32) {
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < 32; ++q) {
           const double u0 = __fma_rn(-y0, y0, y0);
           const double u1 = __fma_rn(-y1, y1, y1);
           y0 = __fma_rn(kR, u0, e0);
