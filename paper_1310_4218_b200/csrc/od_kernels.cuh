@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 
 namespace odb {
 
@@ -829,6 +830,17 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     }
     cp_async_commit();
   };
+  // the same without the bound test (callers know L < levels; full tiles)
+  auto issue_full = [&](int L) {
+    double* slot = ring + (L & (R - 1)) * kPlaneMax;
+    cp_async16(slot + oc, pc);
+    if (px) cp_async8(slot + ox, px);
+    if (ny_cells == 2) cp_async16(slot + oy, py);
+    pc += ks;
+    px += xstep;
+    py += ystep;
+    cp_async_commit();
+  };
 
   ColumnState s0, s1;
   int q0 = 0, q1 = 0;
@@ -912,6 +924,31 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     pout += ks;
   };
   (void)PLANE;
+  // full-tile level with its k position known: FIRST (k == 0: no level below),
+  // LAST (k == nz - 1: no level above), neither -- no per-level predicates
+  auto level_k = [&](int L, auto first, auto last) {
+    const double* pl = rc + (L & (R - 1)) * kPlaneMax;
+    const double2 uc = *reinterpret_cast<const double2*>(pl);
+    const double xl = pl[-1], xr = pl[2];
+    const double2 ym = *reinterpret_cast<const double2*>(pl - PW);
+    const double2 yp = *reinterpret_cast<const double2*>(pl + PW);
+    double2 zu = uc;
+    if (!decltype(last)::value)
+      zu = *reinterpret_cast<const double2*>(rc + ((L + 1) & (R - 1)) * kPlaneMax);
+    const double zd0 = decltype(first)::value ? uc.x : zm0;
+    const double zd1 = decltype(first)::value ? uc.y : zm1;
+    const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                __dadd_rn(zd0, zu.x));
+    const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                __dadd_rn(zd1, zu.y));
+    double2 o;
+    o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+    o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+    __stcs(reinterpret_cast<double2*>(pout), o);
+    zm0 = uc.x;
+    zm1 = uc.y;
+    pout += ks;
+  };
 
   if (hw.n > 0 || hw.ndeps > 0) {
     // The tile reads strips a peer GPU stores into this GPU's receive buffer
@@ -961,6 +998,41 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 
   uint32_t parity = 0;
   int k = 0, L = 0;
+  if (FULL && (nz & 1) == 0 && nz >= 4) {
+    // even nz: a level pair never straddles two fields; the first and last
+    // pair of a field are peeled so the levels carry no k tests, and the
+    // copies skip their bound test until the last S planes
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const int tail = levels - S - 2;  // pairs with L <= tail copy planes < levels
+    for (int f = 0; f < F; ++f) {
+      for (int kk = 0; kk < nz; kk += 2, L += 2) {
+        mbar_wait(&s_ring_bar, parity);
+        parity ^= 1;
+        if (L <= tail) {
+          issue_full(L + S);
+          issue_full(L + S + 1);
+        } else {
+          issue(L + S);
+          issue(L + S + 1);
+        }
+        if (kk == 0) {
+          level_k(L, T_{}, F_{});
+          level_k(L + 1, F_{}, F_{});
+        } else if (kk == nz - 2) {
+          level_k(L, F_{}, F_{});
+          level_k(L + 1, F_{}, T_{});
+        } else {
+          level_k(L, F_{}, F_{});
+          level_k(L + 1, F_{}, F_{});
+        }
+        cp_async_wait<S - 3>();  // this thread's planes <= L+4 landed
+        od_jitter(4u + unsigned(L));
+        mbar_arrive(&s_ring_bar);
+        physics(2 * q0, 2 * q1);
+      }
+    }
+  }
   for (; L + 1 < levels; L += 2) {
     mbar_wait(&s_ring_bar, parity);  // everyone: planes <= L+2 landed, planes L-2, L-1 read
     parity ^= 1;
