@@ -301,6 +301,27 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+// the same with the shared address already converted (compile-time slot
+// offsets then fold into the instruction's immediate)
+__device__ __forceinline__ void cp_async8s(uint32_t s, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16s(uint32_t s, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// shared loads at a register + compile-time byte offset
+template <int OFF>
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];\n" : "=d"(v.x), "=d"(v.y) : "r"(a), "n"(OFF));
+  return v;
+}
+template <int OFF>
+__device__ __forceinline__ double lds1(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1+%2];\n" : "=d"(v) : "r"(a), "n"(OFF));
+  return v;
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
@@ -842,6 +863,28 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     cp_async_commit();
   };
 
+  // slot-constant copies: SLOT known at compile time (the 8-level unrolled loop)
+  const uint32_t sh_c = static_cast<uint32_t>(__cvta_generic_to_shared(ring + oc));
+  const uint32_t sh_x = static_cast<uint32_t>(__cvta_generic_to_shared(ring + ox));
+  const uint32_t sh_y = static_cast<uint32_t>(__cvta_generic_to_shared(ring + oy));
+  const uint32_t sh_m = sh_c - uint32_t(PW) * 8u, sh_p = sh_c + uint32_t(PW) * 8u;
+  // the plane stride re-read from shared memory through a thread-dependent
+  // address, so it lives in a vector register: the walkers' 64-bit steps use
+  // it directly instead of copying it out of a uniform register at each use
+  __shared__ int64_t s_ks[1];
+  if (threadIdx.x == 0 && threadIdx.y == 0) s_ks[0] = ks;
+  int64_t ksv = ks;  // re-read after the ring barrier's __syncthreads below
+  auto issue_slot = [&](auto slot) {
+    constexpr uint32_t off = uint32_t(decltype(slot)::value) * kPlaneMax * 8u;
+    cp_async16s(sh_c + off, pc);
+    if (px) cp_async8s(sh_x + off, px);
+    if (ny_cells == 2) cp_async16s(sh_y + off, py);
+    pc += ksv;
+    px += xstep;
+    py += ystep;
+    cp_async_commit();
+  };
+
   ColumnState s0, s1;
   int q0 = 0, q1 = 0;
   if (ncell >= 1) {
@@ -950,6 +993,36 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
     pout += ks;
   };
 
+  // the same with the slot (and the next level's) known at compile time
+  // the same with the slot known at compile time: every plane read is a
+  // register + immediate shared load; the level's centre plane comes in as
+  // `uc` (the level below read it as its upper neighbour) and its upper
+  // neighbour goes out as the next level's centre
+  auto level_s = [&](auto slot, auto first, auto last, double2 uc) -> double2 {
+    constexpr int sl = decltype(slot)::value;
+    constexpr int off = sl * kPlaneMax * 8;
+    constexpr int offn = ((sl + 1) & (R - 1)) * kPlaneMax * 8;
+    const double xl = lds1<off - 8>(sh_c), xr = lds1<off + 16>(sh_c);
+    const double2 ym = lds2<off>(sh_m);
+    const double2 yp = lds2<off>(sh_p);
+    double2 zu = uc;
+    if (!decltype(last)::value) zu = lds2<offn>(sh_c);
+    const double zd0 = decltype(first)::value ? uc.x : zm0;
+    const double zd1 = decltype(first)::value ? uc.y : zm1;
+    const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                __dadd_rn(zd0, zu.x));
+    const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                __dadd_rn(zd1, zu.y));
+    double2 o;
+    o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+    o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+    __stcs(reinterpret_cast<double2*>(pout), o);
+    zm0 = uc.x;
+    zm1 = uc.y;
+    pout += ksv;
+    return zu;
+  };
+
   if (hw.n > 0 || hw.ndeps > 0) {
     // The tile reads strips a peer GPU stores into this GPU's receive buffer
     // during this step, or cells of same-GPU tiles still finishing the previous
@@ -990,6 +1063,7 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
   const bool bar_lead = threadIdx.x == 0 && threadIdx.y == 0;
   if (bar_lead) mbar_init(&s_ring_bar, blockDim.x * blockDim.y);
   __syncthreads();
+  ksv = s_ks[threadIdx.y >> 3];  // (index 0: blockDim.y <= 8)
 
 #pragma unroll
   for (int L = 0; L < S; ++L) issue(L);
@@ -998,7 +1072,53 @@ __device__ __forceinline__ void tile_step(double* __restrict__ ring, const TileD
 
   uint32_t parity = 0;
   int k = 0, L = 0;
-  if (FULL && (nz & 1) == 0 && nz >= 4) {
+  if (FULL && R == 8 && (nz & 7) == 0) {
+    // nz a multiple of 8: the level loop unrolled over the 8 ring slots, so
+    // every plane address is a register plus an immediate (no per-level slot
+    // arithmetic); the first and last pair of a field are peeled as below
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    double2 ucn = make_double2(0.0, 0.0);  // the next level's centre plane
+    // IN_RANGE: every copy of the 8-level block is below `levels`
+    auto pair = [&](auto P, auto first, auto last, auto in_range) {
+      constexpr int p = decltype(P)::value;
+      mbar_wait(&s_ring_bar, parity);
+      parity ^= 1;
+      if (decltype(in_range)::value) {
+        issue_slot(std::integral_constant<int, (2 * p + S) & 7>{});
+        issue_slot(std::integral_constant<int, (2 * p + S + 1) & 7>{});
+      } else {
+        issue(L + S);
+        issue(L + S + 1);
+      }
+      if (decltype(first)::value) ucn = lds2<2 * p * kPlaneMax * 8>(sh_c);
+      ucn = level_s(std::integral_constant<int, 2 * p>{}, first, F_{}, ucn);
+      ucn = level_s(std::integral_constant<int, 2 * p + 1>{}, F_{}, last, ucn);
+      cp_async_wait<S - 3>();
+      od_jitter(4u + unsigned(L));
+      mbar_arrive(&s_ring_bar);
+      physics(2 * q0, 2 * q1);
+      L += 2;
+    };
+    using P0 = std::integral_constant<int, 0>;
+    using P1 = std::integral_constant<int, 1>;
+    using P2 = std::integral_constant<int, 2>;
+    using P3 = std::integral_constant<int, 3>;
+    for (int f = 0; f < F; ++f) {
+      for (int kk = 0; kk < nz; kk += 8) {
+        auto block = [&](auto in_range) {
+          if (kk == 0) pair(P0{}, T_{}, F_{}, in_range);
+          else pair(P0{}, F_{}, F_{}, in_range);
+          pair(P1{}, F_{}, F_{}, in_range);
+          pair(P2{}, F_{}, F_{}, in_range);
+          if (kk == nz - 8) pair(P3{}, F_{}, T_{}, in_range);
+          else pair(P3{}, F_{}, F_{}, in_range);
+        };
+        if (L + S + 8 <= levels) block(T_{});
+        else block(F_{});
+      }
+    }
+  } else if (FULL && (nz & 1) == 0 && nz >= 4) {
     // even nz: a level pair never straddles two fields; the first and last
     // pair of a field are peeled so the levels carry no k tests, and the
     // copies skip their bound test until the last S planes

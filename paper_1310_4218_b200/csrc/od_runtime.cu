@@ -66,7 +66,7 @@ static double now_s() {
 }
 
 constexpr int kTX = 32, kTY = 8, kPrefetch = 4, kFusedPrefetch = 6;
-constexpr int kGridMinBlocks = 5;  // column_step_grid CTAs per SM (94 registers)
+constexpr int kGridMinBlocks = 4;  // column_step_grid CTAs per SM (<= 128 registers)
 constexpr int kWsMinBlocks = 3;    // column_step_ws CTAs per SM
 
 // Fused-tile width for a chunk of w x h columns: the shape (tw x 256/tw, two
