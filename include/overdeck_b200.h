@@ -263,11 +263,11 @@ typedef struct od_config {
   int32_t n_inner;      /* FMA micro-steps per physics trip (f cost), >= 0 */
   int32_t measure;      /* OD_MEASURE_EVENTS | _TIMER | _TIMER_RAW | _OPS */
   int32_t overlap;      /* kernel mode: 0 separate jacobi_step + physics_step;
-                           4 fused interleaved tiles (column_step_grid); 5 automatic
-                           (default): column_step_grid from one wave of tiles per
-                           GPU up, column_step_ws below; 7 warp-specialised tiles
-                           (column_step_ws).  Fused modes overlap consecutive step
-                           kernels (programmatic dependent launch) */
+                           4 fused interleaved tiles (column_step_grid); 5 (default)
+                           and 7 warp-specialised tiles (column_step_ws; 5 kept as
+                           the default's name from round 1, when it switched between
+                           the two by tile count).  Fused modes overlap consecutive
+                           step kernels (programmatic dependent launch) */
   int32_t capacity_mib;  /* per-GPU cap on resident chunk data (MiB, B200 extension):
                             > 0 makes the epoch's Greedy / RefineSwap calls
                             capacity-aware (od_*_lb_capacity, one bin per GPU);

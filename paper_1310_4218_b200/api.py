@@ -798,9 +798,9 @@ class ExperimentConfig:  # engine.hpp:43-83, B200 fields appended
     n_inner: int = DEFAULT_N_INNER
     measure: MeasureMode = MeasureMode.Timer
     # kernel mode: 0 jacobi_step then physics_step (two launches); 4 fused
-    # interleaved tiles (column_step_grid); 5 automatic (default): interleaved
-    # from one wave of tiles per GPU up, warp-specialised below; 7
-    # warp-specialised tiles (column_step_ws).  Fused tiles are tw x 256/tw
+    # interleaved tiles (column_step_grid); 5 (default) and 7 warp-specialised
+    # tiles (column_step_ws: physics and Jacobi in sibling warps; faster than
+    # the interleaved tile at every size measured).  Fused tiles are tw x 256/tw
     # columns (tw = 64/32/16/8 by chunk width), heaviest first, consecutive
     # step kernels overlapped.
     overlap: int = 5

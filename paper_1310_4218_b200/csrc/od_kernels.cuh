@@ -1796,6 +1796,21 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
     }
     cp_async_commit();
   };
+  // full tiles: slot-constant copies and levels, as in tile_step
+  const uint32_t sh_c = static_cast<uint32_t>(__cvta_generic_to_shared(ring + oc));
+  const uint32_t sh_x = static_cast<uint32_t>(__cvta_generic_to_shared(ring + ox));
+  const uint32_t sh_y = static_cast<uint32_t>(__cvta_generic_to_shared(ring + oy));
+  const uint32_t sh_m = sh_c - uint32_t(PW) * 8u, sh_p = sh_c + uint32_t(PW) * 8u;
+  auto issue_slot = [&](auto slot) {
+    constexpr uint32_t off = uint32_t(decltype(slot)::value) * kPlaneMax * 8u;
+    cp_async16s(sh_c + off, pc);
+    if (px) cp_async8s(sh_x + off, px);
+    if (ny_cells == 2) cp_async16s(sh_y + off, py);
+    pc += ks;
+    px += xstep;
+    py += ystep;
+    cp_async_commit();
+  };
 
   ColumnState s0, s1;
   if (phys && ncell >= 1) physics_init(s0, c, x, y, cfield, nx, ny, shift, nz, n_inner);
@@ -1834,6 +1849,30 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
       zm0 = uc;
     }
     pout += ks;
+  };
+  auto level_s = [&](auto slot, auto first, auto last, double2 uc) -> double2 {
+    constexpr int sl = decltype(slot)::value;
+    constexpr int off = sl * kPlaneMax * 8;
+    constexpr int offn = ((sl + 1) & (R - 1)) * kPlaneMax * 8;
+    const double xl = lds1<off - 8>(sh_c), xr = lds1<off + 16>(sh_c);
+    const double2 ym = lds2<off>(sh_m);
+    const double2 yp = lds2<off>(sh_p);
+    double2 zu = uc;
+    if (!decltype(last)::value) zu = lds2<offn>(sh_c);
+    const double zd0 = decltype(first)::value ? uc.x : zm0;
+    const double zd1 = decltype(first)::value ? uc.y : zm1;
+    const double sa = __dadd_rn(__dadd_rn(__dadd_rn(xl, uc.y), __dadd_rn(ym.x, yp.x)),
+                                __dadd_rn(zd0, zu.x));
+    const double sb = __dadd_rn(__dadd_rn(__dadd_rn(uc.x, xr), __dadd_rn(ym.y, yp.y)),
+                                __dadd_rn(zd1, zu.y));
+    double2 o;
+    o.x = __fma_rn(kW1, sa, __dmul_rn(kW0, uc.x));
+    o.y = __fma_rn(kW1, sb, __dmul_rn(kW0, uc.y));
+    __stcs(reinterpret_cast<double2*>(pout), o);
+    zm0 = uc.x;
+    zm1 = uc.y;
+    pout += ks;
+    return zu;
   };
 
   __shared__ uint64_t s_ring_bar;
@@ -1877,6 +1916,49 @@ __device__ __forceinline__ void tile_step_ws(double* __restrict__ ring, const Ti
     mbar_arrive(&s_ring_bar);
     uint32_t parity = 0;
     int k = 0, L = 0;
+    if (FULL && (nz & 7) == 0) {
+      // the level loop unrolled over the 8 ring slots (see tile_step)
+      using T_ = std::true_type;
+      using F_ = std::false_type;
+      double2 ucn = make_double2(0.0, 0.0);
+      auto pair = [&](auto P, auto first, auto last, auto in_range) {
+        constexpr int p = decltype(P)::value;
+        mbar_wait(&s_ring_bar, parity);
+        parity ^= 1;
+        if (decltype(in_range)::value) {
+          issue_slot(std::integral_constant<int, (2 * p + S) & 7>{});
+          issue_slot(std::integral_constant<int, (2 * p + S + 1) & 7>{});
+        } else {
+          issue(L + S);
+          issue(L + S + 1);
+        }
+        if (decltype(first)::value) ucn = lds2<2 * p * kPlaneMax * 8>(sh_c);
+        ucn = level_s(std::integral_constant<int, 2 * p>{}, first, F_{}, ucn);
+        ucn = level_s(std::integral_constant<int, 2 * p + 1>{}, F_{}, last, ucn);
+        cp_async_wait<S - 3>();
+        od_jitter(4u + unsigned(L));
+        mbar_arrive(&s_ring_bar);
+        L += 2;
+      };
+      using P0 = std::integral_constant<int, 0>;
+      using P1 = std::integral_constant<int, 1>;
+      using P2 = std::integral_constant<int, 2>;
+      using P3 = std::integral_constant<int, 3>;
+      for (int f = 0; f < F; ++f) {
+        for (int kk = 0; kk < nz; kk += 8) {
+          auto block = [&](auto in_range) {
+            if (kk == 0) pair(P0{}, T_{}, F_{}, in_range);
+            else pair(P0{}, F_{}, F_{}, in_range);
+            pair(P1{}, F_{}, F_{}, in_range);
+            pair(P2{}, F_{}, F_{}, in_range);
+            if (kk == nz - 8) pair(P3{}, F_{}, T_{}, in_range);
+            else pair(P3{}, F_{}, F_{}, in_range);
+          };
+          if (L + S + 8 <= levels) block(T_{});
+          else block(F_{});
+        }
+      }
+    }
     for (; L + 1 < levels; L += 2) {
       mbar_wait(&s_ring_bar, parity);
       parity ^= 1;

@@ -231,7 +231,8 @@ class Runtime {
   size_t oring_cap_ = 0;
   int oring_pending_ = -1;             // window position of the live mapped order
   const TileDev* cur_tiles_ = nullptr;  // the list the step kernel reads
-  int wave_ = 0;       // tiles one launch keeps resident (SMs x CTAs per SM)
+  int wave_grid_ = 0;  // tiles one launch keeps resident (SMs x CTAs per SM): column_step_grid
+  int wave_ws_ = 0;    // the same for column_step_ws
   // equal-work tiles are dealt round-robin over the chunks in bands of band_
   // consecutive tiles of a chunk: y-neighbours start ~one CTA retirement apart,
   // so the halo rows they share are read within microseconds and hit L2.
@@ -246,8 +247,10 @@ class Runtime {
   void refresh_tile_order(int mapped_pos = -1);
   // mode 5: the warp-specialised tile when a GPU holds less than one wave of
   // tiles (latency-bound), the interleaved tile otherwise; mode 7 always WS
-  bool use_ws(int ntiles) const {
-    return cfg_.overlap == 7 || (cfg_.overlap == 5 && ntiles < wave_);
+  // mode 5 (default) and 7: the warp-specialised tile at every size (faster than
+  // the interleaved one from 256 to 4096 tiles per GPU, profiles/r2_ws_threshold.json)
+  bool use_ws() const {
+    return cfg_.overlap == 7 || cfg_.overlap == 5;
   }
   int32_t last_kernel_ = 0;  // OD_KERNEL_* of the last step kernel launched
   // cross-step overlap of the mode-5 step kernels (PDL + per-tile stamps;
@@ -460,7 +463,10 @@ Runtime::Runtime(const od_config& cfg, int rank, int world, int device, const ui
     int per_sm = 0;
     OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
         &per_sm, column_step_grid<kFusedPrefetch, false, kGridMinBlocks>, 32 * kRowWarps, 0));
-    wave_ = sms * std::max(per_sm, 1);
+    wave_grid_ = sms * std::max(per_sm, 1);
+    OD_CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, column_step_ws<kFusedPrefetch, false, kWsMinBlocks>, 64 * kRowWarps, 0));
+    wave_ws_ = sms * std::max(per_sm, 1);
   }
   if (world_ > 1) {
     ncclUniqueId id;
@@ -678,8 +684,9 @@ void Runtime::refresh_tile_order(int mapped_pos) {
     std::vector<std::tuple<double, int32_t, int32_t>> front, rest;
     front.reserve(n);
     rest.reserve(n);
+    const size_t wave = size_t(use_ws() ? wave_ws_ : wave_grid_);
     for (const auto& k : key)
-      (front.size() < size_t(wave_) && !(tiles4_[std::get<2>(k)].pad & 1) ? front : rest)
+      (front.size() < wave && !(tiles4_[std::get<2>(k)].pad & 1) ? front : rest)
           .push_back(k);
     front.insert(front.end(), rest.begin(), rest.end());
     key.swap(front);
@@ -1571,7 +1578,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     const ChunkDev* chk = d_chunks_[par];
     unsigned long long* nsp = timer ? ns : nullptr;
     unsigned long long* waitp = timer ? ns + (ns_cols_ - 1) : (r.ovl ? nullptr : tl_wait());
-    if (use_ws(nt)) {
+    if (use_ws()) {
       // warp-specialised tiles (column_step_ws): physics and Jacobi warps
       lc.blockDim = dim3(32, 2 * kRowWarps);
       if (timer)

@@ -59,6 +59,22 @@ def test_fields_tile_widths(nx, kx, ny, ky, mode, tma, monkeypatch):
     assert_bitwise(A, Ao, "A")
 
 
+@pytest.mark.parametrize("mode", [4, 5])
+@pytest.mark.parametrize("nz,F", [(8, 3), (16, 2), (24, 1), (40, 2)])
+@pytest.mark.parametrize("nx,kx,ny,ky", [(128, 2, 16, 2), (64, 2, 32, 2), (96, 3, 44, 2)])
+def test_fields_unrolled_level_loop(nx, kx, ny, ky, nz, F, mode):
+    # nz a multiple of 8: full tiles run the level loop unrolled over the 8 ring
+    # slots (interleaved tile, mode 4; the warp-specialised tile's Jacobi warps,
+    # mode 5): one 8-level block per field at nz = 8 (its first and last pair
+    # both peeled), the copy-range fallback on the last blocks, partial tiles
+    # (44 rows) beside full ones
+    cfg = small(nx=nx, ny=ny, nz=nz, F=F, kx=kx, ky=ky, n_inner=11, overlap=mode, heavy=3.0)
+    U, A, _ = device_fields(cfg, 3)
+    Uo, Ao = oracle_fields(cfg, 3)
+    assert_bitwise(U, Uo, "U")
+    assert_bitwise(A, Ao, "A")
+
+
 def test_fields_multi_tile_chunks_and_advection():
     # chunks wider than one 32-column tile and taller than 8 rows; moving band
     cfg = small(nx=150, ny=70, nz=9, F=2, kx=2, ky=3, adv=(35, 1, 3), n_inner=3, overlap=5)

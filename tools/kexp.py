@@ -13,10 +13,10 @@ import paper_1310_4218_b200 as od  # noqa: E402
 from paper_1310_4218_b200 import configs  # noqa: E402
 
 a = {"nx": 1024, "ny": 1024, "nz": 64, "F": 50, "n_inner": 1536, "kx": 16, "ky": 16, "mode": 5,
-     "steps": 20, "heavy": 2}
+     "steps": 20, "heavy": 2, "light": 1}
 a.update({k: int(v) for k, v in (x.split("=") for x in sys.argv[1:])})
 cfg = configs.cfg4(nodes=1, epochs=1 << 30, overlap=a["mode"], n_inner=a["n_inner"]).replace(
-    domain=od.Domain(a["nx"], a["ny"], a["nz"], a["F"]), heavy_value=float(a["heavy"]),
+    domain=od.Domain(a["nx"], a["ny"], a["nz"], a["F"]), heavy_value=float(a["heavy"]), light_value=float(a["light"]),
     decomposition=od.Decomposition(od.DecompositionKind.TwoD, a["kx"], a["ky"]))
 import threading  # noqa: E402
 import pynvml  # noqa: E402
