@@ -2,20 +2,24 @@
 TMA / mbarrier / cp.async instructions, and the fall-through path of one in-range
 level pair of the 8-slot unrolled loop (mbarrier wait .. arrive).
 
-usage: python tools/sass_summary.py [OUT]   (reads paper_1310_4218_b200/libod_b200.so)
+usage: python tools/sass_summary.py [OUT] [grid|ws]   (reads paper_1310_4218_b200/libod_b200.so)
 """
 import collections
 import re
 import subprocess
 import sys
 
-KERNEL = ("_ZN3odb16column_step_gridILi6ELb0ELi4ELi8EEEvPKNS_8ChunkDevEPKNS_7TileDevEiiPKdiiii"
-          "PyPKyPKiiyS9_NS_8PackArgsENS_8StepDepsE")
+_ARGS = "EEEvPKNS_8ChunkDevEPKNS_7TileDevEiiPKdiiiiPyPKyiyS9_NS_8PackArgsENS_8StepDepsE"
+KERNELS = {
+    "grid": ("_ZN3odb16column_step_gridILi6ELb0ELi4ELi8" + _ARGS, "column_step_grid<6,false,4,8>"),
+    "ws": ("_ZN3odb14column_step_wsILi6ELb0ELi3" + _ARGS, "column_step_ws<6,false,3>"),
+}
 
 
 def main():
     out_path = sys.argv[1] if len(sys.argv) > 1 else "profiles/r2_sass_column_step_grid.txt"
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", KERNEL, "paper_1310_4218_b200/libod_b200.so"],
+    kernel, label = KERNELS[sys.argv[2] if len(sys.argv) > 2 else "grid"]
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", kernel, "paper_1310_4218_b200/libod_b200.so"],
                           check=True, capture_output=True, text=True).stdout
     ins, pos = [], {}
     for line in sass.splitlines():
@@ -29,7 +33,7 @@ def main():
 
     mix = collections.Counter(op(s) for _, s in ins)
     out = ["# cuobjdump -sass paper_1310_4218_b200/libod_b200.so, kernel "
-           "column_step_grid<6,false,4,8> (sm_100a)", "# instruction mix:"]
+           f"{label} (sm_100a)", "# instruction mix:"]
     out += [f"{v:7d} {k}" for k, v in mix.most_common(32)]
     out.append("# TMA (UTMALDG), mbarrier (SYNCS), cp.async (LDGSTS) and proxy fences (first 80):")
     keep = ("UTMALDG", "SYNCS", "LDGSTS", "FENCE", "ARRIVES")
@@ -48,6 +52,10 @@ def main():
         path.append(ins[i])
         return path
 
+    if len(waits) < 9:  # (a kernel without the interleaved tile's pair layout)
+        open(out_path, "w").write("\n".join(out) + "\n")
+        print(out[2])
+        return
     # waits[3..8]: the six in-range pair bodies (P0 first / other, P1, P2, P3 last / other)
     bodies = [pair_path(w) for w in waits[3:9]]
     fps = [sum(op(s) in ("DADD", "DFMA", "DMUL") for _, s in b) for b in bodies]
