@@ -45,7 +45,9 @@ struct ChunkDev {
   double* a;         // physics state A, [nz][h][pitch]
   int64_t fstride;   // nz * kstride
   int64_t kstride;   // h * pitch
-  int32_t w, h, pitch, x0, y0, vp, pad0, pad1;
+  int32_t w, h, pitch, x0, y0, vp;
+  int32_t rmask;  // P2P halos: bit d set when face d is a strip received from a peer GPU
+  int32_t pad1;
   FaceDev face[4];
   // TMA tensor maps of U^t for full tiles (null: the chunk has no full tile or
   // TMA staging is off): box tw x th x 1 (main) and tw x 1 x 1 (row)
@@ -66,7 +68,8 @@ __device__ __forceinline__ int share_tag(const TileDev& t) {
 struct PackJob {
   int32_t slot, side, len, lenp;  // side: which edge of the source chunk; lenp: row stride
   int64_t dst;                   // element offset into the send buffer
-  int32_t peer, pad;             // destination rank
+  int32_t peer;                  // destination rank
+  int32_t rflag;                 // index of the face's flag in the peer's flag array
   int64_t rdst;                  // element offset in the peer's receive buffer half
 };
 
@@ -235,10 +238,14 @@ __device__ __forceinline__ void wait_stamps(const unsigned long long* __restrict
 // strips are known to have landed.
 constexpr int kPreroll = 256;  // physics units per pre-roll round (multiple of 16)
 
+// P2P halos are published per face: the sender's pack stores the stamp into
+// flags[fbase + 4 * vp + side] on the receiving GPU (vp: the receiving chunk,
+// side: its face) once all fields of that strip have landed, so a tile waits
+// only for the strips it reads, not for every strip of every sender.
 struct HaloWait {
   const unsigned long long* flags;
-  const int32_t* senders;
-  int32_t n;
+  int32_t fbase;  // flags[fbase + 4 * vp + side]
+  int32_t n;      // bit mask of the remote faces this tile reads (0: none)
   unsigned long long stamp;
   unsigned long long* wait_ns;  // longest blocking wait (diagnostic), may be null
   // cross-step overlap: neighbour tiles on this GPU that must have finished the
@@ -259,8 +266,8 @@ __device__ __forceinline__ void st_release_gpu_u32(unsigned* p, unsigned v) {
 }
 
 __device__ __forceinline__ bool stamps_ready(const HaloWait& hw) {
-  for (int i = 0; i < hw.n; ++i)
-    if (ld_acquire_sys(hw.flags + hw.senders[i]) < hw.stamp) return false;
+  for (int d = 0; d < 4; ++d)
+    if (((hw.n >> d) & 1) && ld_acquire_sys(hw.flags + hw.fbase + d) < hw.stamp) return false;
   for (int i = 0; i < hw.ndeps; ++i)
     if (ld_acquire_gpu_u32(hw.done + hw.deps[i]) < hw.need) return false;
   return true;
@@ -1508,6 +1515,7 @@ struct PackArgs {
   int64_t half_elems;
   int32_t par, n_notify, my_rank, first;  // first: lowest blockIdx that packs
   unsigned int* counters;  // [next unit, units done], zeroed before the launch
+  unsigned int* jcnt;      // per job: fields packed this step, zeroed before the launch
   unsigned long long* const* peer_flags;
   const int32_t* notify;
 };
@@ -1580,12 +1588,27 @@ __device__ __noinline__ void pack_units(const PackArgs pk, const ChunkDev* __res
     __threadfence_system();
     __syncthreads();
     od_jitter(3u);
+    // the last field of a strip publishes that strip to its reader
+    if (lead && atomicAdd(&pk.jcnt[u / F], 1u) == unsigned(F - 1)) {
+      __threadfence_system();
+      st_release_sys(pk.peer_flags[j.peer] + j.rflag, stamp);
+    }
     if (lead && atomicAdd(&pk.counters[1], 1u) == unsigned(total - 1)) {
       __threadfence_system();
       for (int i = 0; i < pk.n_notify; ++i)
         st_release_sys(pk.peer_flags[pk.notify[i]] + pk.my_rank, stamp);
     }
   }
+}
+
+// Remote faces of chunk c that tile t touches (bit d: face d), i.e. the strips it reads.
+__device__ __forceinline__ int tile_remote_faces(const TileDev& t, const ChunkDev& c) {
+  int m = 0;
+  if (t.tx0 == 0) m |= 1 << kLeft;
+  if (t.tx0 + t.tw >= c.w) m |= 1 << kRight;
+  if (t.ty0 == 0) m |= 1 << kTop;
+  if (t.ty0 + t.th >= c.h) m |= 1 << kBottom;
+  return m & c.rmask;
 }
 
 // Cross-step overlap, tile side: block on the tile's own previous step (its
@@ -1647,8 +1670,7 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
                      int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
                      int32_t ny, int32_t shift, int32_t n_inner,
                      unsigned long long* __restrict__ chunk_ns,
-                     const unsigned long long* __restrict__ halo_flags,
-                     const int32_t* __restrict__ senders, int32_t n_senders,
+                     const unsigned long long* __restrict__ halo_flags, int32_t face_base,
                      unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                      const PackArgs pk, const StepDeps sd) {
   // rings deeper than 8 slots exceed the 48 KB static limit: dynamic smem
@@ -1665,8 +1687,8 @@ __global__ void __launch_bounds__(32 * kRowWarps, MINB)
   const TileDev t = tiles[blockIdx.x - pk.ctas];
   const ChunkDev& c = chunks[t.slot];
   const int self = t.pad >> 1;
-  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
-              nullptr, nullptr, 0, 0};
+  HaloWait hw{halo_flags, face_base + 4 * c.vp, (t.pad & 1) ? tile_remote_faces(t, c) : 0,
+              stamp, wait_ns, nullptr, nullptr, 0, 0};
   tile_deps(sd, self, hw);
   if (tile_full(t, c) && c.tm_main && R == kRingSlots)
     tile_step_tma<S, TIMED>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns, hw);
@@ -2014,8 +2036,7 @@ __global__ void __launch_bounds__(64 * kRowWarps, MINB)
                    int32_t nz, int32_t F, const double* __restrict__ cfield, int32_t nx,
                    int32_t ny, int32_t shift, int32_t n_inner,
                    unsigned long long* __restrict__ chunk_ns,
-                   const unsigned long long* __restrict__ halo_flags,
-                   const int32_t* __restrict__ senders, int32_t n_senders,
+                   const unsigned long long* __restrict__ halo_flags, int32_t face_base,
                    unsigned long long stamp, unsigned long long* __restrict__ wait_ns,
                    const PackArgs pk, const StepDeps sd) {
   __shared__ __align__(16) double ring[kRingSlots * kPlaneMax];
@@ -2027,8 +2048,8 @@ __global__ void __launch_bounds__(64 * kRowWarps, MINB)
   const TileDev t = tiles[blockIdx.x - pk.ctas];
   const ChunkDev& c = chunks[t.slot];
   const int self = t.pad >> 1;
-  HaloWait hw{halo_flags, senders, (t.pad & 1) ? n_senders : 0, stamp, wait_ns,
-              nullptr, nullptr, 0, 0};
+  HaloWait hw{halo_flags, face_base + 4 * c.vp, (t.pad & 1) ? tile_remote_faces(t, c) : 0,
+              stamp, wait_ns, nullptr, nullptr, 0, 0};
   tile_deps(sd, self, hw);
   if (tile_full(t, c))
     tile_step_ws<S, TIMED, true>(ring, t, chunks, nz, F, cfield, nx, ny, shift, n_inner, chunk_ns,
@@ -2105,6 +2126,8 @@ __global__ void pack_faces_p2p(const ChunkDev* __restrict__ chunks,
     if (atomicAdd(counter, 1u) == total - 1) {
       __threadfence_system();
       for (int i = 0; i < n_notify; ++i) st_release_sys(peer_flags[notify[i]] + my_rank, value);
+      for (unsigned q = 0; q < gridDim.x; ++q)
+        st_release_sys(peer_flags[jobs[q].peer] + jobs[q].rflag, value);
       *counter = 0u;  // next step's count (stream ordered)
     }
   }

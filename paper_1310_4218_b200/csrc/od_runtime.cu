@@ -265,6 +265,8 @@ class Runtime {
   size_t d_done_cap_ = 0;
   unsigned long long* d_stepend_ = nullptr;  // [window steps + 1]: start, end of each step
   unsigned* d_pcnt_ = nullptr;                // [window steps][2] fused-pack counters
+  unsigned* d_jcnt_ = nullptr;                // [window steps][4 K] per-strip field counts
+  unsigned* d_jcnt1_ = nullptr;               // [4 K] the same for a step outside a window
   int32_t win_cap_ = 0;
   bool win_overlap_ = false;  // this window's steps ran overlapped
   void build_step_deps();
@@ -301,7 +303,8 @@ class Runtime {
   // NVLink peer-memory halo exchange (CUDA IPC), default for world > 1
   bool p2p_ = false;
   int64_t recv_half_ = 0;  // elements per parity half of d_recv_ (p2p)
-  unsigned long long* d_flags_ = nullptr;  // [world] step published by each sender
+  // [world] step published by each sender, then [4 K] per receiving chunk face
+  unsigned long long* d_flags_ = nullptr;
   std::vector<double*> peer_recv_;
   std::vector<double*> peer_slab_;  // every rank's chunk slab (IPC), for migration pulls
   bool peer_slabs_ok_ = false;
@@ -568,6 +571,8 @@ Runtime::~Runtime() {
   cudaFree(d_done_);
   cudaFree(d_stepend_);
   cudaFree(d_pcnt_);
+  cudaFree(d_jcnt_);
+  cudaFree(d_jcnt1_);
   slog_dump();
   cudaFree(d_slog_);
   for (auto& m : chunks_)
@@ -1012,7 +1017,9 @@ void Runtime::rebuild_tables() {
   }
   std::vector<size_t> taken(world_, 0);
   for (const FaceXfer& f : sends) {
-    PackJob pj{slot_of[f.vp], f.side, f.len, f.lenp, f.offset, f.peer, 0, 0};
+    // the receiver's flag of this strip: its chunk f.nbr, face opposite(f.side)
+    PackJob pj{slot_of[f.vp], f.side, f.len, f.lenp, f.offset, f.peer,
+               world_ + 4 * f.nbr + opposite(f.side), 0};
     if (p2p_) pj.rdst = remote_off[f.peer].at(taken[f.peer]++);
     jobs_.push_back(pj);
     send_cnt_[f.peer] += per_cell * f.lenp;
@@ -1075,6 +1082,7 @@ void Runtime::rebuild_tables() {
       c.x0 = m.sub.x0;
       c.y0 = m.sub.y0;
       c.vp = m.vp;
+      c.rmask = 0;
       for (int d = 0; d < 4; ++d) {
         const int32_t n = nbr(m.vp, d);
         if (n < 0) {
@@ -1084,6 +1092,7 @@ void Runtime::rebuild_tables() {
         } else {
           const int32_t len = (d == kLeft || d == kRight) ? c.h : c.w;
           c.face[d].p = d_recv_ + par * recv_half_ + recv_face_off_[i][d];
+          if (p2p_) c.rmask |= 1 << d;
           c.face[d].lo = d_recv_ + par * recv_half_;
           c.face[d].hi = d_recv_ + par * recv_half_ + int64_t(recv_cap_);
           const int32_t lenp = (len + 1) & ~1;
@@ -1210,8 +1219,9 @@ void Runtime::alloc_comm_buffers() {
 // Map every peer's receive buffer and flag array into this process (CUDA IPC;
 // handles all-gathered over the NCCL communicator).
 void Runtime::setup_p2p() {
-  OD_CU(cudaMalloc(&d_flags_, sizeof(unsigned long long) * world_));
-  OD_CU(cudaMemset(d_flags_, 0, sizeof(unsigned long long) * world_));
+  OD_CU(cudaMalloc(&d_flags_, sizeof(unsigned long long) * (world_ + 4 * size_t(K()))));
+  OD_CU(cudaMemset(d_flags_, 0, sizeof(unsigned long long) * (world_ + 4 * size_t(K()))));
+  OD_CU(cudaMalloc(&d_jcnt1_, 4 * size_t(K()) * sizeof(unsigned)));
   OD_CU(cudaMalloc(&d_pack_counter_, sizeof(unsigned int)));
   OD_CU(cudaMemset(d_pack_counter_, 0, sizeof(unsigned int)));
   // [recv buffer, flags, chunk slab (migration pulls; zeroed if no slab)]
@@ -1317,12 +1327,15 @@ void Runtime::begin_window(bool allow_overlap) {
       OD_CU(cudaStreamSynchronize(s0_));
       cudaFree(d_stepend_);
       cudaFree(d_pcnt_);
+      cudaFree(d_jcnt_);
       win_cap_ = S;
+      OD_CU(cudaMalloc(&d_jcnt_, size_t(S) * 4 * size_t(K()) * sizeof(unsigned)));
       OD_CU(cudaMalloc(&d_stepend_, size_t(2 * S) * sizeof(unsigned long long)));
       OD_CU(cudaMalloc(&d_pcnt_, size_t(4 * S) * sizeof(unsigned)));
     }
     OD_CU(cudaMemsetAsync(d_stepend_, 0, size_t(2 * win_cap_) * sizeof(unsigned long long), s0_));
     OD_CU(cudaMemsetAsync(d_pcnt_, 0, size_t(4 * win_cap_) * sizeof(unsigned), s0_));
+    OD_CU(cudaMemsetAsync(d_jcnt_, 0, size_t(win_cap_) * 4 * size_t(K()) * sizeof(unsigned), s0_));
     // every tile is current with every step launched so far (earlier steps may
     // have run without the per-tile stamps)
     if (!tiles4_.empty()) {
@@ -1541,10 +1554,13 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
       pk.my_rank = rank_;
       pk.first = 0;
       pk.counters = r.ovl ? d_pcnt_ + 4 * pos : d_counter_ + 1;
+      pk.jcnt = r.ovl ? d_jcnt_ + size_t(pos) * 4 * size_t(K()) : d_jcnt1_;
+      if (!r.ovl)
+        OD_CU(cudaMemsetAsync(pk.jcnt, 0, jobs_.size() * sizeof(unsigned), s0_));
       pk.peer_flags = d_peer_flags_;
       pk.notify = d_notify_;
     }
-    const int32_t nsend = p2p_ ? n_senders_ : 0;
+    const int32_t face_base = world_;  // per-face flags follow the per-sender ones
     const unsigned long long stamp = (unsigned long long)(st_.steps + 1);
     StepDeps sd{};
     if (r.ovl) {
@@ -1585,12 +1601,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
         OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, kWsMinBlocks>, chk,
                                  tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
                                  cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
-                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+                                 face_base, stamp, waitp, pk, sd));
       else
         OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, false, kWsMinBlocks>, chk,
                                  tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
                                  cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
-                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+                                 face_base, stamp, waitp, pk, sd));
       last_kernel_ = OD_KERNEL_STEP_WS;
     } else {
       // interleaved tiles (column_step_grid)
@@ -1598,12 +1614,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
         OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<kFusedPrefetch, true, kGridMinBlocks>,
                                  chk, tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
                                  cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
-                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+                                 face_base, stamp, waitp, pk, sd));
       else
         OD_CU(cudaLaunchKernelEx(&lc, column_step_grid<kFusedPrefetch, false, kGridMinBlocks>,
                                  chk, tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
                                  cfg_.n_inner, nsp, (const unsigned long long*)d_flags_,
-                                 (const int32_t*)d_senders_, nsend, stamp, waitp, pk, sd));
+                                 face_base, stamp, waitp, pk, sd));
       last_kernel_ = OD_KERNEL_STEP_GRID;
     }
     OD_CU(cudaGetLastError());
@@ -1664,7 +1680,7 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
         column_step_grid<kFusedPrefetch, false, kGridMinBlocks>
             <<<tile4_count_[i], dim3(32, kRowWarps), 0, s0_>>>(
                 d_chunks_[par], d_tiles4_ + tile4_begin_[i], cfg_.nz, cfg_.fields, cfield,
-                cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, d_senders_, 0, 0ull,
+                cfg_.nx, cfg_.ny, shift, cfg_.n_inner, nullptr, d_flags_, world_, 0ull,
                 nullptr, PackArgs{}, StepDeps{});
         st_.kernel_launches += 1;
         st_.fused_launches += 1;
