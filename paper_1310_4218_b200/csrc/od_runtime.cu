@@ -267,6 +267,9 @@ class Runtime {
   unsigned* d_pcnt_ = nullptr;                // [window steps][2] fused-pack counters
   unsigned* d_jcnt_ = nullptr;                // [window steps][4 K] per-strip field counts
   unsigned* d_jcnt1_ = nullptr;               // [4 K] the same for a step outside a window
+  int64_t* d_mig_off_ = nullptr;              // migration: [world + 1][K] slab offsets
+  CopyJob* d_mig_jobs_ = nullptr;             // migration: pull jobs (at most 2 K)
+  int32_t* d_mig_one_ = nullptr;              // migration: ordering all-reduce word
   int32_t win_cap_ = 0;
   bool win_overlap_ = false;  // this window's steps ran overlapped
   void build_step_deps();
@@ -573,6 +576,9 @@ Runtime::~Runtime() {
   cudaFree(d_pcnt_);
   cudaFree(d_jcnt_);
   cudaFree(d_jcnt1_);
+  cudaFree(d_mig_off_);
+  cudaFree(d_mig_jobs_);
+  cudaFree(d_mig_one_);
   slog_dump();
   cudaFree(d_slog_);
   for (auto& m : chunks_)
@@ -2112,15 +2118,21 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
         if (rank_of_proc(map_[v]) == rank_ && chunks_[v].base && chunks_[v].base >= slab_ &&
             chunks_[v].base < slab_ + slab_elems)
           mine[v] = int64_t(chunks_[v].base - slab_);
-      int64_t* d_off = nullptr;
-      OD_CU(cudaMalloc(&d_off, sizeof(int64_t) * size_t(K()) * (world_ + 1)));
-      OD_CU(cudaMemcpy(d_off, mine.data(), sizeof(int64_t) * K(), cudaMemcpyHostToDevice));
+      // migration scratch (offsets, pull jobs, ordering word) allocated once: a
+      // cudaMalloc/cudaFree pair per epoch would synchronise the device each time
+      if (!d_mig_off_) {
+        OD_CU(cudaMalloc(&d_mig_off_, sizeof(int64_t) * size_t(K()) * (world_ + 1)));
+        OD_CU(cudaMalloc(&d_mig_jobs_, sizeof(CopyJob) * 2 * size_t(K())));
+        OD_CU(cudaMalloc(&d_mig_one_, sizeof(int32_t)));
+      }
+      int64_t* d_off = d_mig_off_;
+      OD_CU(cudaMemcpyAsync(d_off, mine.data(), sizeof(int64_t) * K(), cudaMemcpyHostToDevice,
+                            s0_));
       OD_NC(odb::nccl().AllGather(d_off, d_off + K(), size_t(K()), ncclInt64, comm_, s0_));
       std::vector<int64_t> all(size_t(K()) * world_);
       OD_CU(cudaMemcpyAsync(all.data(), d_off + K(), sizeof(int64_t) * all.size(),
                             cudaMemcpyDeviceToHost, s0_));
       OD_CU(cudaStreamSynchronize(s0_));
-      cudaFree(d_off);
       bool ok = true;
       for (int32_t v : moved) ok = ok && all[size_t(rank_of_proc(map_[v])) * K() + v] >= 0;
       if (ok) {
@@ -2140,8 +2152,7 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
           pulls.push_back(CopyJob{sb + (in.a - in.base), in.a, int64_t(ae)});
         }
         if (!pulls.empty()) {
-          CopyJob* d_jobs = nullptr;
-          OD_CU(cudaMalloc(&d_jobs, pulls.size() * sizeof(CopyJob)));
+          CopyJob* d_jobs = d_mig_jobs_;
           OD_CU(cudaMemcpyAsync(d_jobs, pulls.data(), pulls.size() * sizeof(CopyJob),
                                 cudaMemcpyHostToDevice, s0_));
           // ~2 waves of 256-thread CTAs spread over the jobs
@@ -2149,15 +2160,12 @@ void Runtime::migrate(const std::vector<MoveRec>& plan) {
           pull_chunks<<<dim3(per_job, unsigned(pulls.size())), 256, 0, s0_>>>(d_jobs);
           OD_CU(cudaGetLastError());
           ++st_.kernel_launches;
-          OD_CU(cudaStreamSynchronize(s0_));
-          cudaFree(d_jobs);
         }
-        int32_t* d_one = nullptr;
-        OD_CU(cudaMalloc(&d_one, sizeof(int32_t)));
+        // (stream order: the all-reduce runs after this rank's pulls)
+        int32_t* d_one = d_mig_one_;
         OD_CU(cudaMemsetAsync(d_one, 0, sizeof(int32_t), s0_));
         OD_NC(odb::nccl().AllReduce(d_one, d_one, 1, ncclInt32, ncclSum, comm_, s0_));
         OD_CU(cudaStreamSynchronize(s0_));
-        cudaFree(d_one);
         pulled = true;
       }
     }
