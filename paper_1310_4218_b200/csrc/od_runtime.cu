@@ -1230,6 +1230,28 @@ void Runtime::setup_p2p() {
   OD_CU(cudaMalloc(&d_jcnt1_, 4 * size_t(K()) * sizeof(unsigned)));
   OD_CU(cudaMalloc(&d_pack_counter_, sizeof(unsigned int)));
   OD_CU(cudaMemset(d_pack_counter_, 0, sizeof(unsigned int)));
+  // senders address a peer's parity half as peer_base + par * half, so every
+  // rank's half must have the same size: the largest rank's (resident chunk
+  // counts, hence worst-case capacities, differ between ranks)
+  {
+    int64_t* d_cap = nullptr;
+    OD_CU(cudaMalloc(&d_cap, sizeof(int64_t) * (world_ + 1)));
+    const int64_t cap = int64_t(recv_cap_);
+    OD_CU(cudaMemcpy(d_cap, &cap, sizeof(int64_t), cudaMemcpyHostToDevice));
+    OD_NC(odb::nccl().AllGather(d_cap, d_cap + 1, 1, ncclInt64, comm_, s0_));
+    std::vector<int64_t> caps(world_);
+    OD_CU(cudaMemcpyAsync(caps.data(), d_cap + 1, sizeof(int64_t) * world_,
+                          cudaMemcpyDeviceToHost, s0_));
+    OD_CU(cudaStreamSynchronize(s0_));
+    cudaFree(d_cap);
+    const size_t top = size_t(*std::max_element(caps.begin(), caps.end()));
+    if (top > recv_cap_) {
+      cudaFree(d_recv_);
+      recv_cap_ = top;
+      OD_CU(cudaMalloc(&d_recv_, 2 * recv_cap_ * sizeof(double)));
+    }
+    recv_half_ = int64_t(recv_cap_);
+  }
   // [recv buffer, flags, chunk slab (migration pulls; zeroed if no slab)]
   cudaIpcMemHandle_t mine[3];
   std::memset(mine, 0, sizeof(mine));
