@@ -44,14 +44,21 @@ def test_four_gpus_fields_and_plans(mode, halo, extra):
     _run_ranks(4, mode, halo, extra)
 
 
-def _run_ranks(n, mode, halo, extra):
+@pytest.mark.skipif(ngpus() < 2, reason="needs 2 GPUs")
+def test_two_gpus_cfg3_full_grid():
+    # the bench's cfg3 grid (512x512x64, F=50, 256 chunks) over 2 GPUs: GreedyLB
+    # re-places ~half the chunks over NVLink every epoch, most faces remote
+    _run_ranks(2, 5, "p2p", {}, shape="cfg3")
+
+
+def _run_ranks(n, mode, halo, extra, shape="small"):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
            "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.join(ROOT, "tools", "mgpu_check.py"), str(mode)]
+           os.path.join(ROOT, "tools", "mgpu_check.py"), str(mode), shape]
     env = dict(os.environ, OD_HALO=halo, **extra)
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-3000:]

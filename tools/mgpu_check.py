@@ -1,7 +1,10 @@
 """Multi-rank correctness check (run under torchrun, one rank per GPU):
 decomposed chunks over ranks, cross-rank halo exchange, greedy balancing every
 epoch with real chunk migration; each rank compares the chunks it owns at the
-end bitwise with the CPU field oracle.  Prints one JSON line per rank."""
+end bitwise with the CPU field oracle.  Prints one JSON line per rank.
+  torchrun --nproc-per-node N tools/mgpu_check.py MODE [small|cfg3]
+cfg3: the full 512x512x64, F=50 bench grid (256 chunks, moving hotspot, GreedyLB
+on N processors), two epochs."""
 import json
 import os
 import sys
@@ -23,18 +26,25 @@ from tests.gpu_util import oracle_fields  # noqa: E402
 mode = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 obj = [od.nccl_unique_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
-cfg = od.ExperimentConfig(
-    cluster=od.ClusterSpec(world, 2), domain=od.Domain(97, 61, 7, 3),
-    decomposition=od.Decomposition(od.DecompositionKind.TwoD, 5, 4),
-    window=od.MeasurementWindow(1, 1), epochs=1000, pattern=od.LoadPattern.UpperHalfHeavy,
-    advection=od.AdvectionSchedule(17, 2, 2),
-    policy=od.BalancePolicy(od.Strategy.Greedy, od.Strategy.RefineSwap, 1.0, 0.02),
-    seed=99, n_inner=9, overlap=mode)
+shape = sys.argv[2] if len(sys.argv) > 2 else "small"
+if shape == "cfg3":
+    from paper_1310_4218_b200 import configs  # noqa: E402
+    cfg = configs.cfg3(nodes=world, epochs=1000, overlap=mode)
+    n_epochs = 2
+else:
+    cfg = od.ExperimentConfig(
+        cluster=od.ClusterSpec(world, 2), domain=od.Domain(97, 61, 7, 3),
+        decomposition=od.Decomposition(od.DecompositionKind.TwoD, 5, 4),
+        window=od.MeasurementWindow(1, 1), epochs=1000, pattern=od.LoadPattern.UpperHalfHeavy,
+        advection=od.AdvectionSchedule(17, 2, 2),
+        policy=od.BalancePolicy(od.Strategy.Greedy, od.Strategy.RefineSwap, 1.0, 0.02),
+        seed=99, n_inner=9, overlap=mode)
+    n_epochs = 4
 eng = od.Engine(cfg, rank, world, local, obj[0])
-recs = [eng.run_epoch(e) for e in range(1, 5)]
+recs = [eng.run_epoch(e) for e in range(1, n_epochs + 1)]
 U, A, own = eng.gather_fields()
 st = eng.stats()
-Uo, Ao = oracle_fields(cfg, 8)
+Uo, Ao = oracle_fields(cfg, n_epochs * cfg.window.epoch_steps())
 ok_u = bool(np.array_equal(U[:, :, own], Uo[:, :, own]))
 ok_a = bool(np.array_equal(A[:, own], Ao[:, own]))
 maps = [r.mapping.assignment().tolist() for r in recs]
@@ -47,7 +57,7 @@ tot = [0] * world
 dist.all_gather_object(tot, owned)
 row = ({"rank": rank, "mode": mode, "fields_ok": ok_u and ok_a, "U_ok": ok_u,
                   "A_ok": ok_a, "consistent_plans": same, "owned_columns": owned,
-                  "all_columns_covered": sum(tot) == 97 * 61,
+                  "all_columns_covered": sum(tot) == cfg.domain.nx * cfg.domain.ny,
                   "moves": [len(r.plan.moves) for r in recs],
                   "halo_bytes": st["halo_bytes_sent"], "migrated_bytes": st["migrated_bytes"],
                   "imbalance": [[round(r.imbalance_before, 3), round(r.imbalance_after, 3)]
