@@ -311,6 +311,9 @@ class Runtime {
   std::vector<double*> peer_recv_;
   std::vector<double*> peer_slab_;  // every rank's chunk slab (IPC), for migration pulls
   bool peer_slabs_ok_ = false;
+  // column_step_ws: spread grids of at most one tile per SM (see launch_step)
+  static constexpr size_t kWsSpreadSmem = 150 * 1024;
+  bool ws_spread_ = true;
   std::vector<unsigned long long*> peer_flags_;
   double** d_peer_base_ = nullptr;
   unsigned long long** d_peer_flags_ = nullptr;
@@ -750,6 +753,13 @@ std::vector<int32_t> Runtime::classify() const {
 // One slab of equal chunk slots, sized at creation for the resident chunks plus
 // migration headroom (bounded by free HBM), so migrations do not cudaMalloc.
 void Runtime::init_slab() {
+  if (const char* e = std::getenv("OD_WS_SPREAD")) ws_spread_ = std::atoi(e) != 0;
+  if (ws_spread_) {
+    OD_CU(cudaFuncSetAttribute(column_step_ws<kFusedPrefetch, true, kWsMinBlocks>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWsSpreadSmem)));
+    OD_CU(cudaFuncSetAttribute(column_step_ws<kFusedPrefetch, false, kWsMinBlocks>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, int(kWsSpreadSmem)));
+  }
   for (const Sub& sb : subs_) {
     const size_t plane = size_t(sb.h()) * ((sb.w() + 15) / 16 * 16);
     const size_t b = (2 * plane * cfg_.nz * cfg_.fields + plane * cfg_.nz) * sizeof(double);
@@ -1625,6 +1635,12 @@ void Runtime::launch_step(int32_t mode, int32_t epoch_step, bool host_io,
     if (use_ws()) {
       // warp-specialised tiles (column_step_ws): physics and Jacobi warps
       lc.blockDim = dim3(32, 2 * kRowWarps);
+      // a grid that fits the GPU one tile per SM is spread one per SM: unused
+      // dynamic shared memory caps the kernel at one CTA per SM, so no two
+      // tiles' serial physics chains share an SM's FP64 pipe (the block
+      // scheduler packs small grids onto fewer SMs otherwise; 128 heavy tiles:
+      // 1.95 -> 1.71 ms per step).  OD_WS_SPREAD=0 turns it off.
+      if (ws_spread_ && nt + pk.ctas <= sms_) lc.dynamicSmemBytes = kWsSpreadSmem;
       if (timer)
         OD_CU(cudaLaunchKernelEx(&lc, column_step_ws<kFusedPrefetch, true, kWsMinBlocks>, chk,
                                  tl4, cfg_.nz, cfg_.fields, cfield, cfg_.nx, cfg_.ny, shift,
